@@ -1,0 +1,224 @@
+/*
+ * ogcp_b200 -- B200-native (sm_100a) engine for the OnlineGCP per-slice solve.
+ *
+ * C ABI: plain pointers and sizes, no torch types.  Device pointers are raw
+ * CUDA device addresses owned by the caller unless stated otherwise; the
+ * context owns only scratch.  Every call is enqueued on the context's CUDA
+ * stream; calls that return scalars or status synchronize that stream.
+ *
+ * The reference (pkg/src/ogcp, pure Python/numpy) has no FFI: these entry
+ * points replace its Python functions one for one, and the Python package
+ * paper_2110_14514_b200 re-exports the reference names on top of them (see
+ * INTEGRATION.md for the ctypes binding).  Each declaration cites the
+ * reference interface it replaces.
+ *
+ * Status codes mirror the reference exception hierarchy (exceptions.py:7-20,
+ * CLI exit codes cli.py:420-425): DataError=3, DivergenceError=4,
+ * SamplingError=5 (a DataError subclass in Python).
+ */
+#ifndef OGCP_B200_H
+#define OGCP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OGCP_ABI_VERSION 1
+
+enum {
+  OGCP_OK = 0,
+  OGCP_E_INTERNAL = 1,
+  OGCP_E_USAGE = 2,
+  OGCP_E_DATA = 3,        /* exceptions.py:11 DataError */
+  OGCP_E_DIVERGENCE = 4,  /* exceptions.py:19 DivergenceError */
+  OGCP_E_SAMPLING = 5,    /* exceptions.py:15 SamplingError (subclass of DataError) */
+  OGCP_E_CUDA = 6
+};
+
+/* losses.py:24 KINDS */
+enum { OGCP_GAUSSIAN = 0, OGCP_POISSON = 1, OGCP_BERNOULLI = 2,
+       /* gradient-tensor mode: y = x (apply MTTKRP to a given sparse tensor Y,
+        * kernels.py:33-72); no model evaluation, no domain checks */
+       OGCP_IDENTITY = 3 };
+
+typedef struct ogcp_ctx ogcp_ctx;      /* one per (stream, device); owns scratch, not thread-safe */
+typedef struct ogcp_slice ogcp_slice;  /* a device-resident validated COO slice + membership hash */
+
+/* losses.py:27-38 LossFunction(kind, eps) */
+typedef struct {
+  int32_t kind;
+  double eps;
+} ogcp_loss;
+
+/* sampling.py:45-54 SamplerConfig; a count < 0 means None ("all" nonzeros);
+ * max_rejects < 0 means None (1000*q at draw time). */
+typedef struct {
+  int64_t grad_nonzeros;
+  int64_t grad_zeros;
+  int64_t obj_nonzeros;
+  int64_t obj_zeros;
+  uint64_t seed;
+  int64_t max_rejects;
+} ogcp_sampler_config;
+
+/* solvers.py:40-69 SolverConfig (gradient_mode "sampled", temporal_solver "sgd");
+ * lower_bound is already resolved against the loss (solvers.py:86-87). */
+typedef struct {
+  double tol_weights, tol_factors;
+  int32_t max_epochs_weights, max_epochs_factors;
+  int32_t iters_weights, iters_factors;
+  double reg_factors, reg_weights, hist_weight, hist_decay;
+  int32_t warm_start_weights;
+  double rate_weights, rate_factors, beta1, beta2, adam_eps, rate_decay;
+  double lower_bound;
+  ogcp_sampler_config samples;
+} ogcp_solver_config;
+
+/* A CP model bound to caller-owned device buffers.  factors[k] is a row-major
+ * dims[k] x ldr float32 matrix whose first `rank` columns are the factor and
+ * whose padding columns are zero (ldr is a multiple of 4, see ogcp_padded_rank). */
+typedef struct {
+  int32_t ndim;
+  int32_t rank;
+  int32_t ldr;
+  const int64_t* dims;     /* host, [ndim] */
+  float* const* factors;   /* host array of ndim device pointers */
+} ogcp_model;
+
+/* Persistent factor Adam (adam.py:20-109): device buffers shaped like the
+ * factors; rate is read and written back (rejections decay it). */
+typedef struct {
+  float* const* u;
+  float* const* v;
+  float* const* u_o;
+  float* const* v_o;
+  float* const* a_o;
+  double rate;
+} ogcp_adam_state;
+
+/* solvers.py:94-100 EpochTrace; objective[] must hold max_epochs+1 doubles. */
+typedef struct {
+  double* objective;
+  int32_t n_objective;
+  int32_t epochs;
+  int32_t rejections;
+} ogcp_trace;
+
+/* ------------------------------------------------------------------ misc */
+int ogcp_abi_version(void);
+/* Message of the last failing call on this thread (empty if none). */
+const char* ogcp_last_error(void);
+/* Padded row stride the kernels require for a given rank. */
+int32_t ogcp_padded_rank(int32_t rank);
+
+/* Keyed generator state, sampling.py:39-42 rng_at(seed, *key): the PCG64 state
+ * and increment as {state_hi, state_lo, inc_hi, inc_lo}.  Host only. */
+int ogcp_rng_state(uint64_t seed, const int64_t* key, int32_t nkey, uint64_t out[4]);
+/* Host restatement of Generator.integers(0, highs[j % nhigh]) for n draws on the
+ * keyed stream (sampling.py:125, 138; streaming.py:51).  Host only. */
+int ogcp_rng_integers(uint64_t seed, const int64_t* key, int32_t nkey, const int64_t* highs,
+                      int32_t nhigh, int64_t n, int64_t* out);
+
+/* --------------------------------------------------------------- context */
+int ogcp_ctx_create(int32_t device, void* cuda_stream, ogcp_ctx** out);
+int ogcp_ctx_destroy(ogcp_ctx* ctx);
+int ogcp_ctx_set_stream(ogcp_ctx* ctx, void* cuda_stream);
+/* Number of kernels this context has launched so far. */
+int64_t ogcp_ctx_launches(const ogcp_ctx* ctx);
+
+/* ----------------------------------------------------------------- slice */
+/* SparseTensor.from_zero_based (tensor.py:75-119): validates bounds,
+ * finiteness, stored zeros (unless allow_zero) and duplicates with the
+ * reference's messages, then builds the AoS records and the membership hash.
+ * subs0_dev: int64 [nnz x ndim] row-major, vals_dev: float64 [nnz]. */
+int ogcp_slice_create(ogcp_ctx* ctx, int32_t ndim, const int64_t* dims, int64_t nnz,
+                      const int64_t* subs0_dev, const double* vals_dev, int32_t allow_zero,
+                      ogcp_slice** out);
+/* Same from int32 coordinates and float32 values (device generators). */
+int ogcp_slice_create_i32(ogcp_ctx* ctx, int32_t ndim, const int64_t* dims, int64_t nnz,
+                          const int32_t* subs0_dev, const float* vals_dev, int32_t allow_zero,
+                          ogcp_slice** out);
+int ogcp_slice_destroy(ogcp_slice* s);
+/* nnz (eta), num_cells (omega, as double and exact int64 when < 2^63),
+ * frobenius_sq (tensor.py:138-141). */
+int ogcp_slice_info(const ogcp_slice* s, int64_t* nnz, int64_t* omega, double* frobenius_sq);
+/* SparseTensor.contains_linear (tensor.py:163-169) for device coords [n x ndim] int64. */
+int ogcp_slice_contains(ogcp_ctx* ctx, const ogcp_slice* s, const int64_t* subs0_dev, int64_t n,
+                        uint8_t* hit_dev);
+
+/* --------------------------------------------------------------- sampler */
+/* draw_samples (sampling.py:108-153) on rng_at(seed, *key): bit-exact nonzero
+ * ordinals [p] and zero coordinates [q x ndim] (int32, device). */
+int ogcp_draw_samples(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const int64_t* key,
+                      int32_t nkey, int64_t p, int64_t q, int64_t max_rejects,
+                      int32_t* ordinals_dev, int32_t* zero_subs_dev);
+
+/* ------------------------------------------------------------- estimators */
+/* Data part of factor_gradients (solvers.py:139-140 = sampled_mttkrp(Y,k)*s,
+ * kernels.py:33-56) and weight_gradient_mttkrp (kernels.py:59-72) for the
+ * sampled gradient tensor Y of sampled_gradient_tensor (sampling.py:209-239),
+ * given the replayed sample set.  grads_dev (nullable) receives per-mode
+ * dims[k] x ldr float32; gw_dev (nullable) receives rank float64. */
+int ogcp_sampled_gradient(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev,
+                          int64_t p, const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m,
+                          const double* weights, const ogcp_loss* loss, float* const* grads_dev,
+                          double* gw_dev);
+
+/* Full factor_gradients (solvers.py:127-142, 159-179): data term + lambda*A
+ * + history Gram term.  old_factors may be NULL when H == 0 or hist_weight == 0.
+ * window_s is host [H x rank] float64, window_ids host [H]. */
+int ogcp_factor_gradients(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev,
+                          int64_t p, const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m,
+                          float* const* old_factors, const double* weights, const ogcp_loss* loss,
+                          const double* window_s, const int64_t* window_ids, int32_t H,
+                          double hist_weight, double hist_decay, int64_t t, double reg_factors,
+                          float* const* grads_dev);
+
+/* estimate_objective (sampling.py:177-206) on a replayed sample set. */
+int ogcp_estimate_objective(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev,
+                            int64_t p, const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m,
+                            float* const* old_factors, const double* weights, const ogcp_loss* loss,
+                            const double* window_s, const int64_t* window_ids, int32_t H,
+                            double hist_weight, double hist_decay, int64_t t, double reg_factors,
+                            double reg_weights, double* out);
+
+/* gram (kernels.py:75-98): hadamard over modes != skip of B_m' A_m, B = other
+ * (nullable -> A).  skip < 0 means all modes.  out: host [rank x rank] float64. */
+int ogcp_gram(ogcp_ctx* ctx, const ogcp_model* m, float* const* other, int32_t skip, double* out);
+
+/* Adam.step (adam.py:51-81) on device buffers shaped like the model. */
+int ogcp_adam_step(ogcp_ctx* ctx, const ogcp_model* m, float* const* grads, ogcp_adam_state* st,
+                   double beta1, double beta2, double eps, double lower_bound, int64_t step_count);
+/* Adam.update (adam.py:83-94): accept snapshots, reject restores + decays rate. */
+int ogcp_adam_update(ogcp_ctx* ctx, const ogcp_model* m, ogcp_adam_state* st, int32_t passed,
+                     double rate_decay);
+
+/* ---------------------------------------------------------------- solves */
+/* solve_weights (solvers.py:197-268): temporal-row GCP-SGD with the factors
+ * fixed; s_init host [rank] (nullable), s_out host [rank]. */
+int ogcp_solve_weights(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_config* cfg,
+                       const ogcp_loss* loss, int64_t t, const ogcp_model* m,
+                       const double* s_init, double* s_out, ogcp_trace* trace);
+
+/* solve_factors (solvers.py:290-368): factor GCP-SGD with the weights fixed,
+ * persistent Adam and counter.  m->factors are updated in place. */
+int ogcp_solve_factors(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_config* cfg,
+                       const ogcp_loss* loss, int64_t t, const ogcp_model* m,
+                       float* const* old_factors, const double* weights, const double* window_s,
+                       const int64_t* window_ids, int32_t H, ogcp_adam_state* adam,
+                       int64_t* iteration, ogcp_trace* trace);
+
+/* local_loss (metrics.py:36-70): mode 0 exact (every cell, <= max_elements),
+ * mode 1 sampled on rng_at(seed, *key) with (p, q) (p < 0: all nonzeros).
+ * Returns the loss total divided by ||X||^2 when that is > 0; *normalized says which. */
+int ogcp_local_loss(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m, const double* weights,
+                    const ogcp_loss* loss, int32_t mode, int64_t p, int64_t q, uint64_t seed,
+                    const int64_t* key, int32_t nkey, int64_t max_rejects, int64_t max_elements,
+                    double* out, int32_t* normalized);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OGCP_B200_H */

@@ -1,0 +1,121 @@
+// Internal engine structures shared by the kernels and the host runtime.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ogcp_b200.h"
+#include "pcg64.cuh"
+
+namespace ogcp {
+
+constexpr int kMaxModes = 8;
+constexpr int kNumSMs = 148;
+
+// Engine error carrying the ABI status code (mirrors exceptions.py).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define OGCP_CUDA(call)                                                                \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::ogcp::Error(OGCP_E_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                           " at " __FILE__ ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+// Device buffer owned by the engine (slices, scratch).
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  // Grow-only; contents are not preserved.
+  void* ensure(size_t b) {
+    if (b <= bytes && ptr) return ptr;
+    release();
+    size_t nb = b < 256 ? 256 : b;
+    OGCP_CUDA(cudaMalloc(&ptr, nb));
+    bytes = nb;
+    return ptr;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(ptr); }
+};
+
+// Record layout of one stored nonzero in HBM: ndim int32 coordinates followed
+// by the float32 value, padded to 16 B (ndim <= 3) or 32 B (ndim <= 7).
+inline int record_ints(int ndim) { return ndim + 1 <= 4 ? 4 : 8; }
+
+// Device-side error/event word.  Codes are event*4 + sub with sub 0 = draw,
+// 1 = loss-domain check, 2 = non-finite iterate, so the smallest code is the
+// error the reference would have raised first (solvers.py:243-254, 337-355).
+struct DevFlags {
+  long long first_code[4];   // [0] sampling error, [1] data error, [2] divergence, [3] shortfall
+  unsigned int data_bits;    // bit0 non-finite m, bit1 m < 0
+  unsigned int pad;
+};
+
+enum : int { kFlagSampling = 0, kFlagData = 1, kFlagDiverge = 2, kFlagShortfall = 3 };
+constexpr long long kNoEvent = 0x7fffffffffffffffLL;
+
+struct Slice {
+  int ndim = 0;
+  int64_t dims[kMaxModes] = {0};
+  int64_t nnz = 0;
+  bool omega_fits = true;   // omega < 2^63
+  int64_t omega = 0;
+  double omega_d = 0;
+  double frob_sq = 0;
+  bool x_negative = false;  // any stored value < 0   (poisson domain, losses.py:52)
+  bool x_nonbinary = false; // any stored value not in {0,1} (losses.py:54)
+  int rec_ints = 4;
+  DevBuf records;           // nnz * rec_ints int32
+  DevBuf hash;              // table_size uint64 linear keys, ~0 = empty
+  uint64_t table_mask = 0;
+  uint64_t strides[kMaxModes] = {0};
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  double slack = 1.0;           // sampler over-provisioning multiplier (grows on shortfall)
+  // scratch
+  DevBuf flags;                 // DevFlags
+  DevBuf draw_a, draw_b, draw_c, draw_d, draw_e;   // sampler scratch
+  DevBuf scalars;               // small device scalars (int64 x 16)
+  DevBuf partials;              // reduction partials (double)
+  DevBuf gram;                  // gram scratch
+  DevBuf hist;                  // history coefficient matrices
+  DevBuf wsolve;                // weight-solve state
+  DevBuf grads;                 // factor-gradient buffers
+  DevBuf grad_ord, grad_zero;   // gradient sample set
+  DevBuf obj_ord, obj_zero;     // objective sample set
+  DevBuf window;                // window matrix / vectors
+  DevBuf pinned_dummy;
+  double* host_scalars = nullptr;  // pinned host mirror
+  DevFlags* host_flags = nullptr;  // pinned
+  void count(int n = 1) { launches += n; }
+};
+
+inline void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(OGCP_E_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+}
+
+inline int ceil_div_i(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace ogcp

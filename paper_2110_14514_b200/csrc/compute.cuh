@@ -1,0 +1,71 @@
+#pragma once
+#include "common.cuh"
+
+namespace ogcp {
+
+// One sample set on the device: p nonzero ordinals into the slice records and
+// q zero coordinates (int32 [q x ndim]); scales per sampling.py:99-105.
+struct SamplesP {
+  const int32_t* ord;
+  int64_t p;
+  const int32_t* zsub;
+  int64_t q;
+  const int* rec;
+  int rec_ints;
+  double nz_scale, zero_scale;
+};
+
+struct GradPtrs {
+  float* g[kMaxModes];
+};
+
+struct ModelP {
+  const float* A[kMaxModes];
+  int ndim, rank, ldr;
+  int64_t dims[kMaxModes];
+};
+
+struct LossP {
+  int kind;
+  float eps;
+  double eps_d;
+};
+
+// K2+K3: data term of every factor gradient, grads[k] = mttkrp(Y,k)*diag(s)
+// (zeroed and written).  s_f: float [ldr] weights (padding zero).
+void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                   float* const* grads, long long code);
+// K2 (weight solve): per-block partial sums of Z'vec(Y) into partials [nblk x ldr] double.
+int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                  double* partials, long long code);
+// K6: per-block partial sums of scale*f(x,m) into partials; returns the block count.
+int objective_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                      double* partials, long long code);
+// Sum nblk partial vectors of length len (fixed order) into out.
+void sum_partials_enqueue(Ctx* ctx, const double* partials, int nblk, int len, double* out);
+// K4: out[R x R] = B' A over rows (fp64 accumulation), A/B rows x ldr.
+void gram_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* out,
+                  DevBuf& scratch);
+// History coefficients: Mk = w*(hadamard_{m!=k} P_m) o S, Nk = w*(hadamard_{m!=k} C_m) o S  (float [d][R][R]).
+void hist_coeffs_enqueue(Ctx* ctx, int ndim, int rank, const double* P, const double* C, const double* S,
+                         double w, float* Mk, float* Nk);
+// K5: g = G + lambda*A + (A Mk - Aold Nk) ; Adam ; clamp ; isfinite  (one mode).
+void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, const float* Aold,
+                           const float* G, float* u, float* v, const float* Mk, const float* Nk,
+                           double reg, double rate_i, double beta1, double beta2, double eps, double lower,
+                           long long code);
+// Weight solve step: g = sum(partials) + mu*s ; Adam on the R-vector (double) ; s_f refresh.
+void weight_step_enqueue(Ctx* ctx, const double* partials, int nblk, int rank, int ldr, double* wstate,
+                         float* s_f, double mu, double rate_i, double beta1, double beta2, double eps,
+                         double lower, long long code);
+// Objective finalisation on device: data partials + window quad forms + regularizers.
+void hist_penalty_enqueue(Ctx* ctx, int ndim, int rank, const double* Poo, const double* Pon,
+                          const double* Pnn, const double* window_s, const double* window_coef, int H,
+                          double* out);
+// Exact loss over every cell (metrics.py:50-57) : partial sums.
+int exact_cells_enqueue(Ctx* ctx, const ModelP& M, const float* s_f, const LossP& L, int64_t omega,
+                        double* partials, long long code);
+int exact_nz_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                     double* partials, long long code);
+
+}  // namespace ogcp

@@ -1,0 +1,995 @@
+// Native runtime of the engine: context, slices, the per-slice solvers and
+// the extern "C" boundary declared in include/ogcp_b200.h.
+//
+// The solver loops (solve_weights solvers.py:197-268, solve_factors
+// solvers.py:290-368) run on the host and enqueue every iteration on the
+// context stream without synchronising; the host synchronises once per epoch
+// to read the objective estimate and the device error word, then applies the
+// reference gate (fest > fest_old rejects, ties accept) with the reference's
+// Adam accept/reject semantics (adam.py:83-94).
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "common.cuh"
+#include "compute.cuh"
+#include "sampler.cuh"
+
+namespace ogcp {
+
+template <class CT, class VT>
+Slice* slice_create_impl(Ctx* ctx, int ndim, const int64_t* dims, int64_t nnz, const CT* subs, const VT* vals,
+                         int allow_zero);
+void slice_contains_impl(Ctx* ctx, const Slice* s, const int64_t* subs, int64_t n, uint8_t* hit);
+
+static thread_local std::string g_last_error;
+
+static const char* kind_name(int k) {
+  return k == OGCP_GAUSSIAN ? "gaussian" : (k == OGCP_POISSON ? "poisson" : "bernoulli");
+}
+
+// --------------------------------------------------------------------- flags
+static void reset_flags(Ctx* ctx) {
+  DevFlags f;
+  for (int i = 0; i < 4; ++i) f.first_code[i] = kNoEvent;
+  f.data_bits = 0;
+  f.pad = 0;
+  *ctx->host_flags = f;
+  OGCP_CUDA(cudaMemcpyAsync(ctx->flags.ptr, ctx->host_flags, sizeof(DevFlags), cudaMemcpyHostToDevice, ctx->stream));
+}
+
+static void fetch_flags(Ctx* ctx) {
+  OGCP_CUDA(cudaMemcpyAsync(ctx->host_flags, ctx->flags.ptr, sizeof(DevFlags), cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+struct DrawCtx {
+  const Slice* X;
+  double budget_q_mult = 1000.0;
+};
+
+static std::string fmt_g4(double v) {
+  char buf[64];
+  snprintf(buf, sizeof(buf), "%.4g", v);
+  return buf;
+}
+
+static int64_t budget_of(int64_t q, int64_t max_rejects) {
+  return max_rejects < 0 ? (q ? 1000 * q : 0) : max_rejects;
+}
+
+static void precheck_draw(const Slice* X, int64_t p, int64_t q) {
+  if (p > 0 && X->nnz == 0) throw Error(OGCP_E_SAMPLING, "cannot draw nonzero samples: slice has no nonzeros");
+  if (q > 0 && X->omega == X->nnz) throw Error(OGCP_E_SAMPLING, "cannot draw zero samples: tensor has no zeros");
+}
+
+// Outcome of an enqueued batch of events, read after a synchronisation.
+// Returns 0 (clean), 1 (shortfall: redo with more candidates) or throws.
+static int check_flags(Ctx* ctx, const Slice* X, int kind, int64_t budget, const std::string& what, int64_t t) {
+  const DevFlags& f = *ctx->host_flags;
+  long long e_min = kNoEvent;
+  int which = -1;
+  for (int i = 0; i < 3; ++i)
+    if (f.first_code[i] < e_min) { e_min = f.first_code[i]; which = i; }
+  if (f.first_code[kFlagShortfall] <= e_min && f.first_code[kFlagShortfall] != kNoEvent) return 1;
+  if (which < 0) return 0;
+  if (which == kFlagSampling)
+    throw Error(OGCP_E_SAMPLING, "zero sampling exhausted " + std::to_string(budget) +
+                                     " rejects; nonzero density is " + fmt_g4((double)X->nnz / X->omega_d) +
+                                     ", set the zero sample count to 0 for dense data");
+  if (which == kFlagData) {
+    if (f.data_bits & 1u) throw Error(OGCP_E_DATA, std::string(kind_name(kind)) + " loss: non-finite input");
+    throw Error(OGCP_E_DATA, std::string(kind_name(kind)) + " loss requires m >= 0");
+  }
+  throw Error(OGCP_E_DIVERGENCE,
+              what + " produced non-finite values at slice " + std::to_string(t) + "; lower the learning rate");
+}
+
+static void x_domain_check(const Slice* X, int kind) {
+  if (kind == OGCP_IDENTITY) return;
+  if (kind == OGCP_POISSON && X->x_negative) throw Error(OGCP_E_DATA, "poisson loss requires x >= 0");
+  if (kind == OGCP_BERNOULLI && X->x_nonbinary) throw Error(OGCP_E_DATA, "bernoulli loss requires x in {0, 1}");
+}
+
+// ------------------------------------------------------------- model helpers
+static ModelP model_of(const ogcp_model* m) {
+  if (!m || m->ndim < 1 || m->ndim > 7) throw Error(OGCP_E_USAGE, "model must have 1..7 modes");
+  if (m->rank < 1) throw Error(OGCP_E_USAGE, "rank must be >= 1");
+  if (m->ldr != ogcp_padded_rank(m->rank))
+    throw Error(OGCP_E_USAGE, "model ldr must equal ogcp_padded_rank(rank)");
+  ModelP M;
+  M.ndim = m->ndim;
+  M.rank = m->rank;
+  M.ldr = m->ldr;
+  for (int k = 0; k < kMaxModes; ++k) {
+    M.A[k] = k < m->ndim ? m->factors[k] : nullptr;
+    M.dims[k] = k < m->ndim ? m->dims[k] : 1;
+  }
+  return M;
+}
+
+static void check_model_slice(const ModelP& M, const Slice* X) {
+  if (M.ndim != X->ndim)
+    throw Error(OGCP_E_DATA, "tensor has " + std::to_string(X->ndim) + " modes but " + std::to_string(M.ndim) +
+                                 " factors given");
+  for (int k = 0; k < M.ndim; ++k)
+    if (M.dims[k] != X->dims[k])
+      throw Error(OGCP_E_DATA, "factor " + std::to_string(k) + " has " + std::to_string(M.dims[k]) +
+                                   " rows, tensor dim is " + std::to_string(X->dims[k]));
+}
+
+static LossP loss_of(const ogcp_loss* l) {
+  if (!l || l->kind < 0 || l->kind > 3) throw Error(OGCP_E_DATA, "unknown loss kind");
+  if (!(l->eps > 0)) throw Error(OGCP_E_DATA, "eps must be positive");
+  LossP L;
+  L.kind = l->kind;
+  L.eps = (float)l->eps;
+  L.eps_d = l->eps;
+  return L;
+}
+
+static SamplesP samples_of(const Slice* X, const int32_t* ord, int64_t p, const int32_t* z, int64_t q) {
+  SamplesP S;
+  S.ord = ord;
+  S.p = p;
+  S.zsub = z;
+  S.q = q;
+  S.rec = X->records.as<int>();
+  S.rec_ints = X->rec_ints;
+  S.nz_scale = p ? (double)X->nnz / (double)p : 0.0;
+  S.zero_scale = q ? (X->omega_d - (double)X->nnz) / (double)q : 0.0;
+  if (X->omega_fits && q) S.zero_scale = (double)(X->omega - X->nnz) / (double)q;
+  return S;
+}
+
+static void upload_weights(Ctx* ctx, const double* w, int rank, int ldr, float* s_f) {
+  std::vector<float> h(ldr, 0.0f);
+  for (int r = 0; r < rank; ++r) h[r] = (float)w[r];
+  OGCP_CUDA(cudaMemcpyAsync(s_f, h.data(), ldr * 4, cudaMemcpyHostToDevice, ctx->stream));
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// resolve_counts (sampling.py:71-77)
+static void resolve_counts(int64_t nonzeros, int64_t zeros, const Slice* X, int64_t* p, int64_t* q) {
+  *p = nonzeros < 0 ? X->nnz : nonzeros;
+  if (X->nnz == 0) *p = 0;
+  *q = zeros;
+}
+
+struct SampleBufs {
+  DevBuf ord, zero;
+  DrawScratch scr;
+  int64_t p = 0, q = 0;
+  void size(int64_t p_, int64_t q_, int ndim) {
+    p = p_;
+    q = q_;
+    ord.ensure((size_t)std::max<int64_t>(p, 1) * 4);
+    zero.ensure((size_t)std::max<int64_t>(q, 1) * ndim * 4);
+  }
+};
+
+// Synchronous draw with shortfall retry (used for objective sets).
+static void draw_sync(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t max_rejects,
+                      SampleBufs& b) {
+  precheck_draw(X, p, q);
+  b.size(p, q, X->ndim);
+  const int64_t budget = budget_of(q, max_rejects);
+  for (int attempt = 0;; ++attempt) {
+    reset_flags(ctx);
+    draw_enqueue(ctx, X, g, p, q, budget, b.ord.as<int32_t>(), b.zero.as<int32_t>(), 0, b.scr);
+    fetch_flags(ctx);
+    OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+    int r = check_flags(ctx, X, OGCP_GAUSSIAN, budget, "draw", 0);
+    if (r == 0) break;
+    ctx->slack *= 4.0;
+    if (attempt > 8) throw Error(OGCP_E_INTERNAL, "sampler could not provision enough candidates");
+  }
+}
+
+static Pcg64 keyed(uint64_t seed, std::initializer_list<int64_t> key) {
+  uint64_t k[8];
+  int n = 0;
+  for (int64_t v : key) k[n++] = (uint64_t)v;
+  return seedseq_pcg64(seed, k, n);
+}
+
+// Grams for history/regularisation: per mode P_m = A_m'A_m, C_m = Aold_m'A_m.
+struct HistBufs {
+  DevBuf P, C, Poo, S, Ws, coef, out, Mk, Nk, scratch, part, tmp;
+};
+
+static void grams_enqueue(Ctx* ctx, const ModelP& M, float* const* other, double* out_per_mode, HistBufs& hb,
+                          bool self) {
+  const int RR = M.rank * M.rank;
+  for (int k = 0; k < M.ndim; ++k) {
+    const float* A = M.A[k];
+    const float* B = self ? M.A[k] : other[k];
+    gram_enqueue(ctx, A, B, M.dims[k], M.rank, M.ldr, out_per_mode + (int64_t)k * RR, hb.scratch);
+  }
+}
+
+// Device objective for a fixed sample set: returns data term + history + regs.
+struct ObjectiveParts {
+  double data = 0, hist = 0, trace = 0;
+};
+
+static long long code_of(long long ev, int sub) { return ev * 4 + sub; }
+
+// ============================================================= solve_weights
+static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config* cfg, const ogcp_loss* loss,
+                               int64_t t, const ogcp_model* mdl, const double* s_init, double* s_out,
+                               ogcp_trace* trace) {
+  ModelP M = model_of(mdl);
+  check_model_slice(M, X);
+  LossP L = loss_of(loss);
+  const int R = M.rank, ldr = M.ldr;
+  const uint64_t seed = cfg->samples.seed;
+  cudaStream_t st = ctx->stream;
+  // state: s u v s_o u_o v_o (double ldr each) + s_f float ldr
+  ctx->wsolve.ensure((size_t)ldr * (6 * 8 + 4));
+  double* ws = ctx->wsolve.as<double>();
+  float* s_f = reinterpret_cast<float*>(ws + 6 * ldr);
+  std::vector<double> h(6 * ldr, 0.0);
+  std::vector<double> s(R, 0.0);
+  if (cfg->warm_start_weights && s_init)
+    for (int r = 0; r < R; ++r) s[r] = s_init[r];
+  for (int r = 0; r < R; ++r) {
+    h[r] = s[r];
+    h[3 * ldr + r] = s[r];  // snapshot of the entry state (solvers.py:217-218)
+  }
+  OGCP_CUDA(cudaMemcpyAsync(ws, h.data(), 6 * ldr * 8, cudaMemcpyHostToDevice, st));
+  upload_weights(ctx, s.data(), R, ldr, s_f);
+  double rate = cfg->rate_weights;
+
+  int64_t po, qo, p, q;
+  resolve_counts(cfg->samples.obj_nonzeros, cfg->samples.obj_zeros, X, &po, &qo);
+  resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
+  if (po > 0 || p > 0) x_domain_check(X, L.kind);
+  static thread_local SampleBufs obj, grad;
+  draw_sync(ctx, X, keyed(seed, {t, 2}), po, qo, cfg->samples.max_rejects, obj);
+  SamplesP So = samples_of(X, obj.ord.as<int32_t>(), po, obj.zero.as<int32_t>(), qo);
+  precheck_draw(X, p, q);
+  grad.size(p, q, X->ndim);
+  const int64_t budget = budget_of(q, cfg->samples.max_rejects);
+  ctx->partials.ensure((size_t)kNumSMs * 8 * ldr * 8 + 64);
+  double* part = ctx->partials.as<double>();
+  ctx->scalars.ensure(64 * 8);
+  double* dsc = ctx->scalars.as<double>();
+  double* hsc = ctx->host_scalars;
+
+  long long ev = 1;
+  auto fest_fn = [&]() -> double {
+    reset_flags(ctx);
+    const long long c = code_of(ev++, 1);
+    int nb = objective_enqueue(ctx, So, M, s_f, L, part, c);
+    sum_partials_enqueue(ctx, part, nb, 1, dsc);
+    OGCP_CUDA(cudaMemcpyAsync(hsc, dsc, 8, cudaMemcpyDeviceToHost, st));
+    OGCP_CUDA(cudaMemcpyAsync(hsc + 8, ws, R * 8, cudaMemcpyDeviceToHost, st));
+    fetch_flags(ctx);
+    OGCP_CUDA(cudaStreamSynchronize(st));
+    check_flags(ctx, X, L.kind, budget, "temporal weight solve", t);
+    double val = hsc[0];
+    if (cfg->reg_weights) {
+      double ss = 0.0;
+      for (int r = 0; r < R; ++r) ss += hsc[8 + r] * hsc[8 + r];
+      val += 0.5 * cfg->reg_weights * ss;
+    }
+    return val;
+  };
+
+  double fest = fest_fn();
+  std::vector<double> objv{fest};
+  int64_t i = 0;
+  int epochs = 0, rejections = 0;
+  for (int epoch = 0; epoch < cfg->max_epochs_weights; ++epoch) {
+    if (!(fest > cfg->tol_weights)) break;
+    const double fold = fest;
+    for (int attempt = 0;; ++attempt) {
+      reset_flags(ctx);
+      const long long ev0 = ev;
+      for (int it = 0; it < cfg->iters_weights; ++it) {
+        const long long e = ev++;
+        draw_enqueue(ctx, X, keyed(seed, {t, 1, epoch, it}), p, q, budget, grad.ord.as<int32_t>(),
+                     grad.zero.as<int32_t>(), code_of(e, 0), grad.scr);
+        SamplesP Sg = samples_of(X, grad.ord.as<int32_t>(), p, grad.zero.as<int32_t>(), q);
+        int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1));
+        const int64_t cnt = i + it + 1;
+        const double rate_i = rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
+                              (1.0 - std::pow(cfg->beta1, (double)cnt));
+        weight_step_enqueue(ctx, part, nb, R, ldr, ws, s_f, cfg->reg_weights, rate_i, cfg->beta1, cfg->beta2,
+                            cfg->adam_eps, cfg->lower_bound, code_of(e, 2));
+      }
+      fetch_flags(ctx);
+      OGCP_CUDA(cudaStreamSynchronize(st));
+      int r = check_flags(ctx, X, L.kind, budget, "temporal weight solve", t);
+      if (r == 0) break;
+      // shortfall: restore the epoch-start snapshot and redo with more candidates
+      ctx->slack *= 4.0;
+      OGCP_CUDA(cudaMemcpyAsync(ws, ws + 3 * ldr, 3 * ldr * 8, cudaMemcpyDeviceToDevice, st));
+      OGCP_CUDA(cudaMemcpyAsync(hsc, ws, ldr * 8, cudaMemcpyDeviceToHost, st));
+      OGCP_CUDA(cudaStreamSynchronize(st));
+      upload_weights(ctx, hsc, R, ldr, s_f);
+      ev = ev0;
+      if (attempt > 8) throw Error(OGCP_E_INTERNAL, "sampler could not provision enough candidates");
+    }
+    i += cfg->iters_weights;
+    fest = fest_fn();
+    if (!std::isfinite(fest))
+      throw Error(OGCP_E_DIVERGENCE, "temporal weight solve diverged at slice " + std::to_string(t));
+    if (fest > fold) {
+      // reject: restore u, v, s and decay the rate (adam.py:91-94)
+      OGCP_CUDA(cudaMemcpyAsync(ws, ws + 3 * ldr, 3 * ldr * 8, cudaMemcpyDeviceToDevice, st));
+      rate *= cfg->rate_decay;
+      fest = fold;
+      i -= cfg->iters_weights;
+      ++rejections;
+    } else {
+      OGCP_CUDA(cudaMemcpyAsync(ws + 3 * ldr, ws, 3 * ldr * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    OGCP_CUDA(cudaMemcpyAsync(hsc, ws, ldr * 8, cudaMemcpyDeviceToHost, st));
+    OGCP_CUDA(cudaStreamSynchronize(st));
+    upload_weights(ctx, hsc, R, ldr, s_f);
+    ++epochs;
+    objv.push_back(fest);
+  }
+  OGCP_CUDA(cudaMemcpyAsync(hsc, ws, ldr * 8, cudaMemcpyDeviceToHost, st));
+  OGCP_CUDA(cudaStreamSynchronize(st));
+  for (int r = 0; r < R; ++r) s_out[r] = hsc[r];
+  if (trace) {
+    trace->n_objective = 0;
+    for (size_t j = 0; j < objv.size() && (int)j <= cfg->max_epochs_weights; ++j)
+      trace->objective[trace->n_objective++] = objv[j];
+    trace->epochs = epochs;
+    trace->rejections = rejections;
+  }
+}
+
+// ============================================================= solve_factors
+struct FactorWork {
+  DevBuf grads;
+  HistBufs hb;
+  SampleBufs obj, grad;
+};
+
+static void window_upload(Ctx* ctx, HistBufs& hb, int R, const double* window_s, const int64_t* window_ids, int H,
+                          double decay, int64_t t) {
+  hb.Ws.ensure((size_t)std::max(H, 1) * R * 8);
+  hb.coef.ensure((size_t)std::max(H, 1) * 8);
+  std::vector<double> coef(std::max(H, 1), 0.0);
+  for (int h = 0; h < H; ++h) coef[h] = std::pow(decay, (double)(t - window_ids[h]));
+  if (H > 0) OGCP_CUDA(cudaMemcpyAsync(hb.Ws.ptr, window_s, (size_t)H * R * 8, cudaMemcpyHostToDevice, ctx->stream));
+  OGCP_CUDA(cudaMemcpyAsync(hb.coef.ptr, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+__global__ void k_window_matrix(int R, int H, const double* __restrict__ Ws, const double* __restrict__ coef,
+                                double* __restrict__ S) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, j = e % R;
+    double acc = 0.0;
+    for (int h = 0; h < H; ++h) acc += coef[h] * (Ws[(int64_t)h * R + i] * Ws[(int64_t)h * R + j]);
+    S[e] = acc;
+  }
+}
+
+__global__ void k_trace_sum(int ndim, int R, const double* __restrict__ P, double* __restrict__ out) {
+  if (threadIdx.x || blockIdx.x) return;
+  double t = 0.0;
+  for (int m = 0; m < ndim; ++m)
+    for (int i = 0; i < R; ++i) t += P[(int64_t)m * R * R + i * R + i];
+  *out = t;
+}
+
+// F(factors) = data term on the fixed objective set + (w/2) history + (lambda/2) sum ||A||^2
+static double factor_objective(Ctx* ctx, const Slice* X, const SamplesP& So, const ModelP& M, const float* s_f,
+                               const LossP& L, float* const* old_factors, int H, const ogcp_solver_config* cfg,
+                               HistBufs& hb, long long code, int64_t budget, int64_t t) {
+  cudaStream_t st = ctx->stream;
+  const int RR = M.rank * M.rank;
+  double* part = ctx->partials.as<double>();
+  double* dsc = ctx->scalars.as<double>();
+  double* hsc = ctx->host_scalars;
+  reset_flags(ctx);
+  int nb = objective_enqueue(ctx, So, M, s_f, L, part, code);
+  sum_partials_enqueue(ctx, part, nb, 1, dsc);
+  const bool hist = cfg->hist_weight != 0.0 && H > 0;
+  const bool reg = cfg->reg_factors != 0.0;
+  if (hist || reg) {
+    grams_enqueue(ctx, M, nullptr, hb.P.as<double>(), hb, true);
+    if (reg) {
+      k_trace_sum<<<1, 1, 0, st>>>(M.ndim, M.rank, hb.P.as<double>(), dsc + 2);
+      ctx->count();
+    }
+    if (hist) {
+      grams_enqueue(ctx, M, old_factors, hb.C.as<double>(), hb, false);
+      hist_penalty_enqueue(ctx, M.ndim, M.rank, hb.Poo.as<double>(), hb.C.as<double>(), hb.P.as<double>(),
+                           hb.Ws.as<double>(), hb.coef.as<double>(), H, dsc + 1);
+    }
+  }
+  (void)RR;
+  OGCP_CUDA(cudaMemcpyAsync(hsc, dsc, 3 * 8, cudaMemcpyDeviceToHost, st));
+  fetch_flags(ctx);
+  OGCP_CUDA(cudaStreamSynchronize(st));
+  check_flags(ctx, X, L.kind, budget, "factor solve", t);
+  double val = hsc[0];
+  if (hist) val += 0.5 * cfg->hist_weight * hsc[1];
+  if (reg) val += 0.5 * cfg->reg_factors * hsc[2];
+  return val;
+}
+
+static void adam_epoch(Ctx* ctx, const ModelP& M, float* const* A, ogcp_adam_state* ad, bool passed) {
+  for (int k = 0; k < M.ndim; ++k) {
+    const size_t b = (size_t)M.dims[k] * M.ldr * 4;
+    if (passed) {
+      OGCP_CUDA(cudaMemcpyAsync(ad->u_o[k], ad->u[k], b, cudaMemcpyDeviceToDevice, ctx->stream));
+      OGCP_CUDA(cudaMemcpyAsync(ad->v_o[k], ad->v[k], b, cudaMemcpyDeviceToDevice, ctx->stream));
+      OGCP_CUDA(cudaMemcpyAsync(ad->a_o[k], A[k], b, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      OGCP_CUDA(cudaMemcpyAsync(ad->u[k], ad->u_o[k], b, cudaMemcpyDeviceToDevice, ctx->stream));
+      OGCP_CUDA(cudaMemcpyAsync(ad->v[k], ad->v_o[k], b, cudaMemcpyDeviceToDevice, ctx->stream));
+      OGCP_CUDA(cudaMemcpyAsync(A[k], ad->a_o[k], b, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  }
+}
+
+// One factor iteration: draw -> K2/K3 -> (K4 Grams -> coefficients) -> K5 per mode.
+static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* const* A, const float* s_f,
+                             const LossP& L, float* const* old_factors, bool hist, const ogcp_solver_config* cfg,
+                             ogcp_adam_state* ad, double rate_i, const Pcg64& g, int64_t p, int64_t q,
+                             int64_t budget, FactorWork& W, long long ev) {
+  const int RR = M.rank * M.rank;
+  draw_enqueue(ctx, X, g, p, q, budget, W.grad.ord.as<int32_t>(), W.grad.zero.as<int32_t>(), code_of(ev, 0),
+               W.grad.scr);
+  SamplesP Sg = samples_of(X, W.grad.ord.as<int32_t>(), p, W.grad.zero.as<int32_t>(), q);
+  float* gp[kMaxModes];
+  size_t off = 0;
+  for (int k = 0; k < M.ndim; ++k) {
+    gp[k] = W.grads.as<float>() + off;
+    off += (size_t)M.dims[k] * M.ldr;
+  }
+  sgrad_enqueue(ctx, Sg, M, s_f, L, gp, code_of(ev, 1));
+  if (hist) {
+    grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true);
+    grams_enqueue(ctx, M, old_factors, W.hb.C.as<double>(), W.hb, false);
+    hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), W.hb.C.as<double>(), W.hb.S.as<double>(),
+                        cfg->hist_weight, W.hb.Mk.as<float>(), W.hb.Nk.as<float>());
+  }
+  for (int k = 0; k < M.ndim; ++k) {
+    factor_update_enqueue(ctx, M.dims[k], M.rank, M.ldr, A[k], hist ? old_factors[k] : nullptr, gp[k], ad->u[k],
+                          ad->v[k], hist ? W.hb.Mk.as<float>() + (size_t)k * RR : nullptr,
+                          hist ? W.hb.Nk.as<float>() + (size_t)k * RR : nullptr, cfg->reg_factors, rate_i,
+                          cfg->beta1, cfg->beta2, cfg->adam_eps, cfg->lower_bound, code_of(ev, 2));
+  }
+}
+
+static FactorWork& factor_work() {
+  static thread_local FactorWork w;
+  return w;
+}
+
+static void hist_alloc(HistBufs& hb, int ndim, int R) {
+  const size_t RR = (size_t)R * R;
+  hb.P.ensure(ndim * RR * 8);
+  hb.C.ensure(ndim * RR * 8);
+  hb.Poo.ensure(ndim * RR * 8);
+  hb.S.ensure(RR * 8);
+  hb.Mk.ensure(ndim * RR * 4);
+  hb.Nk.ensure(ndim * RR * 4);
+}
+
+static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config* cfg, const ogcp_loss* loss,
+                               int64_t t, const ogcp_model* mdl, float* const* old_factors, const double* weights,
+                               const double* window_s, const int64_t* window_ids, int H, ogcp_adam_state* ad,
+                               int64_t* iteration, ogcp_trace* trace) {
+  ModelP M = model_of(mdl);
+  check_model_slice(M, X);
+  LossP L = loss_of(loss);
+  cudaStream_t st = ctx->stream;
+  const uint64_t seed = cfg->samples.seed;
+  FactorWork& W = factor_work();
+  float* const* A = mdl->factors;
+  ctx->wsolve.ensure((size_t)M.ldr * (6 * 8 + 4));
+  float* s_f = reinterpret_cast<float*>(ctx->wsolve.as<double>() + 6 * M.ldr);
+  upload_weights(ctx, weights, M.rank, M.ldr, s_f);
+  ctx->partials.ensure((size_t)kNumSMs * 8 * M.ldr * 8 + 64);
+  ctx->scalars.ensure(64 * 8);
+  size_t gtot = 0;
+  for (int k = 0; k < M.ndim; ++k) gtot += (size_t)M.dims[k] * M.ldr;
+  W.grads.ensure(gtot * 4);
+  hist_alloc(W.hb, M.ndim, M.rank);
+  const bool hist = cfg->hist_weight != 0.0 && H > 0;
+  if (hist && !old_factors) throw Error(OGCP_E_DATA, "history terms require the previous-step factors");
+  window_upload(ctx, W.hb, M.rank, window_s, window_ids, H, cfg->hist_decay, t);
+  if (hist) {
+    k_window_matrix<<<1, 256, 0, st>>>(M.rank, H, W.hb.Ws.as<double>(), W.hb.coef.as<double>(), W.hb.S.as<double>());
+    ctx->count();
+    // Poo = Aold'Aold, constant during the solve
+    for (int k = 0; k < M.ndim; ++k)
+      gram_enqueue(ctx, old_factors[k], old_factors[k], M.dims[k], M.rank, M.ldr,
+                   W.hb.Poo.as<double>() + (size_t)k * M.rank * M.rank, W.hb.scratch);
+  }
+  // entry snapshot (solvers.py:303-305)
+  adam_epoch(ctx, M, A, ad, true);
+
+  int64_t po, qo, p, q;
+  resolve_counts(cfg->samples.obj_nonzeros, cfg->samples.obj_zeros, X, &po, &qo);
+  resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
+  if (po > 0 || p > 0) x_domain_check(X, L.kind);
+  draw_sync(ctx, X, keyed(seed, {t, 4}), po, qo, cfg->samples.max_rejects, W.obj);
+  SamplesP So = samples_of(X, W.obj.ord.as<int32_t>(), po, W.obj.zero.as<int32_t>(), qo);
+  precheck_draw(X, p, q);
+  W.grad.size(p, q, X->ndim);
+  const int64_t budget = budget_of(q, cfg->samples.max_rejects);
+
+  long long ev = 1;
+  double fest = factor_objective(ctx, X, So, M, s_f, L, old_factors, H, cfg, W.hb, code_of(ev++, 1), budget, t);
+  std::vector<double> objv{fest};
+  int64_t iter = *iteration;
+  int epochs = 0, rejections = 0;
+  for (int epoch = 0; epoch < cfg->max_epochs_factors; ++epoch) {
+    if (!(fest > cfg->tol_factors)) break;
+    const double fold = fest;
+    for (int attempt = 0;; ++attempt) {
+      reset_flags(ctx);
+      const long long ev0 = ev;
+      for (int it = 0; it < cfg->iters_factors; ++it) {
+        const int64_t cnt = iter + it + 1;
+        const double rate_i = ad->rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
+                              (1.0 - std::pow(cfg->beta1, (double)cnt));
+        factor_iteration(ctx, X, M, A, s_f, L, old_factors, hist, cfg, ad, rate_i, keyed(seed, {t, 3, epoch, it}),
+                         p, q, budget, W, ev++);
+      }
+      fetch_flags(ctx);
+      OGCP_CUDA(cudaStreamSynchronize(st));
+      int r = check_flags(ctx, X, L.kind, budget, "factor solve", t);
+      if (r == 0) break;
+      ctx->slack *= 4.0;
+      adam_epoch(ctx, M, A, ad, false);  // restore the epoch-start state (no rate decay)
+      ev = ev0;
+      if (attempt > 8) throw Error(OGCP_E_INTERNAL, "sampler could not provision enough candidates");
+    }
+    iter += cfg->iters_factors;
+    fest = factor_objective(ctx, X, So, M, s_f, L, old_factors, H, cfg, W.hb, code_of(ev++, 1), budget, t);
+    if (!std::isfinite(fest)) throw Error(OGCP_E_DIVERGENCE, "factor solve diverged at slice " + std::to_string(t));
+    if (fest > fold) {
+      adam_epoch(ctx, M, A, ad, false);
+      ad->rate *= cfg->rate_decay;
+      fest = fold;
+      iter -= cfg->iters_factors;
+      ++rejections;
+    } else {
+      adam_epoch(ctx, M, A, ad, true);
+    }
+    ++epochs;
+    objv.push_back(fest);
+  }
+  OGCP_CUDA(cudaStreamSynchronize(st));
+  *iteration = iter;
+  if (trace) {
+    trace->n_objective = 0;
+    for (size_t j = 0; j < objv.size() && (int)j <= cfg->max_epochs_factors; ++j)
+      trace->objective[trace->n_objective++] = objv[j];
+    trace->epochs = epochs;
+    trace->rejections = rejections;
+  }
+}
+
+}  // namespace ogcp
+
+// ===================================================================== C ABI
+using namespace ogcp;
+
+struct ogcp_ctx : Ctx {};
+struct ogcp_slice : Slice {};
+
+#define OGCP_API_BEGIN try {
+#define OGCP_API_END                                  \
+  return OGCP_OK;                                     \
+  }                                                   \
+  catch (const ogcp::Error& e) {                      \
+    g_last_error = e.what();                          \
+    return e.code;                                    \
+  }                                                   \
+  catch (const std::exception& e) {                   \
+    g_last_error = e.what();                          \
+    return OGCP_E_INTERNAL;                           \
+  }
+
+extern "C" {
+
+int ogcp_abi_version(void) { return OGCP_ABI_VERSION; }
+
+const char* ogcp_last_error(void) { return g_last_error.c_str(); }
+
+int32_t ogcp_padded_rank(int32_t rank) {
+  int32_t l = 4;
+  while (l < rank) l <<= 1;
+  return l;
+}
+
+int ogcp_rng_state(uint64_t seed, const int64_t* key, int32_t nkey, uint64_t out[4]) {
+  OGCP_API_BEGIN
+  if (nkey < 0 || nkey > 16) throw Error(OGCP_E_USAGE, "key too long");
+  uint64_t k[16];
+  for (int i = 0; i < nkey; ++i) {
+    if (key[i] < 0) throw Error(OGCP_E_USAGE, "key elements must be >= 0");
+    k[i] = (uint64_t)key[i];
+  }
+  Pcg64 g = seedseq_pcg64(seed, k, nkey);
+  out[0] = (uint64_t)(g.state >> 64);
+  out[1] = (uint64_t)g.state;
+  out[2] = (uint64_t)(g.inc >> 64);
+  out[3] = (uint64_t)g.inc;
+  OGCP_API_END
+}
+
+int ogcp_rng_integers(uint64_t seed, const int64_t* key, int32_t nkey, const int64_t* highs, int32_t nhigh, int64_t n,
+                      int64_t* out) {
+  OGCP_API_BEGIN
+  if (nkey < 0 || nkey > 16 || nhigh < 1) throw Error(OGCP_E_USAGE, "bad key or bounds");
+  uint64_t k[16];
+  for (int i = 0; i < nkey; ++i) k[i] = (uint64_t)key[i];
+  HostStream hs;
+  hs.g = seedseq_pcg64(seed, k, nkey);
+  hs.has_half = 0;
+  hs.half = 0;
+  hs.words = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t hi = highs[i % nhigh];
+    if (hi < 1 || hi > 0xffffffffLL) throw Error(OGCP_E_USAGE, "bounds must lie in [1, 2^32)");
+    out[i] = (int64_t)hs.bounded((uint32_t)hi);
+  }
+  OGCP_API_END
+}
+
+int ogcp_ctx_create(int32_t device, void* cuda_stream, ogcp_ctx** out) {
+  OGCP_API_BEGIN
+  OGCP_CUDA(cudaSetDevice(device));
+  std::unique_ptr<ogcp_ctx> c(new ogcp_ctx());
+  c->device = device;
+  c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  c->flags.ensure(sizeof(DevFlags));
+  OGCP_CUDA(cudaMallocHost((void**)&c->host_scalars, 64 * 8));
+  OGCP_CUDA(cudaMallocHost((void**)&c->host_flags, sizeof(DevFlags)));
+  init_jump_table();
+  *out = c.release();
+  OGCP_API_END
+}
+
+int ogcp_ctx_destroy(ogcp_ctx* ctx) {
+  OGCP_API_BEGIN
+  if (ctx) {
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->host_scalars) cudaFreeHost(ctx->host_scalars);
+    if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
+    delete ctx;
+  }
+  OGCP_API_END
+}
+
+int ogcp_ctx_set_stream(ogcp_ctx* ctx, void* cuda_stream) {
+  OGCP_API_BEGIN
+  ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  OGCP_API_END
+}
+
+int64_t ogcp_ctx_launches(const ogcp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ogcp_slice_create(ogcp_ctx* ctx, int32_t ndim, const int64_t* dims, int64_t nnz, const int64_t* subs0_dev,
+                      const double* vals_dev, int32_t allow_zero, ogcp_slice** out) {
+  OGCP_API_BEGIN
+  Slice* s = slice_create_impl<int64_t, double>(ctx, ndim, dims, nnz, subs0_dev, vals_dev, allow_zero);
+  *out = static_cast<ogcp_slice*>(s);
+  OGCP_API_END
+}
+
+int ogcp_slice_create_i32(ogcp_ctx* ctx, int32_t ndim, const int64_t* dims, int64_t nnz, const int32_t* subs0_dev,
+                          const float* vals_dev, int32_t allow_zero, ogcp_slice** out) {
+  OGCP_API_BEGIN
+  Slice* s = slice_create_impl<int32_t, float>(ctx, ndim, dims, nnz, subs0_dev, vals_dev, allow_zero);
+  *out = static_cast<ogcp_slice*>(s);
+  OGCP_API_END
+}
+
+int ogcp_slice_destroy(ogcp_slice* s) {
+  OGCP_API_BEGIN
+  delete static_cast<Slice*>(s);
+  OGCP_API_END
+}
+
+int ogcp_slice_info(const ogcp_slice* s, int64_t* nnz, int64_t* omega, double* frob) {
+  OGCP_API_BEGIN
+  if (nnz) *nnz = s->nnz;
+  if (omega) *omega = s->omega;
+  if (frob) *frob = s->frob_sq;
+  OGCP_API_END
+}
+
+int ogcp_slice_contains(ogcp_ctx* ctx, const ogcp_slice* s, const int64_t* subs0_dev, int64_t n, uint8_t* hit_dev) {
+  OGCP_API_BEGIN
+  slice_contains_impl(ctx, s, subs0_dev, n, hit_dev);
+  OGCP_API_END
+}
+
+int ogcp_draw_samples(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const int64_t* key, int32_t nkey, int64_t p,
+                      int64_t q, int64_t max_rejects, int32_t* ordinals_dev, int32_t* zero_subs_dev) {
+  OGCP_API_BEGIN
+  if (p < 0 || q < 0) throw Error(OGCP_E_USAGE, "counts must be >= 0");
+  uint64_t k[16];
+  if (nkey < 0 || nkey > 16) throw Error(OGCP_E_USAGE, "key too long");
+  for (int i = 0; i < nkey; ++i) k[i] = (uint64_t)key[i];
+  Pcg64 g = seedseq_pcg64(seed, k, nkey);
+  precheck_draw(s, p, q);
+  const int64_t budget = budget_of(q, max_rejects);
+  static thread_local DrawScratch scr;
+  for (int attempt = 0;; ++attempt) {
+    reset_flags(ctx);
+    draw_enqueue(ctx, s, g, p, q, budget, ordinals_dev, zero_subs_dev, 0, scr);
+    fetch_flags(ctx);
+    OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (check_flags(ctx, s, OGCP_GAUSSIAN, budget, "draw", 0) == 0) break;
+    ctx->slack *= 4.0;
+    if (attempt > 8) throw Error(OGCP_E_INTERNAL, "sampler could not provision enough candidates");
+  }
+  OGCP_API_END
+}
+
+int ogcp_sampled_gradient(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev, int64_t p,
+                          const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m, const double* weights,
+                          const ogcp_loss* loss, float* const* grads_dev, double* gw_dev) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  check_model_slice(M, s);
+  LossP L = loss_of(loss);
+  if (p > 0) x_domain_check(s, L.kind);
+  ctx->wsolve.ensure((size_t)M.ldr * (6 * 8 + 4));
+  float* s_f = reinterpret_cast<float*>(ctx->wsolve.as<double>() + 6 * M.ldr);
+  upload_weights(ctx, weights, M.rank, M.ldr, s_f);
+  SamplesP S = samples_of(s, ordinals_dev, p, zero_subs_dev, q);
+  reset_flags(ctx);
+  if (grads_dev) sgrad_enqueue(ctx, S, M, s_f, L, grads_dev, code_of(1, 1));
+  if (gw_dev) {
+    ctx->partials.ensure((size_t)kNumSMs * 8 * M.ldr * 8 + 64);
+    ctx->scalars.ensure(64 * 8 + M.ldr * 8);
+    int nb = wgrad_enqueue(ctx, S, M, s_f, L, ctx->partials.as<double>(), code_of(1, 1));
+    sum_partials_enqueue(ctx, ctx->partials.as<double>(), nb, M.ldr, ctx->scalars.as<double>() + 64);
+    OGCP_CUDA(cudaMemcpyAsync(gw_dev, ctx->scalars.as<double>() + 64, M.rank * 8, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+  }
+  fetch_flags(ctx);
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+  check_flags(ctx, s, L.kind, 0, "gradient", 0);
+  OGCP_API_END
+}
+
+int ogcp_factor_gradients(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev, int64_t p,
+                          const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m, float* const* old_factors,
+                          const double* weights, const ogcp_loss* loss, const double* window_s,
+                          const int64_t* window_ids, int32_t H, double hist_weight, double hist_decay, int64_t t,
+                          double reg_factors, float* const* grads_dev) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  check_model_slice(M, s);
+  LossP L = loss_of(loss);
+  if (p > 0) x_domain_check(s, L.kind);
+  ctx->wsolve.ensure((size_t)M.ldr * (6 * 8 + 4));
+  float* s_f = reinterpret_cast<float*>(ctx->wsolve.as<double>() + 6 * M.ldr);
+  upload_weights(ctx, weights, M.rank, M.ldr, s_f);
+  SamplesP S = samples_of(s, ordinals_dev, p, zero_subs_dev, q);
+  FactorWork& W = factor_work();
+  hist_alloc(W.hb, M.ndim, M.rank);
+  const bool hist = hist_weight != 0.0 && H > 0;
+  if (hist && !old_factors) throw Error(OGCP_E_DATA, "history terms require the previous-step factors");
+  reset_flags(ctx);
+  sgrad_enqueue(ctx, S, M, s_f, L, grads_dev, code_of(1, 1));
+  window_upload(ctx, W.hb, M.rank, window_s, window_ids, H, hist_decay, t);
+  const int RR = M.rank * M.rank;
+  if (hist) {
+    k_window_matrix<<<1, 256, 0, ctx->stream>>>(M.rank, H, W.hb.Ws.as<double>(), W.hb.coef.as<double>(),
+                                                W.hb.S.as<double>());
+    ctx->count();
+    grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true);
+    grams_enqueue(ctx, M, old_factors, W.hb.C.as<double>(), W.hb, false);
+    hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), W.hb.C.as<double>(), W.hb.S.as<double>(),
+                        hist_weight, W.hb.Mk.as<float>(), W.hb.Nk.as<float>());
+  }
+  // G += lambda A + history, via the K5 kernel with Adam disabled is not
+  // possible; use a dedicated pass: rate 0 Adam would still touch u/v, so we
+  // apply the terms with the same kernel on scratch moments and beta1 = 0,
+  // beta2 = 0, rate = 0: u' = g is the assembled gradient.
+  for (int k = 0; k < M.ndim; ++k) {
+    DevBuf& tmp = W.hb.tmp;
+    const size_t n = (size_t)M.dims[k] * M.ldr;
+    tmp.ensure(n * 3 * 4);
+    float* u = tmp.as<float>();
+    float* v = u + n;
+    float* a = v + n;
+    OGCP_CUDA(cudaMemsetAsync(u, 0, n * 4, ctx->stream));
+    OGCP_CUDA(cudaMemsetAsync(v, 0, n * 4, ctx->stream));
+    OGCP_CUDA(cudaMemcpyAsync(a, M.A[k], n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    factor_update_enqueue(ctx, M.dims[k], M.rank, M.ldr, a, hist ? old_factors[k] : nullptr, grads_dev[k], u, v,
+                          hist ? W.hb.Mk.as<float>() + (size_t)k * RR : nullptr,
+                          hist ? W.hb.Nk.as<float>() + (size_t)k * RR : nullptr, reg_factors, 0.0, 0.0, 0.0, 1.0,
+                          -INFINITY, code_of(1, 2));
+    OGCP_CUDA(cudaMemcpyAsync(grads_dev[k], u, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  fetch_flags(ctx);
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+  check_flags(ctx, s, L.kind, 0, "gradient", t);
+  OGCP_API_END
+}
+
+int ogcp_estimate_objective(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev, int64_t p,
+                            const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m, float* const* old_factors,
+                            const double* weights, const ogcp_loss* loss, const double* window_s,
+                            const int64_t* window_ids, int32_t H, double hist_weight, double hist_decay, int64_t t,
+                            double reg_factors, double reg_weights, double* out) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  check_model_slice(M, s);
+  LossP L = loss_of(loss);
+  if (p > 0) x_domain_check(s, L.kind);
+  ctx->wsolve.ensure((size_t)M.ldr * (6 * 8 + 4));
+  float* s_f = reinterpret_cast<float*>(ctx->wsolve.as<double>() + 6 * M.ldr);
+  upload_weights(ctx, weights, M.rank, M.ldr, s_f);
+  ctx->partials.ensure((size_t)kNumSMs * 8 * M.ldr * 8 + 64);
+  ctx->scalars.ensure(64 * 8);
+  SamplesP S = samples_of(s, ordinals_dev, p, zero_subs_dev, q);
+  FactorWork& W = factor_work();
+  hist_alloc(W.hb, M.ndim, M.rank);
+  const bool hist = hist_weight != 0.0 && H > 0;
+  if (hist && !old_factors) throw Error(OGCP_E_DATA, "history terms require the previous-step factors");
+  window_upload(ctx, W.hb, M.rank, window_s, window_ids, H, hist_decay, t);
+  if (hist)
+    for (int k = 0; k < M.ndim; ++k)
+      gram_enqueue(ctx, old_factors[k], old_factors[k], M.dims[k], M.rank, M.ldr,
+                   W.hb.Poo.as<double>() + (size_t)k * M.rank * M.rank, W.hb.scratch);
+  ogcp_solver_config cfg{};
+  cfg.hist_weight = hist_weight;
+  cfg.hist_decay = hist_decay;
+  cfg.reg_factors = reg_factors;
+  double v = factor_objective(ctx, s, S, M, s_f, L, old_factors, hist ? H : 0, &cfg, W.hb, code_of(1, 1), 0, t);
+  if (reg_weights) {
+    double ss = 0.0;
+    for (int r = 0; r < M.rank; ++r) ss += weights[r] * weights[r];
+    v += 0.5 * reg_weights * ss;
+  }
+  *out = v;
+  OGCP_API_END
+}
+
+int ogcp_gram(ogcp_ctx* ctx, const ogcp_model* m, float* const* other, int32_t skip, double* out) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  const int RR = M.rank * M.rank;
+  FactorWork& W = factor_work();
+  hist_alloc(W.hb, M.ndim, M.rank);
+  grams_enqueue(ctx, M, other, W.hb.P.as<double>(), W.hb, other == nullptr);
+  std::vector<double> h((size_t)M.ndim * RR);
+  OGCP_CUDA(cudaMemcpyAsync(h.data(), W.hb.P.ptr, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+  bool any = false;
+  for (int e = 0; e < RR; ++e) out[e] = 1.0;
+  for (int k = 0; k < M.ndim; ++k) {
+    if (k == skip) continue;
+    any = true;
+    for (int e = 0; e < RR; ++e) out[e] *= h[(size_t)k * RR + e];
+  }
+  if (!any) throw Error(OGCP_E_DATA, "gram over zero modes is undefined");
+  OGCP_API_END
+}
+
+int ogcp_adam_step(ogcp_ctx* ctx, const ogcp_model* m, float* const* grads, ogcp_adam_state* st, double beta1,
+                   double beta2, double eps, double lower_bound, int64_t step_count) {
+  OGCP_API_BEGIN
+  if (step_count < 1) throw Error(OGCP_E_DATA, "step_count is 1-based and must be >= 1");
+  ModelP M = model_of(m);
+  const double rate_i =
+      st->rate * std::sqrt(1.0 - std::pow(beta2, (double)step_count)) / (1.0 - std::pow(beta1, (double)step_count));
+  reset_flags(ctx);
+  for (int k = 0; k < M.ndim; ++k)
+    factor_update_enqueue(ctx, M.dims[k], M.rank, M.ldr, m->factors[k], nullptr, grads[k], st->u[k], st->v[k],
+                          nullptr, nullptr, 0.0, rate_i, beta1, beta2, eps, lower_bound, code_of(1, 2));
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+  OGCP_API_END
+}
+
+int ogcp_adam_update(ogcp_ctx* ctx, const ogcp_model* m, ogcp_adam_state* st, int32_t passed, double rate_decay) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  adam_epoch(ctx, M, m->factors, st, passed != 0);
+  if (!passed) st->rate *= rate_decay;
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+  OGCP_API_END
+}
+
+int ogcp_solve_weights(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_config* cfg, const ogcp_loss* loss,
+                       int64_t t, const ogcp_model* m, const double* s_init, double* s_out, ogcp_trace* trace) {
+  OGCP_API_BEGIN
+  solve_weights_impl(ctx, s, cfg, loss, t, m, s_init, s_out, trace);
+  OGCP_API_END
+}
+
+int ogcp_solve_factors(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_config* cfg, const ogcp_loss* loss,
+                       int64_t t, const ogcp_model* m, float* const* old_factors, const double* weights,
+                       const double* window_s, const int64_t* window_ids, int32_t H, ogcp_adam_state* adam,
+                       int64_t* iteration, ogcp_trace* trace) {
+  OGCP_API_BEGIN
+  solve_factors_impl(ctx, s, cfg, loss, t, m, old_factors, weights, window_s, window_ids, H, adam, iteration, trace);
+  OGCP_API_END
+}
+
+int ogcp_local_loss(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m, const double* weights,
+                    const ogcp_loss* loss, int32_t mode, int64_t p, int64_t q, uint64_t seed, const int64_t* key,
+                    int32_t nkey, int64_t max_rejects, int64_t max_elements, double* out, int32_t* normalized) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  if (M.ndim != s->ndim) throw Error(OGCP_E_DATA, "dims differ");
+  for (int k = 0; k < M.ndim; ++k)
+    if (M.dims[k] != s->dims[k]) throw Error(OGCP_E_DATA, "dims differ");
+  LossP L = loss_of(loss);
+  ctx->wsolve.ensure((size_t)M.ldr * (6 * 8 + 4));
+  float* s_f = reinterpret_cast<float*>(ctx->wsolve.as<double>() + 6 * M.ldr);
+  upload_weights(ctx, weights, M.rank, M.ldr, s_f);
+  ctx->partials.ensure((size_t)kNumSMs * 8 * M.ldr * 8 + 64);
+  ctx->scalars.ensure(64 * 8);
+  double* part = ctx->partials.as<double>();
+  double* dsc = ctx->scalars.as<double>();
+  double total = 0.0;
+  if (mode == 0) {
+    if (!s->omega_fits || s->omega > max_elements)
+      throw Error(OGCP_E_DATA, "exact local loss over " + std::to_string(s->omega) + " cells exceeds cap " +
+                                   std::to_string(max_elements) + "; use sampled mode");
+    if (s->nnz > 0) x_domain_check(s, L.kind);
+    reset_flags(ctx);
+    int nb = exact_cells_enqueue(ctx, M, s_f, L, s->omega, part, code_of(1, 1));
+    sum_partials_enqueue(ctx, part, nb, 1, dsc);
+    SamplesP S = samples_of(s, nullptr, 0, nullptr, 0);
+    if (s->nnz > 0) {
+      // every stored entry once: ordinals 0..nnz-1
+      static thread_local DevBuf iota;
+      iota.ensure((size_t)s->nnz * 4);
+      std::vector<int32_t> h(s->nnz);
+      for (int64_t i = 0; i < s->nnz; ++i) h[i] = (int32_t)i;
+      OGCP_CUDA(cudaMemcpyAsync(iota.ptr, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+      S = samples_of(s, iota.as<int32_t>(), s->nnz, nullptr, 0);
+      int nb2 = exact_nz_enqueue(ctx, S, M, s_f, L, part + nb, code_of(1, 1));
+      sum_partials_enqueue(ctx, part + nb, nb2, 1, dsc + 1);
+    } else {
+      OGCP_CUDA(cudaMemsetAsync(dsc + 1, 0, 8, ctx->stream));
+    }
+    OGCP_CUDA(cudaMemcpyAsync(ctx->host_scalars, dsc, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    fetch_flags(ctx);
+    OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+    check_flags(ctx, s, L.kind, 0, "local loss", 0);
+    total = ctx->host_scalars[0] + ctx->host_scalars[1];
+  } else {
+    int64_t pp, qq;
+    resolve_counts(p, q, s, &pp, &qq);
+    if (pp > 0) x_domain_check(s, L.kind);
+    uint64_t k[16];
+    for (int i = 0; i < nkey; ++i) k[i] = (uint64_t)key[i];
+    static thread_local SampleBufs b;
+    draw_sync(ctx, s, seedseq_pcg64(seed, k, nkey), pp, qq, max_rejects, b);
+    SamplesP S = samples_of(s, b.ord.as<int32_t>(), pp, b.zero.as<int32_t>(), qq);
+    reset_flags(ctx);
+    int nb = objective_enqueue(ctx, S, M, s_f, L, part, code_of(1, 1));
+    sum_partials_enqueue(ctx, part, nb, 1, dsc);
+    OGCP_CUDA(cudaMemcpyAsync(ctx->host_scalars, dsc, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    fetch_flags(ctx);
+    OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+    check_flags(ctx, s, L.kind, 0, "local loss", 0);
+    total = ctx->host_scalars[0];
+  }
+  if (s->frob_sq > 0) {
+    *out = total / s->frob_sq;
+    *normalized = 1;
+  } else {
+    *out = total;
+    *normalized = 0;
+  }
+  OGCP_API_END
+}
+
+}  // extern "C"
