@@ -1,0 +1,350 @@
+"""Benchmark: sampled GCP gradient entries/s of the OnlineGCP per-slice solve.
+
+Workload (BASELINE.json configs[3]): synthetic planted Poisson
+stream, 1M x 1M x 1K per slice, 1e8 nonzeros per slice, rank 32, taxi-poisson
+schedule (kappa_w = kappa_f = 1, tau = 100, rate_w 10, rate_f 1e-3, w = 1,
+H = 30), gradient samples p = all nonzeros (eta draws with replacement) and
+q = 2^24 zeros, objective samples p' = q' = 2^24.
+
+One step = one ``process_slice`` (temporal solve + factor solve + sampled local
+loss) on one slice.  ``value`` counts the sampled gradient entries of every
+executed weight and factor iteration, (p + q) each, per second with the slice
+resident in HBM; ``e2e`` is the same through the public API with the slice
+handed over as host numpy arrays in pinned memory (H2D + device ingest inside
+the timed region) and the per-slice metrics read back.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DIMS = (1_000_000, 1_000_000, 1_000)
+NNZ = 100_000_000
+RANK = 32
+Q = 1 << 24
+POBJ = QOBJ = 1 << 24
+H = 30
+WORKLOAD = "c4: planted Poisson stream 1Mx1Mx1K, 1e8 nnz/slice, R=32, p=all, q=2^24 (taxi-poisson schedule)"
+CPU_SAMPLE_PQ = 1 << 19
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--nnz", type=int, default=NNZ)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def bytes_per_entry(d, R):
+    """factor-solve entry B_f = 8dR + 4d + 4 ; weight-solve entry B_w = 4dR + 4d + 4."""
+    return 8 * d * R + 4 * d + 4, 4 * d * R + 4 * d + 4
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_cfg(P):
+    return P.SolverConfig(max_epochs_weights=1, max_epochs_factors=1, iters_weights=100, iters_factors=100,
+                          rate_weights=10.0, rate_factors=1e-3, hist_weight=1.0, warm_start_weights=True,
+                          samples=P.SamplerConfig(None, Q, POBJ, QOBJ, seed=7))
+
+
+def make_state(P, X, factors, mix, total_events, cfg, loss, seed=11):
+    """Near-fit stream state: planted factors with 5% noise, H past weight vectors."""
+    rng = np.random.default_rng(seed)
+    init = [a * (1.0 + 0.05 * rng.uniform(-1, 1, a.shape)) for a in factors]
+    st = P.fresh_state(X.dims, RANK, loss, cfg, factors=init)
+    st.window = P.HistoryWindow(capacity=H)
+    truth_w = total_events * np.asarray(mix)
+    for h in range(1, H + 1):
+        s_h = truth_w * (1.0 + 0.05 * rng.uniform(-1, 1, truth_w.shape))
+        st.weights_log.append(s_h)
+        st.window.observe(h, s_h, P.rng_at(cfg.samples.seed, h, P.sampling.PHASE_WINDOW))
+    st.t = H
+    return st
+
+
+def entries_of(st, t0, p, q, cfg):
+    """Sampled gradient entries executed by the slices after step t0 (weight + factor iterations)."""
+    n = 0
+    for m in st.metrics:
+        if m.t > t0:
+            n += (m.epochs_weights * cfg.iters_weights + m.epochs_factors * cfg.iters_factors) * (p + q)
+    return n
+
+
+def cpu_baseline_oracle(subs0, vals, dims, factors, weights, old, window, t, pq, reps=1):
+    """The oracle restatement of the reference path timed on this host: one factor iteration
+    (sampled_gradient_tensor + factor_gradients + Adam.step, solvers.py:345-355) at p = q = pq."""
+    from oracle import ogcp_oracle as O
+    X = O.Slice(dims, subs0, vals)
+    adam = O.AdamOracle(1e-3, lower=0.0)
+    adam.init(factors)
+    best = None
+    for r in range(reps):
+        t0 = time.perf_counter()
+        _, ys, yv = O.sampled_y(X, factors, weights, "poisson", pq, pq, O.keyed_rng(7, t, 3, 0, r))
+        grads = O.assemble_factor_grads(ys, yv, dims, factors, weights, old, window, 1.0, 1.0, t, 0.0)
+        adam.step([a.copy() for a in factors], grads, 1)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return 2 * pq / best, best
+
+
+def run_reference(args):
+    """--impl reference: the oracle port of the reference path on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    import paper_2110_14514_b200 as P
+    from paper_2110_14514_b200.synthetic import gen_slice
+    torch.cuda.set_device(0)
+    X, factors, mix, total = gen_slice(DIMS, args.nnz, RANK, "poisson", seed=42)
+    subs0, vals = X.subs0, X.vals
+    del X
+    torch.cuda.empty_cache()
+    rng = np.random.default_rng(11)
+    init = [a * (1.0 + 0.05 * rng.uniform(-1, 1, a.shape)) for a in factors]
+    w = total * np.asarray(mix)
+    window = [(h, w * (1.0 + 0.05 * rng.uniform(-1, 1, w.shape))) for h in range(1, H + 1)]
+    from oracle import ogcp_oracle as O
+    Xo = O.Slice(DIMS, subs0, vals)
+    adam = O.AdamOracle(1e-3, lower=0.0)
+    adam.init(init)
+    pq = CPU_SAMPLE_PQ
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        _, ys, yv = O.sampled_y(Xo, init, w, "poisson", pq, pq, O.keyed_rng(7, H + 1, 3, 0, i))
+        grads = O.assemble_factor_grads(ys, yv, DIMS, init, w, init, window, 1.0, 1.0, H + 1, 0.0)
+        adam.step([a.copy() for a in init], grads, i + 1)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = args.steps * 2 * pq / tot
+    sample = f"one factor iteration per step at p=q=2^19 on the c4 slice (oracle numpy port, 1 process)"
+    line = {"metric": "sampled GCP gradient entries/s", "value": value, "unit": "entries/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample_per_step": sample},
+            "cpu_baseline": {"value": value, "unit": "entries/s", "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2110_14514_b200 as P
+    from paper_2110_14514_b200 import _lib
+    from paper_2110_14514_b200.synthetic import gen_slice
+    import ctypes as C
+
+    loss = P.make_loss("poisson")
+    cfg = make_cfg(P)
+    X, factors, mix, total = gen_slice(DIMS, args.nnz, RANK, "poisson", seed=42 + rank)
+    st = make_state(P, X, factors, mix, total, cfg, loss, seed=11 + rank)
+    p, q = X.nnz, Q
+    B_f, B_w = bytes_per_entry(len(DIMS), RANK)
+
+    for _ in range(args.warmup):
+        P.process_slice(st, X, loss, cfg, exact_loss=False)
+    torch.cuda.synchronize()
+    ctx = _lib.ctx()
+    L = _lib.lib()
+    L.ogcp_ctx_profile_reset(ctx)
+    L.ogcp_ctx_profile_enable(ctx, 1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    launches0 = _lib.launches()
+    t_first = st.t
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        P.process_slice(st, X, loss, cfg, exact_loss=False)
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = _lib.launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    prof = {}
+    for cls, name in enumerate(["draw", "sgrad", "wgrad", "objective", "gram", "update", "ingest"]):
+        n, tms = C.c_int64(), C.c_double()
+        L.ogcp_ctx_profile_read(ctx, cls, C.byref(n), C.byref(tms))
+        prof[name] = {"launches": int(n.value), "ms": float(tms.value)}
+    L.ogcp_ctx_profile_enable(ctx, 0)
+    entries = entries_of(st, t_first, p, q, cfg)
+    ms_max = ms
+    entries_tot = entries
+    if world > 1:
+        tt = torch.tensor([ms, float(entries)], dtype=torch.float64, device="cuda")
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        ms_max, entries_tot = float(mx[0]), float(tt[1])
+    value = entries_tot / (ms_max / 1000.0)
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    sg = prof["sgrad"]
+    sg_ms = sg["ms"] / max(sg["launches"], 1)
+    sg_bytes = B_f * (p + q)
+    achieved = sg_bytes / (sg_ms / 1000.0) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("sgrad_dram_bytes_per_launch")
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        subs_pin = torch.from_numpy(X.subs0).pin_memory()
+        vals_pin = torch.from_numpy(X.vals).pin_memory()
+        subs_np, vals_np = subs_pin.numpy(), vals_pin.numpy()
+        h2d = subs_np.nbytes + vals_np.nbytes
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        t_e2e = st.t
+        d2h = 0
+        for _ in range(args.steps):
+            Xh = P.SparseTensor.from_zero_based(DIMS, subs_np, vals_np)
+            row = P.process_slice(st, Xh, loss, cfg, exact_loss=False)
+            _ = float(row.local_loss_sampled)
+            d2h += 8 * (RANK + 1)
+            del Xh
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        ent = entries_of(st, t_e2e, p, q, cfg)
+        if world > 1:
+            tt = torch.tensor([dt, float(ent)], dtype=torch.float64, device="cuda")
+            mx = tt.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            dt, ent = float(mx[0]), float(tt[1])
+        e2e = {"value": ent / dt, "unit": "entries/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h // args.steps)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        fs = st.factors
+        w = st.weights_log[-1]
+        val, secs = cpu_baseline_oracle(X.subs0, X.vals, DIMS, fs, w, st.old_factors, list(st.window.entries),
+                                        st.t + 1, CPU_SAMPLE_PQ)
+        cpu = {"value": val, "unit": "entries/s", "cores": 1, "kind": "port",
+               "sample": f"1 oracle factor iteration at p=q=2^19 on the same c4 slice ({secs:.1f} s)"}
+
+    if rank == 0:
+        steps_iters = 200
+        line = {
+            "metric": "sampled GCP gradient entries/s", "value": value, "unit": "entries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "nnz_per_slice": int(p), "q": Q, "p_obj": POBJ, "q_obj": QOBJ,
+                       "rank": RANK, "iterations_per_step": steps_iters,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (slice 1.6 GB + factors 256 MB)"},
+            "slices_per_s": 1000.0 * args.steps / ms_max * world,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgrad (K2+K3 fused eval/scatter)",
+                         "algorithmic_bytes_per_launch": sg_bytes, "avg_launch_ms": sg_ms},
+            "kernel_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+            "kernel_launch_brackets": {k: v["launches"] for k, v in prof.items()},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -127,6 +127,14 @@ int ogcp_ctx_destroy(ogcp_ctx* ctx);
 int ogcp_ctx_set_stream(ogcp_ctx* ctx, void* cuda_stream);
 /* Number of kernels this context has launched so far. */
 int64_t ogcp_ctx_launches(const ogcp_ctx* ctx);
+/* CUDA-event timing per kernel class on the context stream (measurement):
+ * classes 0 draw (K1), 1 eval+scatter (K2/K3), 2 weight gradient, 3 objective (K6),
+ * 4 Gram (K4), 5 fused update (K5 / weight Adam), 6 ingest (K0). */
+int ogcp_ctx_profile_enable(ogcp_ctx* ctx, int32_t on);
+/* Resolves pending events (synchronizes) and returns the accumulated bracket
+ * count and milliseconds of one class. */
+int ogcp_ctx_profile_read(ogcp_ctx* ctx, int32_t cls, int64_t* brackets, double* total_ms);
+int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
 
 /* ----------------------------------------------------------------- slice */
 /* SparseTensor.from_zero_based (tensor.py:75-119): validates bounds,

@@ -88,10 +88,51 @@ struct Slice {
   uint64_t strides[kMaxModes] = {0};
 };
 
+// Per-kernel-class CUDA-event timing on the context stream (bench evidence).
+enum : int { kProfDraw = 0, kProfSgrad, kProfWgrad, kProfObjective, kProfGram, kProfUpdate, kProfIngest,
+             kProfClasses };
+
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[kProfClasses];
+  double total_ms[kProfClasses] = {0};
+  int64_t count[kProfClasses] = {0};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) throw Error(OGCP_E_CUDA, "cudaEventCreate failed");
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void resolve() {
+    for (int c = 0; c < kProfClasses; ++c) {
+      for (auto& pr : pending[c]) {
+        cudaEventSynchronize(pr.second);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pr.first, pr.second);
+        total_ms[c] += ms;
+        count[c] += 1;
+        pool.push_back(pr.first);
+        pool.push_back(pr.second);
+      }
+      pending[c].clear();
+    }
+  }
+  void reset() {
+    resolve();
+    for (int c = 0; c < kProfClasses; ++c) { total_ms[c] = 0; count[c] = 0; }
+  }
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
+  Profiler prof;
   double slack = 1.0;           // sampler over-provisioning multiplier (grows on shortfall)
   // scratch
   DevBuf flags;                 // DevFlags
@@ -109,6 +150,26 @@ struct Ctx {
   double* host_scalars = nullptr;  // pinned host mirror
   DevFlags* host_flags = nullptr;  // pinned
   void count(int n = 1) { launches += n; }
+};
+
+// RAII event bracket around the launches of one kernel class.
+struct ProfScope {
+  Ctx* ctx;
+  int cls;
+  cudaEvent_t start = nullptr;
+  ProfScope(Ctx* c, int k) : ctx(c), cls(k) {
+    if (ctx->prof.on) {
+      start = ctx->prof.get();
+      cudaEventRecord(start, ctx->stream);
+    }
+  }
+  ~ProfScope() {
+    if (start) {
+      cudaEvent_t end = ctx->prof.get();
+      cudaEventRecord(end, ctx->stream);
+      ctx->prof.pending[cls].emplace_back(start, end);
+    }
+  }
 };
 
 inline void check_launch() {

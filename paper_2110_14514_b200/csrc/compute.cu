@@ -667,6 +667,7 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
     }
   }
   const size_t smem = (size_t)used * 4;
+  ProfScope prof_scope(ctx, kProfSgrad);
   dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
     auto kern = k_sgrad<D, G, V>;
@@ -683,6 +684,7 @@ int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f
                   double* partials, long long code) {
   const int64_t total = S.p + S.q;
   int grid = 1;
+  ProfScope prof_scope(ctx, kProfWgrad);
   dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
     grid = sample_grid(std::max<int64_t>(total, 1), G, 4);
@@ -700,6 +702,7 @@ int objective_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float*
   dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
     grid = sample_grid(std::max<int64_t>(total, 1), G, 4);
+    ProfScope prof_scope(ctx, kProfObjective);
     k_objective<D, G, V><<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(),
                                                              code);
   });
@@ -747,6 +750,7 @@ void gram_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int ra
   scratch.ensure((size_t)nblk * RR * 8);
   const size_t smem = (size_t)2 * kGramTile * ldr * 4;
   if (smem > 48 * 1024) OGCP_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ProfScope prof_scope(ctx, kProfGram);
   k_gram<<<nblk, kThreads, smem, ctx->stream>>>(A, B, rows, rank, ldr, rpb, scratch.as<double>());
   ctx->count();
   check_launch();
@@ -768,6 +772,7 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
   const size_t smem = Mk ? (size_t)2 * rank * rank * 4 : 0;
   int GR = 1;
   while (GR < rank && GR < 32) GR <<= 1;
+  ProfScope prof_scope(ctx, kProfUpdate);
   auto launch = [&](auto kern) {
     if (smem > 48 * 1024) OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t groups = kThreads / GR;
@@ -790,6 +795,7 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
 void weight_step_enqueue(Ctx* ctx, const double* partials, int nblk, int rank, int ldr, double* wstate, float* s_f,
                          double mu, double rate_i, double beta1, double beta2, double eps, double lower,
                          long long code) {
+  ProfScope prof_scope(ctx, kProfUpdate);
   k_weight_step<<<1, ldr, 0, ctx->stream>>>(partials, nblk, rank, ldr, wstate, s_f, mu, rate_i, beta1, beta2, eps,
                                             lower, ctx->flags.as<DevFlags>(), code);
   ctx->count();

@@ -676,6 +676,27 @@ int ogcp_ctx_set_stream(ogcp_ctx* ctx, void* cuda_stream) {
 
 int64_t ogcp_ctx_launches(const ogcp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int ogcp_ctx_profile_enable(ogcp_ctx* ctx, int32_t on) {
+  OGCP_API_BEGIN
+  ctx->prof.on = on != 0;
+  OGCP_API_END
+}
+
+int ogcp_ctx_profile_read(ogcp_ctx* ctx, int32_t cls, int64_t* brackets, double* total_ms) {
+  OGCP_API_BEGIN
+  if (cls < 0 || cls >= kProfClasses) throw Error(OGCP_E_USAGE, "bad profile class");
+  ctx->prof.resolve();
+  *brackets = ctx->prof.count[cls];
+  *total_ms = ctx->prof.total_ms[cls];
+  OGCP_API_END
+}
+
+int ogcp_ctx_profile_reset(ogcp_ctx* ctx) {
+  OGCP_API_BEGIN
+  ctx->prof.reset();
+  OGCP_API_END
+}
+
 int ogcp_slice_create(ogcp_ctx* ctx, int32_t ndim, const int64_t* dims, int64_t nnz, const int64_t* subs0_dev,
                       const double* vals_dev, int32_t allow_zero, ogcp_slice** out) {
   OGCP_API_BEGIN

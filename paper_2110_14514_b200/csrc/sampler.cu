@@ -449,6 +449,7 @@ static double reject_rate(uint32_t n) { return (double)lemire_threshold(n) / 429
 void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
                   int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr) {
   init_jump_table();
+  ProfScope prof_scope(ctx, kProfDraw);
   const int d = X->ndim;
   const int64_t eta = X->nnz;
   cudaStream_t s = ctx->stream;
