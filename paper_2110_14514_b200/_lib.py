@@ -17,7 +17,7 @@ import numpy as np
 from .exceptions import DataError, DivergenceError, OgcpError, SamplingError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libogcp_b200.so")
+LIB_PATH = os.environ.get("OGCP_LIB", os.path.join(_HERE, "libogcp_b200.so"))
 
 OK, E_INTERNAL, E_USAGE, E_DATA, E_DIVERGENCE, E_SAMPLING, E_CUDA = range(7)
 LOSS_KINDS = {"gaussian": 0, "poisson": 1, "bernoulli": 2}

@@ -13,11 +13,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libogcp_b200.so")
-OBJ = os.path.join(HERE, "..", "build", "obj")
+OUT = os.environ.get("OGCP_LIB_OUT", os.path.join(HERE, "libogcp_b200.so"))
+OBJ = os.environ.get("OGCP_OBJ_DIR", os.path.join(HERE, "..", "build", "obj"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xcompiler", "-fPIC",
-         "-Xcompiler", "-O3", "-Wno-deprecated-gpu-targets"]
+         "-Xcompiler", "-O3", "-Wno-deprecated-gpu-targets"] + os.environ.get("OGCP_NVCC_DEFS", "").split()
 
 
 def _newest(paths):

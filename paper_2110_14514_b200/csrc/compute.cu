@@ -5,7 +5,10 @@
 // lane gl owns the float4 chunks v*G+gl (v < V) of every factor row, so the
 // d row gathers of a sample are G*16-byte contiguous 128-bit loads (one 128 B
 // line per row at R = 32), the Hadamard product and the dot with s stay in
-// registers and m is reduced with log2(G) xor-shuffles.
+// registers and m is reduced with log2(G) xor-shuffles.  Each group works on
+// U samples at a time and issues the three dependent gather stages
+// (ordinal -> record -> factor rows) for all U before using any of them, so a
+// warp keeps 3*U*SPW independent 128-bit loads in flight.
 //
 // Reference: model_values tensor.py:203-211; LossFunction losses.py:58-78;
 // sampled_mttkrp kernels.py:33-56 (times s, solvers.py:139-140);
@@ -21,6 +24,10 @@ namespace ogcp {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;
+#ifndef OGCP_SAMPLE_U
+#define OGCP_SAMPLE_U 4
+#endif
+constexpr int kU = OGCP_SAMPLE_U;  // samples per lane group per pass
 
 template <int D>
 struct ND {
@@ -69,56 +76,185 @@ struct Sample {
   float4 a[ND<D>::v][V];
   float x;
   float scale;
+  bool nz;
 };
 
-// Load coordinates, value and the d factor-row chunks of sample n.
-template <int D, int G, int V>
-__device__ __forceinline__ void gather(int64_t n, bool valid, const SamplesP& S, const ModelP& M, int gl,
-                                       Sample<D, V>& s) {
-  constexpr int NDm = ND<D>::v;
-  const int nd = D > 0 ? D : M.ndim;
-  int t[8];
+// Software-pipelined sample stream.  A warp walks batches of SPW*U samples with
+// a grid stride; while the factor rows of batch b are in flight, the records
+// (or zero coordinates) of batch b+stride and the ordinals of batch b+2*stride
+// are already being fetched, so the three dependent gathers of a sample
+// (ordinal -> record -> rows) overlap across batches instead of serialising.
+template <int D, int G, int V, int U>
+struct SampleStream {
+  static constexpr int NDm = ND<D>::v;
+  static constexpr int SPW = 32 / G;
+  static constexpr int SPB = SPW * U;
+  static constexpr int RI = (D > 0 && D <= 3) ? 4 : 8;
+  SamplesP S;
+  const ModelP* M;
+  int64_t total, stride, b;
+  int lane, gl, nd;
+  int oB[U];
+  int tC[U][RI];
+
+  __device__ __forceinline__ int64_t nidx(int64_t base, int u) const { return base + u * SPW + lane / G; }
+
+  __device__ __forceinline__ void load_ord(int64_t base, int (&o)[U]) const {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) t[k] = 0;
-  s.x = 0.0f;
-  s.scale = 0.0f;
-  if (valid) {
-    if (n < S.p) {
-      const int o = __ldg(S.ord + n);
-      const int4* r = reinterpret_cast<const int4*>(S.rec + (int64_t)o * S.rec_ints);
+    for (int u = 0; u < U; ++u) {
+      const int64_t n = nidx(base, u);
+      o[u] = n < S.p ? __ldg(S.ord + n) : 0;
+    }
+  }
+
+  __device__ __forceinline__ void load_rec(int64_t base, const int (&o)[U], int (&t)[U][RI]) const {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t n = nidx(base, u);
+#pragma unroll
+      for (int k = 0; k < RI; ++k) t[u][k] = 0;
+      if (n < S.p) {
+        const int4* r = reinterpret_cast<const int4*>(S.rec + (int64_t)o[u] * S.rec_ints);
+        const int4 v0 = __ldg(r);
+        t[u][0] = v0.x; t[u][1] = v0.y; t[u][2] = v0.z; t[u][3] = v0.w;
+        if (RI == 8 && S.rec_ints == 8) {
+          const int4 v1 = __ldg(r + 1);
+          t[u][RI > 4 ? 4 : 0] = v1.x; t[u][RI > 4 ? 5 : 1] = v1.y;
+          t[u][RI > 4 ? 6 : 2] = v1.z; t[u][RI > 4 ? 7 : 3] = v1.w;
+        }
+      } else if (n < total) {
+        const int32_t* z = S.zsub + (n - S.p) * nd;
+#pragma unroll
+        for (int k = 0; k < NDm; ++k)
+          if (k < nd) t[u][k] = __ldg(z + k);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void init(const SamplesP& S_, const ModelP& M_, int lane_, int64_t warp,
+                                       int64_t nwarps) {
+    S = S_;
+    M = &M_;
+    total = S.p + S.q;
+    lane = lane_;
+    gl = lane & (G - 1);
+    nd = D > 0 ? D : M_.ndim;
+    stride = nwarps * SPB;
+    b = warp * SPB;
+    int o0[U];
+    load_ord(b, o0);
+    load_rec(b, o0, tC);
+    load_ord(b + stride, oB);
+  }
+
+  // Issue the row gathers of the current batch (and the next batches' earlier
+  // stages); returns false when the warp has no batch left.
+  __device__ __forceinline__ bool next(Sample<D, V> (&s)[U], bool (&valid)[U]) {
+    if (b >= total) return false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t n = nidx(b, u);
+      valid[u] = n < total;
+      s[u].nz = n < S.p;
+      s[u].scale = s[u].nz ? (float)S.nz_scale : (float)S.zero_scale;
+      float x = 0.0f;
+      if (D > 0) x = __int_as_float(tC[u][D < RI ? D : 0]);
+      else {
+#pragma unroll
+        for (int k = 0; k < RI; ++k)
+          if (k == nd) x = __int_as_float(tC[u][k]);
+      }
+      s[u].x = s[u].nz ? x : 0.0f;
+#pragma unroll
+      for (int k = 0; k < NDm; ++k) {
+        s[u].idx[k] = tC[u][k < RI ? k : 0];
+        if (k < nd) {
+          const float4* row = reinterpret_cast<const float4*>(M->A[k] + (int64_t)s[u].idx[k] * M->ldr);
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            s[u].a[k][v] = valid[u] ? __ldg(row + v * G + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) s[u].a[k][v] = make_float4(1.f, 1.f, 1.f, 1.f);
+        }
+      }
+    }
+    // stage 2 for the next batch, stage 1 for the one after
+    int tB[U][RI];
+    load_rec(b + stride, oB, tB);
+    load_ord(b + 2 * stride, oB);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < RI; ++k) tC[u][k] = tB[u][k];
+    b += stride;
+    return true;
+  }
+};
+
+// (unpipelined variant kept for reference-shaped small launches)
+template <int D, int G, int V, int U>
+__device__ __forceinline__ void gather_batch(int64_t base, int64_t total, const SamplesP& S, const ModelP& M,
+                                             int lane, Sample<D, V> (&s)[U], bool (&valid)[U]) {
+  constexpr int NDm = ND<D>::v;
+  constexpr int SPW = 32 / G;
+  const int nd = D > 0 ? D : M.ndim;
+  const int gl = lane & (G - 1);
+  int64_t n[U];
+  int o[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    n[u] = base + u * SPW + lane / G;
+    valid[u] = n[u] < total;
+    s[u].nz = valid[u] && n[u] < S.p;
+    o[u] = s[u].nz ? __ldg(S.ord + n[u]) : 0;
+  }
+  int t[U][8];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[u][k] = 0;
+    s[u].x = 0.0f;
+    s[u].scale = 0.0f;
+    if (s[u].nz) {
+      const int4* r = reinterpret_cast<const int4*>(S.rec + (int64_t)o[u] * S.rec_ints);
       int4 v0 = __ldg(r);
-      t[0] = v0.x; t[1] = v0.y; t[2] = v0.z; t[3] = v0.w;
+      t[u][0] = v0.x; t[u][1] = v0.y; t[u][2] = v0.z; t[u][3] = v0.w;
       if (D == 0 || D > 3) {
         if (S.rec_ints == 8) {
           int4 v1 = __ldg(r + 1);
-          t[4] = v1.x; t[5] = v1.y; t[6] = v1.z; t[7] = v1.w;
+          t[u][4] = v1.x; t[u][5] = v1.y; t[u][6] = v1.z; t[u][7] = v1.w;
         }
       }
-      if (D > 0) s.x = __int_as_float(t[D]);
+      if (D > 0) s[u].x = __int_as_float(t[u][D]);
       else {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          if (k == nd) s.x = __int_as_float(t[k]);
+          if (k == nd) s[u].x = __int_as_float(t[u][k]);
       }
-      s.scale = (float)S.nz_scale;
-    } else {
-      const int32_t* z = S.zsub + (n - S.p) * nd;
+      s[u].scale = (float)S.nz_scale;
+    } else if (valid[u]) {
+      const int32_t* z = S.zsub + (n[u] - S.p) * nd;
 #pragma unroll
       for (int k = 0; k < NDm; ++k)
-        if (k < nd) t[k] = __ldg(z + k);
-      s.scale = (float)S.zero_scale;
+        if (k < nd) t[u][k] = __ldg(z + k);
+      s[u].scale = (float)S.zero_scale;
     }
   }
 #pragma unroll
-  for (int k = 0; k < NDm; ++k) {
-    s.idx[k] = t[k];
-    if (k < nd) {
-      const float4* row = reinterpret_cast<const float4*>(M.A[k] + (int64_t)t[k] * M.ldr);
+  for (int u = 0; u < U; ++u) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) s.a[k][v] = valid ? __ldg(row + v * G + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
-    } else {
+    for (int k = 0; k < NDm; ++k) {
+      s[u].idx[k] = t[u][k];
+      if (k < nd) {
+        const float4* row = reinterpret_cast<const float4*>(M.A[k] + (int64_t)t[u][k] * M.ldr);
 #pragma unroll
-      for (int v = 0; v < V; ++v) s.a[k][v] = make_float4(1.f, 1.f, 1.f, 1.f);
+        for (int v = 0; v < V; ++v)
+          s[u].a[k][v] = valid[u] ? __ldg(row + v * G + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) s[u].a[k][v] = make_float4(1.f, 1.f, 1.f, 1.f);
+      }
     }
   }
 }
@@ -152,15 +288,15 @@ struct PrivP {
 
 template <int D, int G, int V>
 __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const float* __restrict__ s_f, LossP L,
-                                                    GradPtrs GP, PrivP PV,
-                                                    DevFlags* flags, long long code) {
+                                                    GradPtrs GP, PrivP PV, DevFlags* flags, long long code) {
   extern __shared__ float smem[];
   constexpr int NDm = ND<D>::v;
+  constexpr int SPB = (32 / G) * kU;
   const int nd = D > 0 ? D : M.ndim;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
-  for (int64_t i = threadIdx.x; i < (PV.nmodes ? PV.off[PV.nmodes - 1] + PV.len[PV.nmodes - 1] : 0); i += blockDim.x)
-    smem[i] = 0.0f;
+  const int64_t plen = PV.nmodes ? PV.off[PV.nmodes - 1] + PV.len[PV.nmodes - 1] : 0;
+  for (int64_t i = threadIdx.x; i < plen; i += blockDim.x) smem[i] = 0.0f;
   __syncthreads();
   float4 s4[V];
 #pragma unroll
@@ -169,41 +305,45 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
 #pragma unroll
   for (int k = 0; k < NDm; ++k) {
     priv_slot[k] = -1;
-    for (int j = 0; j < PV.nmodes; ++j)
-      if (PV.mode[j] == k) priv_slot[k] = j;
+#pragma unroll
+    for (int j = 0; j < kMaxModes; ++j)
+      if (j < PV.nmodes && PV.mode[j] == k) priv_slot[k] = j;
   }
   const int64_t total = S.p + S.q;
-  constexpr int SPW = 32 / G;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
-  for (int64_t base = warp * SPW; base < total; base += nwarps * SPW) {
-    const int64_t n = base + lane / G;
-    const bool valid = n < total;
-    Sample<D, V> s;
-    gather<D, G, V>(n, valid, S, M, gl, s);
-    const float m = model_value<D, G, V>(s, s4);
-    if (!valid) continue;
-    bits |= domain_bits(L.kind, m);
-    const float y = s.scale * dloss(L.kind, s.x, m, L.eps);
+  SampleStream<D, G, V, kU> stream;
+  stream.init(S, M, lane, warp, nwarps);
+  Sample<D, V> s[kU];
+  bool valid[kU];
+  while (stream.next(s, valid)) {
 #pragma unroll
-    for (int k = 0; k < NDm; ++k) {
-      if (k >= nd) break;
+    for (int u = 0; u < kU; ++u) {
+      const float m = model_value<D, G, V>(s[u], s4);
+      if (valid[u]) {
+        bits |= domain_bits(L.kind, m);
+        const float y = s[u].scale * dloss(L.kind, s[u].x, m, L.eps);
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        float4 c = make_float4(y * s4[v].x, y * s4[v].y, y * s4[v].z, y * s4[v].w);
+        for (int k = 0; k < NDm; ++k) {
+          if (k >= nd) break;
 #pragma unroll
-        for (int j = 0; j < NDm; ++j)
-          if (j != k && j < nd) c = mul4(c, s.a[j][v]);
-        const int64_t off = (int64_t)s.idx[k] * M.ldr + (v * G + gl) * 4;
-        if (priv_slot[k] >= 0) {
-          float* p = smem + PV.off[priv_slot[k]] + off;
-          atomicAdd(p + 0, c.x);
-          atomicAdd(p + 1, c.y);
-          atomicAdd(p + 2, c.z);
-          atomicAdd(p + 3, c.w);
-        } else {
-          red_add_v4(GP.g[k] + off, c);
+          for (int v = 0; v < V; ++v) {
+            float4 c = make_float4(y * s4[v].x, y * s4[v].y, y * s4[v].z, y * s4[v].w);
+#pragma unroll
+            for (int j = 0; j < NDm; ++j)
+              if (j != k && j < nd) c = mul4(c, s[u].a[j][v]);
+            const int64_t off = (int64_t)s[u].idx[k] * M.ldr + (v * G + gl) * 4;
+            if (priv_slot[k] >= 0) {
+              float* p = smem + PV.off[priv_slot[k]] + off;
+              atomicAdd(p + 0, c.x);
+              atomicAdd(p + 1, c.y);
+              atomicAdd(p + 2, c.z);
+              atomicAdd(p + 3, c.w);
+            } else {
+              red_add_v4(GP.g[k] + off, c);
+            }
+          }
         }
       }
     }
@@ -228,6 +368,7 @@ __global__ void __launch_bounds__(kThreads) k_wgrad(SamplesP S, ModelP M, const 
                                                     double* __restrict__ partials, DevFlags* flags, long long code) {
   __shared__ double red[kThreads / 32][4 * V * G];
   constexpr int NDm = ND<D>::v;
+  constexpr int SPB = (32 / G) * kU;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   float4 s4[V];
@@ -237,28 +378,41 @@ __global__ void __launch_bounds__(kThreads) k_wgrad(SamplesP S, ModelP M, const 
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v][0] = acc[v][1] = acc[v][2] = acc[v][3] = 0.0;
   const int64_t total = S.p + S.q;
-  constexpr int SPW = 32 / G;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
-  for (int64_t base = warp * SPW; base < total; base += nwarps * SPW) {
-    const int64_t n = base + lane / G;
-    const bool valid = n < total;
-    Sample<D, V> s;
-    gather<D, G, V>(n, valid, S, M, gl, s);
-    const float m = model_value<D, G, V>(s, s4);
-    if (!valid) continue;
-    bits |= domain_bits(L.kind, m);
-    const float y = s.scale * dloss(L.kind, s.x, m, L.eps);
+  SampleStream<D, G, V, kU> stream;
+  stream.init(S, M, lane, warp, nwarps);
+  Sample<D, V> s[kU];
+  bool valid[kU];
+  while (stream.next(s, valid)) {
+    float4 part[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) part[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const float m = model_value<D, G, V>(s[u], s4);
+      if (valid[u]) {
+        bits |= domain_bits(L.kind, m);
+        const float y = s[u].scale * dloss(L.kind, s[u].x, m, L.eps);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          float4 pr = s[u].a[0][v];
+#pragma unroll
+          for (int k = 1; k < NDm; ++k) pr = mul4(pr, s[u].a[k][v]);
+          part[v].x += y * pr.x;
+          part[v].y += y * pr.y;
+          part[v].z += y * pr.z;
+          part[v].w += y * pr.w;
+        }
+      }
+    }
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      float4 pr = s.a[0][v];
-#pragma unroll
-      for (int k = 1; k < NDm; ++k) pr = mul4(pr, s.a[k][v]);
-      acc[v][0] += (double)(y * pr.x);
-      acc[v][1] += (double)(y * pr.y);
-      acc[v][2] += (double)(y * pr.z);
-      acc[v][3] += (double)(y * pr.w);
+      acc[v][0] += (double)part[v].x;
+      acc[v][1] += (double)part[v].y;
+      acc[v][2] += (double)part[v].z;
+      acc[v][3] += (double)part[v].w;
     }
   }
   if (bits) report(flags, kFlagData, code, bits);
@@ -285,11 +439,13 @@ __global__ void __launch_bounds__(kThreads) k_wgrad(SamplesP S, ModelP M, const 
 }
 
 // ------------------------------------------------------------------ K6
-template <int D, int G, int V>
+// MODE 0: sum scale * f(x, m) (objective); MODE 1: sum f(x,m) - f(0,m) (exact-loss nonzero correction).
+template <int D, int G, int V, int MODE>
 __global__ void __launch_bounds__(kThreads) k_objective(SamplesP S, ModelP M, const float* __restrict__ s_f,
                                                         LossP L, double* __restrict__ partials, DevFlags* flags,
                                                         long long code) {
   __shared__ double red[kThreads / 32];
+  constexpr int SPB = (32 / G) * kU;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   float4 s4[V];
@@ -297,62 +453,28 @@ __global__ void __launch_bounds__(kThreads) k_objective(SamplesP S, ModelP M, co
   for (int v = 0; v < V; ++v) s4[v] = __ldg(reinterpret_cast<const float4*>(s_f) + v * G + gl);
   double acc_nz = 0.0, acc_z = 0.0;
   const int64_t total = S.p + S.q;
-  constexpr int SPW = 32 / G;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
-  for (int64_t base = warp * SPW; base < total; base += nwarps * SPW) {
-    const int64_t n = base + lane / G;
-    const bool valid = n < total;
-    Sample<D, V> s;
-    gather<D, G, V>(n, valid, S, M, gl, s);
-    const float m = model_value<D, G, V>(s, s4);
-    if (!valid || gl != 0) continue;
-    bits |= domain_bits(L.kind, m);
-    const double f = floss(L.kind, (double)s.x, (double)m, L.eps_d);
-    if (n < S.p) acc_nz += f;
-    else acc_z += f;
-  }
-  if (bits) report(flags, kFlagData, code, bits);
-  double acc = acc_nz * S.nz_scale + acc_z * S.zero_scale;
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-  if (lane == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int j = 0; j < kThreads / 32; ++j) t += red[j];
-    partials[blockIdx.x] = t;
-  }
-}
-
-// Exact loss: nonzero correction f(x,m) - f(0,m) over every stored entry.
-template <int D, int G, int V>
-__global__ void __launch_bounds__(kThreads) k_exact_nz(SamplesP S, ModelP M, const float* __restrict__ s_f,
-                                                       LossP L, double* __restrict__ partials, DevFlags* flags,
-                                                       long long code) {
-  __shared__ double red[kThreads / 32];
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  float4 s4[V];
+  SampleStream<D, G, V, kU> stream;
+  stream.init(S, M, lane, warp, nwarps);
+  Sample<D, V> s[kU];
+  bool valid[kU];
+  while (stream.next(s, valid)) {
 #pragma unroll
-  for (int v = 0; v < V; ++v) s4[v] = __ldg(reinterpret_cast<const float4*>(s_f) + v * G + gl);
-  double acc = 0.0;
-  const int64_t total = S.p;
-  constexpr int SPW = 32 / G;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned bits = 0;
-  for (int64_t base = warp * SPW; base < total; base += nwarps * SPW) {
-    const int64_t n = base + lane / G;
-    const bool valid = n < total;
-    Sample<D, V> s;
-    gather<D, G, V>(n, valid, S, M, gl, s);
-    const float m = model_value<D, G, V>(s, s4);
-    if (!valid || gl != 0) continue;
-    bits |= domain_bits(L.kind, m);
-    acc += floss(L.kind, (double)s.x, (double)m, L.eps_d) - floss(L.kind, 0.0, (double)m, L.eps_d);
+    for (int u = 0; u < kU; ++u) {
+      const float m = model_value<D, G, V>(s[u], s4);
+      if (valid[u] && gl == 0) {
+        bits |= domain_bits(L.kind, m);
+        double f = floss(L.kind, (double)s[u].x, (double)m, L.eps_d);
+        if (MODE == 1) f -= floss(L.kind, 0.0, (double)m, L.eps_d);
+        if (s[u].nz) acc_nz += f;
+        else acc_z += f;
+      }
+    }
   }
   if (bits) report(flags, kFlagData, code, bits);
+  double acc = MODE == 0 ? acc_nz * S.nz_scale + acc_z * S.zero_scale : acc_nz + acc_z;
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
   if (lane == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
@@ -407,49 +529,118 @@ __global__ void k_sum_partials_vec(const double* __restrict__ p, int nblk, int l
 }
 
 // ------------------------------------------------------------------ K4 Gram
-// out = B' A (R x R) ; each block reduces a row range in fp32 tiles of kGramTile
-// rows and accumulates tiles in fp64; partials summed in block order.
+// P = A'A and (optionally) C = B'A in one pass over the rows.  Work item =
+// (gram, 4x4 sub-block); a thread accumulates its sub-blocks over a row group
+// in fp32 per 32-row tile and in fp64 across tiles; row groups are reduced in
+// fixed order in shared memory, blocks by the finalize kernel.
 constexpr int kGramTile = 32;
-__global__ void __launch_bounds__(kThreads) k_gram(const float* __restrict__ A, const float* __restrict__ B,
-                                                   int64_t rows, int rank, int ldr, int64_t rows_per_block,
-                                                   double* __restrict__ partials) {
-  extern __shared__ float sm[];
-  float* sa = sm;
-  float* sb = sm + kGramTile * ldr;
-  const int RR = rank * rank;
+constexpr int kGramIPT = 2;
+__global__ void __launch_bounds__(kThreads) k_gram2(const float* __restrict__ A, const float* __restrict__ B,
+                                                    int64_t rows, int ldr, int ngram, int item0, int nitems_pass,
+                                                    int64_t rows_per_block, double* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  float* sa = reinterpret_cast<float*>(gsm);
+  float* sb = sa + kGramTile * ldr;
+  const int nsb = ldr / 4;
+  const int nsub = nsb * nsb;
+  const int nitems = ngram * nsub;
+  // thread -> (items, row group)
+  int nrg = 1, item_base = threadIdx.x;
+  if (nitems_pass < kThreads) {
+    nrg = kThreads / nitems_pass;
+    item_base = threadIdx.x % nitems_pass;
+  }
+  const int rg = nitems_pass < kThreads ? threadIdx.x / nitems_pass : 0;
+  const bool active = rg < nrg;
+  int gi[kGramIPT], bi[kGramIPT], bj[kGramIPT];
+  bool on[kGramIPT];
+#pragma unroll
+  for (int t = 0; t < kGramIPT; ++t) {
+    const int it = item0 + item_base + t * kThreads;
+    on[t] = active && (item_base + t * kThreads) < nitems_pass && it < nitems;
+    const int itc = on[t] ? it : 0;
+    gi[t] = itc / nsub;
+    bi[t] = (itc % nsub) / nsb;
+    bj[t] = (itc % nsub) % nsb;
+  }
+  double dacc[kGramIPT][16];
+#pragma unroll
+  for (int t = 0; t < kGramIPT; ++t)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) dacc[t][e] = 0.0;
   const int64_t r0 = blockIdx.x * rows_per_block;
   const int64_t r1 = min(rows, r0 + rows_per_block);
-  for (int e0 = 0; e0 < RR; e0 += 16 * kThreads) {
-    double acc[16];
-    int ei[16], ej[16];
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      int e = e0 + t * kThreads + threadIdx.x;
-      acc[t] = 0.0;
-      ei[t] = e < RR ? e / rank : -1;
-      ej[t] = e < RR ? e % rank : 0;
+  const bool has_b = ngram > 1;
+  for (int64_t rb = r0; rb < r1; rb += kGramTile) {
+    const int nr = (int)min((int64_t)kGramTile, r1 - rb);
+    __syncthreads();
+    const int nv = nr * ldr / 4;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+      reinterpret_cast<float4*>(sa)[i] = __ldg(reinterpret_cast<const float4*>(A + rb * ldr) + i);
+      if (has_b) reinterpret_cast<float4*>(sb)[i] = __ldg(reinterpret_cast<const float4*>(B + rb * ldr) + i);
     }
-    for (int64_t rb = r0; rb < r1; rb += kGramTile) {
-      const int nr = (int)min((int64_t)kGramTile, r1 - rb);
-      __syncthreads();
-      for (int i = threadIdx.x; i < nr * ldr; i += blockDim.x) {
-        sa[i] = A[rb * ldr + i];
-        sb[i] = B[rb * ldr + i];
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < kGramIPT; ++t) {
+      if (!on[t]) continue;
+      float acc[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+      const float* lhs = gi[t] == 0 ? sa : sb;
+      for (int r = rg; r < nr; r += nrg) {
+        const float4 l = reinterpret_cast<const float4*>(lhs + r * ldr)[bi[t]];
+        const float4 a = reinterpret_cast<const float4*>(sa + r * ldr)[bj[t]];
+        const float lv[4] = {l.x, l.y, l.z, l.w};
+        const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[ii * 4 + jj] += lv[ii] * av[jj];
       }
-      __syncthreads();
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        if (ei[t] < 0) continue;
-        float f = 0.0f;
-        for (int r = 0; r < nr; ++r) f += sb[r * ldr + ei[t]] * sa[r * ldr + ej[t]];
-        acc[t] += (double)f;
-      }
+      for (int e = 0; e < 16; ++e) dacc[t][e] += (double)acc[e];
     }
+  }
+  // reduce row groups in fixed order through shared memory
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(gsm);
+  const int LL = ldr * ldr;
 #pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      int e = e0 + t * kThreads + threadIdx.x;
-      if (e < RR) partials[blockIdx.x * (int64_t)RR + e] = acc[t];
+  for (int t = 0; t < kGramIPT; ++t) {
+    if (nrg > 1 && on[t]) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) red[(rg * nitems_pass + item_base) * 16 + e] = dacc[t][e];
     }
+  }
+  if (nrg > 1) __syncthreads();
+#pragma unroll
+  for (int t = 0; t < kGramIPT; ++t) {
+    if (!on[t] || rg != 0) continue;
+    double v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = dacc[t][e];
+    for (int g2 = 1; g2 < nrg; ++g2)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] += red[(g2 * nitems_pass + item_base) * 16 + e];
+    double* out = partials + ((int64_t)blockIdx.x * ngram + gi[t]) * LL;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) out[(bi[t] * 4 + ii) * ldr + bj[t] * 4 + jj] = v[ii * 4 + jj];
+  }
+}
+
+// Sum block partials (fixed order) and extract the rank x rank blocks.
+__global__ void k_gram_finalize(const double* __restrict__ partials, int nblk, int ngram, int ldr, int rank,
+                                double* __restrict__ outP, double* __restrict__ outC) {
+  const int LL = ldr * ldr;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ngram * rank * rank; e += gridDim.x * blockDim.x) {
+    const int g = e / (rank * rank);
+    const int ij = e % (rank * rank);
+    const int i = ij / rank, j = ij % rank;
+    double t = 0.0;
+    for (int b = 0; b < nblk; ++b) t += partials[((int64_t)b * ngram + g) * LL + i * ldr + j];
+    (g == 0 ? outP : outC)[ij] = t;
   }
 }
 
@@ -473,15 +664,97 @@ __global__ void k_hist_coeffs(int ndim, int rank, const double* __restrict__ P, 
 }
 
 // ------------------------------------------------------------------ K5
-// One warp-group of GR lanes per row; columns c = gl + j*GR.
+// g = G + lambda*a + (A Mk - Aold Nk)[row]; Adam in fp32 (the storage
+// precision) with 1-beta passed from fp64; the clamp keeps NaN so the
+// _ensure_finite semantics (solvers.py:188-194) are preserved.
+__device__ __forceinline__ bool adam_elem(float* __restrict__ A, float* __restrict__ u, float* __restrict__ v,
+                                          int64_t at, float a, float gval, float b1, float omb1, float b2,
+                                          float omb2, float rate_i, float eps, float lower) {
+  const float un = b1 * u[at] + omb1 * gval;
+  const float vn = b2 * v[at] + (omb2 * gval) * gval;
+  float an = a - rate_i * un / (sqrtf(vn) + eps);
+  if (an < lower) an = lower;
+  u[at] = un;
+  v[at] = vn;
+  A[at] = an;
+  return isfinite(an);
+}
+
+// rank <= 32: one group of GR lanes per row, lane c owns column c and keeps
+// column c of Mk and Nk in registers; rows of A / Aold are broadcast across the
+// group with shuffles.  Two rows per group per pass keep 10 loads in flight.
 template <int GR>
 __global__ void __launch_bounds__(kThreads) k_factor_update(int64_t rows, int rank, int ldr, float* __restrict__ A,
                                                             const float* __restrict__ Aold,
                                                             const float* __restrict__ G, float* __restrict__ u,
                                                             float* __restrict__ v, const float* __restrict__ Mk,
-                                                            const float* __restrict__ Nk, double reg, double rate_i,
-                                                            double b1, double b2, double eps, double lower,
-                                                            DevFlags* flags, long long code) {
+                                                            const float* __restrict__ Nk, float reg, float rate_i,
+                                                            float b1, float omb1, float b2, float omb2, float eps,
+                                                            float lower, DevFlags* flags, long long code) {
+  constexpr int RPI = 2;
+  const bool hist = Mk != nullptr;
+  const int lane = threadIdx.x & 31;
+  const int c = lane & (GR - 1);
+  const bool col_on = c < rank;
+  float mcol[GR], ncol[GR];
+#pragma unroll
+  for (int r = 0; r < GR; ++r) {
+    mcol[r] = (hist && r < rank && col_on) ? __ldg(Mk + r * rank + c) : 0.f;
+    ncol[r] = (hist && r < rank && col_on) ? __ldg(Nk + r * rank + c) : 0.f;
+  }
+  const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GR;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / GR;
+  bool bad = false;
+  const int64_t span = ngrp * RPI;
+  const int64_t rows_pad = ((rows + span - 1) / span) * span;
+  for (int64_t i0 = grp * RPI; i0 < rows_pad; i0 += span) {
+    float a[RPI], ao[RPI], gv[RPI];
+    bool ok[RPI];
+#pragma unroll
+    for (int q = 0; q < RPI; ++q) {
+      const int64_t i = i0 + q;
+      ok[q] = i < rows && col_on;
+      const int64_t at = i * ldr + c;
+      a[q] = ok[q] ? A[at] : 0.f;
+      ao[q] = (ok[q] && hist) ? __ldg(Aold + at) : 0.f;
+      gv[q] = ok[q] ? __ldg(G + at) : 0.f;
+    }
+    if (hist) {
+      float h[RPI];
+#pragma unroll
+      for (int q = 0; q < RPI; ++q) h[q] = 0.f;
+#pragma unroll
+      for (int r = 0; r < GR; ++r) {
+#pragma unroll
+        for (int q = 0; q < RPI; ++q) {
+          const float ar = __shfl_sync(kFull, a[q], r, GR);
+          const float aor = __shfl_sync(kFull, ao[q], r, GR);
+          h[q] += ar * mcol[r] - aor * ncol[r];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < RPI; ++q) gv[q] += h[q];
+    }
+#pragma unroll
+    for (int q = 0; q < RPI; ++q)
+      if (ok[q] && !adam_elem(A, u, v, (i0 + q) * ldr + c, a[q], gv[q] + reg * a[q], b1, omb1, b2, omb2, rate_i,
+                              eps, lower))
+        bad = true;
+  }
+  if (bad) report(flags, kFlagDiverge, code, 0);
+}
+
+// rank > 32: one warp per row, CPL columns per lane, Mk / Nk in shared memory.
+template <int CPL>
+__global__ void __launch_bounds__(kThreads) k_factor_update_wide(int64_t rows, int rank, int ldr,
+                                                                 float* __restrict__ A,
+                                                                 const float* __restrict__ Aold,
+                                                                 const float* __restrict__ G, float* __restrict__ u,
+                                                                 float* __restrict__ v, const float* __restrict__ Mk,
+                                                                 const float* __restrict__ Nk, float reg,
+                                                                 float rate_i, float b1, float omb1, float b2,
+                                                                 float omb2, float eps, float lower, DevFlags* flags,
+                                                                 long long code) {
   extern __shared__ float sm[];
   const bool hist = Mk != nullptr;
   const int RR = rank * rank;
@@ -492,12 +765,9 @@ __global__ void __launch_bounds__(kThreads) k_factor_update(int64_t rows, int ra
     }
   }
   __syncthreads();
-  constexpr int CPL = GR < 32 ? 1 : 8;  // columns per lane (rank <= GR, or <= 256 at GR = 32)
   const int lane = threadIdx.x & 31;
-  const int gl = lane & (GR - 1);
-  const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GR;
-  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / GR;
-  const int ncpl = (rank + GR - 1) / GR;
+  const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / 32;
   bool bad = false;
   const int64_t rows_pad = ((rows + ngrp - 1) / ngrp) * ngrp;
   for (int64_t i = grp; i < rows_pad; i += ngrp) {
@@ -505,41 +775,37 @@ __global__ void __launch_bounds__(kThreads) k_factor_update(int64_t rows, int ra
     float a[CPL], ao[CPL];
 #pragma unroll
     for (int j = 0; j < CPL; ++j) {
-      const int c = gl + j * GR;
-      a[j] = (j < ncpl && c < rank && valid) ? A[i * ldr + c] : 0.f;
-      ao[j] = (hist && j < ncpl && c < rank && valid) ? Aold[i * ldr + c] : 0.f;
+      const int cc = lane + j * 32;
+      a[j] = (cc < rank && valid) ? A[i * ldr + cc] : 0.f;
+      ao[j] = (hist && cc < rank && valid) ? Aold[i * ldr + cc] : 0.f;
+    }
+    float h[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) h[j] = 0.f;
+    if (hist) {
+#pragma unroll
+      for (int jj = 0; jj < CPL; ++jj) {
+        for (int src = 0; src < 32; ++src) {
+          const int r = jj * 32 + src;
+          const float ar = __shfl_sync(kFull, a[jj], src);
+          const float aor = __shfl_sync(kFull, ao[jj], src);
+          if (r < rank) {
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) {
+              const int cc = lane + j * 32;
+              if (cc < rank) h[j] += ar * sm[r * rank + cc] - aor * sm[RR + r * rank + cc];
+            }
+          }
+        }
+      }
     }
 #pragma unroll
     for (int j = 0; j < CPL; ++j) {
-      const int c = gl + j * GR;
-      if (j >= ncpl) break;
-      float hsum = 0.0f;
-      if (hist) {
-        // (A Mk)[c] - (Aold Nk)[c] = sum_r a[r] Mk[r][c] - ao[r] Nk[r][c]
-        for (int r = 0; r < rank; ++r) {
-          const int src = r % GR, slot = r / GR;
-          float ar = 0.f, aor = 0.f;
-#pragma unroll
-          for (int jj = 0; jj < CPL; ++jj)
-            if (jj == slot) {
-              ar = __shfl_sync(kFull, a[jj], src, GR);
-              aor = __shfl_sync(kFull, ao[jj], src, GR);
-            }
-          if (c < rank) hsum += ar * sm[r * rank + c] - aor * sm[RR + r * rank + c];
-        }
-      }
-      if (!valid || c >= rank) continue;
-      const int64_t at = i * ldr + c;
-      const double g = (double)G[at] + reg * (double)a[j] + (double)hsum;
-      const double un = b1 * (double)u[at] + (1.0 - b1) * g;
-      const double vn = b2 * (double)v[at] + (1.0 - b2) * g * g;
-      double an = (double)a[j] - rate_i * un / (sqrt(vn) + eps);
-      an = fmax(an, lower);
-      const float af = (float)an;
-      u[at] = (float)un;
-      v[at] = (float)vn;
-      A[at] = af;
-      if (!isfinite(af)) bad = true;
+      const int cc = lane + j * 32;
+      if (!valid || cc >= rank) continue;
+      const int64_t at = i * ldr + cc;
+      if (!adam_elem(A, u, v, at, a[j], G[at] + reg * a[j] + h[j], b1, omb1, b2, omb2, rate_i, eps, lower))
+        bad = true;
     }
   }
   if (bad) report(flags, kFlagDiverge, code, 0);
@@ -562,7 +828,8 @@ __global__ void k_weight_step(const double* __restrict__ partials, int nblk, int
   g += mu * s;
   double u = b1 * ws[ldr + r] + (1.0 - b1) * g;
   double v = b2 * ws[2 * ldr + r] + (1.0 - b2) * g * g;
-  double sn = fmax(s - rate_i * u / (sqrt(v) + eps), lower);
+  double sn = s - rate_i * u / (sqrt(v) + eps);
+  if (sn < lower) sn = lower;
   ws[r] = sn;
   ws[ldr + r] = u;
   ws[2 * ldr + r] = v;
@@ -592,7 +859,6 @@ __global__ void k_hist_penalty(int ndim, int rank, const double* __restrict__ Po
   __syncthreads();
   __shared__ double red[32];
   double tot = 0.0;
-  // one warp per window entry, fixed order of accumulation per warp then warps in order
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   double wsum = 0.0;
   for (int h = w; h < H; h += nw) {
@@ -611,19 +877,16 @@ __global__ void k_hist_penalty(int ndim, int rank, const double* __restrict__ Po
 }
 
 // ==================================================================== host side
-template <class F>
-static void dispatch_dgv(int ndim, int ldr, F&& f);
-
-#define OGCP_DISPATCH_LDR(D)                                        \
-  switch (ldr) {                                                    \
-    case 4: f(std::integral_constant<int, D>(), std::integral_constant<int, 1>(), std::integral_constant<int, 1>()); break;  \
-    case 8: f(std::integral_constant<int, D>(), std::integral_constant<int, 2>(), std::integral_constant<int, 1>()); break;  \
-    case 16: f(std::integral_constant<int, D>(), std::integral_constant<int, 4>(), std::integral_constant<int, 1>()); break; \
-    case 32: f(std::integral_constant<int, D>(), std::integral_constant<int, 8>(), std::integral_constant<int, 1>()); break; \
+#define OGCP_DISPATCH_LDR(D)                                                                                    \
+  switch (ldr) {                                                                                                \
+    case 4: f(std::integral_constant<int, D>(), std::integral_constant<int, 1>(), std::integral_constant<int, 1>()); break;   \
+    case 8: f(std::integral_constant<int, D>(), std::integral_constant<int, 2>(), std::integral_constant<int, 1>()); break;   \
+    case 16: f(std::integral_constant<int, D>(), std::integral_constant<int, 4>(), std::integral_constant<int, 1>()); break;  \
+    case 32: f(std::integral_constant<int, D>(), std::integral_constant<int, 8>(), std::integral_constant<int, 1>()); break;  \
     case 64: f(std::integral_constant<int, D>(), std::integral_constant<int, 16>(), std::integral_constant<int, 1>()); break; \
     case 128: f(std::integral_constant<int, D>(), std::integral_constant<int, 32>(), std::integral_constant<int, 1>()); break; \
     case 256: f(std::integral_constant<int, D>(), std::integral_constant<int, 32>(), std::integral_constant<int, 2>()); break; \
-    default: throw Error(OGCP_E_USAGE, "unsupported padded rank " + std::to_string(ldr));                  \
+    default: throw Error(OGCP_E_USAGE, "unsupported padded rank " + std::to_string(ldr));                    \
   }
 
 template <class F>
@@ -636,9 +899,15 @@ static void dispatch_dgv(int ndim, int ldr, F&& f) {
   }
 }
 
-static int sample_grid(int64_t total, int G, int per_sm) {
-  const int64_t groups_per_block = kThreads / G;
-  const int64_t need = (total + groups_per_block - 1) / groups_per_block;
+// Grid for a grid-stride sample kernel: enough blocks to cover the samples once,
+// capped at the number that can be co-resident (occupancy API).
+template <class K>
+static int sample_grid(K kern, size_t smem, int64_t total, int G) {
+  int per_sm = 0;
+  OGCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  per_sm = std::max(per_sm, 1);
+  const int64_t per_block = (int64_t)(kThreads / G) * kU;
+  const int64_t need = (total + per_block - 1) / per_block;
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)kNumSMs * per_sm));
 }
 
@@ -650,7 +919,7 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
     OGCP_CUDA(cudaMemsetAsync(grads[k], 0, (size_t)M.dims[k] * M.ldr * 4, ctx->stream));
   const int64_t total = S.p + S.q;
   if (total == 0) return;
-  // privatise small modes in shared memory
+  // privatise small modes in shared memory when the per-CTA flush is cheap
   PrivP PV;
   PV.nmodes = 0;
   int64_t used = 0;
@@ -672,8 +941,7 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
     auto kern = k_sgrad<D, G, V>;
     if (smem > 48 * 1024) OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int per_sm = smem > 0 ? std::max(1, (int)(200 * 1024 / std::max<size_t>(smem, 1))) : 8;
-    const int grid = sample_grid(total, G, std::min(per_sm, 8));
+    const int grid = sample_grid(kern, smem, total, G);
     kern<<<grid, kThreads, smem, ctx->stream>>>(S, M, s_f, L, GP, PV, ctx->flags.as<DevFlags>(), code);
   });
   ctx->count();
@@ -687,8 +955,26 @@ int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f
   ProfScope prof_scope(ctx, kProfWgrad);
   dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
-    grid = sample_grid(std::max<int64_t>(total, 1), G, 4);
-    k_wgrad<D, G, V><<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(), code);
+    auto kern = k_wgrad<D, G, V>;
+    grid = sample_grid(kern, 0, std::max<int64_t>(total, 1), G);
+    kern<<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(), code);
+  });
+  ctx->count();
+  check_launch();
+  return grid;
+}
+
+template <int MODE>
+static int objective_like(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                          double* partials, long long code) {
+  const int64_t total = S.p + S.q;
+  int grid = 1;
+  ProfScope prof_scope(ctx, kProfObjective);
+  dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
+    constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
+    auto kern = k_objective<D, G, V, MODE>;
+    grid = sample_grid(kern, 0, std::max<int64_t>(total, 1), G);
+    kern<<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(), code);
   });
   ctx->count();
   check_launch();
@@ -697,32 +983,12 @@ int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f
 
 int objective_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
                       double* partials, long long code) {
-  const int64_t total = S.p + S.q;
-  int grid = 1;
-  dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
-    constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
-    grid = sample_grid(std::max<int64_t>(total, 1), G, 4);
-    ProfScope prof_scope(ctx, kProfObjective);
-    k_objective<D, G, V><<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(),
-                                                             code);
-  });
-  ctx->count();
-  check_launch();
-  return grid;
+  return objective_like<0>(ctx, S, M, s_f, L, partials, code);
 }
 
 int exact_nz_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
                      double* partials, long long code) {
-  int grid = 1;
-  dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
-    constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
-    grid = sample_grid(std::max<int64_t>(S.p, 1), G, 4);
-    k_exact_nz<D, G, V><<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(),
-                                                            code);
-  });
-  ctx->count();
-  check_launch();
-  return grid;
+  return objective_like<1>(ctx, S, M, s_f, L, partials, code);
 }
 
 int exact_cells_enqueue(Ctx* ctx, const ModelP& M, const float* s_f, const LossP& L, int64_t omega,
@@ -741,20 +1007,45 @@ void sum_partials_enqueue(Ctx* ctx, const double* partials, int nblk, int len, d
   check_launch();
 }
 
-void gram_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* out,
-                  DevBuf& scratch) {
-  const int RR = rank * rank;
-  int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, kNumSMs * 2));
+void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* outP,
+                   double* outC, DevBuf& scratch) {
+  const int ngram = B ? 2 : 1;
+  const int nsub = (ldr / 4) * (ldr / 4);
+  const int nitems = ngram * nsub;
+  const int per_pass = kGramIPT * kThreads;
+  int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 127) / 128, kNumSMs * 2));
   const int64_t rpb = (rows + nblk - 1) / nblk;
   nblk = (int)std::max<int64_t>(1, (rows + rpb - 1) / rpb);
-  scratch.ensure((size_t)nblk * RR * 8);
-  const size_t smem = (size_t)2 * kGramTile * ldr * 4;
-  if (smem > 48 * 1024) OGCP_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  scratch.ensure((size_t)nblk * ngram * ldr * ldr * 8);
+  size_t smem = (size_t)2 * kGramTile * ldr * 4;
+  smem = std::max(smem, (size_t)kThreads * 16 * 8);
+  if (smem > 48 * 1024)
+    OGCP_CUDA(cudaFuncSetAttribute(k_gram2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfScope prof_scope(ctx, kProfGram);
-  k_gram<<<nblk, kThreads, smem, ctx->stream>>>(A, B, rows, rank, ldr, rpb, scratch.as<double>());
+  for (int item0 = 0; item0 < nitems; item0 += per_pass) {
+    const int n_pass = std::min(per_pass, nitems - item0);
+    // for small passes each thread owns one item and row groups split the rows
+    const int npass_items = n_pass <= kThreads ? n_pass : n_pass;
+    k_gram2<<<nblk, kThreads, smem, ctx->stream>>>(A, B ? B : A, rows, ldr, ngram, item0, npass_items, rpb,
+                                                   scratch.as<double>());
+    ctx->count();
+  }
+  k_gram_finalize<<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
+                    ctx->stream>>>(scratch.as<double>(), nblk, ngram, ldr, rank, outP, outC);
   ctx->count();
   check_launch();
-  sum_partials_enqueue(ctx, scratch.as<double>(), nblk, RR, out);
+}
+
+void gram_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* out,
+                  DevBuf& scratch) {
+  // out = B'A : run the pair kernel with (A, B) and keep the cross Gram
+  if (A == B) {
+    gram2_enqueue(ctx, A, nullptr, rows, rank, ldr, out, nullptr, scratch);
+  } else {
+    static thread_local DevBuf tmp;
+    tmp.ensure((size_t)rank * rank * 8);
+    gram2_enqueue(ctx, A, B, rows, rank, ldr, tmp.as<double>(), out, scratch);
+  }
 }
 
 void hist_coeffs_enqueue(Ctx* ctx, int ndim, int rank, const double* P, const double* C, const double* S,
@@ -769,24 +1060,43 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
                            double reg, double rate_i, double beta1, double beta2, double eps, double lower,
                            long long code) {
   if (rows <= 0) return;
-  const size_t smem = Mk ? (size_t)2 * rank * rank * 4 : 0;
-  int GR = 1;
-  while (GR < rank && GR < 32) GR <<= 1;
   ProfScope prof_scope(ctx, kProfUpdate);
-  auto launch = [&](auto kern) {
-    if (smem > 48 * 1024) OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t groups = kThreads / GR;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + groups - 1) / groups, kNumSMs * 8));
-    kern<<<grid, kThreads, smem, ctx->stream>>>(rows, rank, ldr, A, Aold, G, u, v, Mk, Nk, reg, rate_i, beta1, beta2,
-                                                eps, lower, ctx->flags.as<DevFlags>(), code);
-  };
-  switch (GR) {
-    case 1: launch(k_factor_update<1>); break;
-    case 2: launch(k_factor_update<2>); break;
-    case 4: launch(k_factor_update<4>); break;
-    case 8: launch(k_factor_update<8>); break;
-    case 16: launch(k_factor_update<16>); break;
-    default: launch(k_factor_update<32>); break;
+  const float fb1 = (float)beta1, fomb1 = (float)(1.0 - beta1), fb2 = (float)beta2, fomb2 = (float)(1.0 - beta2);
+  if (rank <= 32) {
+    int GR = 1;
+    while (GR < rank) GR <<= 1;
+    auto launch = [&](auto kern) {
+      int per_sm = 0;
+      OGCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
+      const int64_t rows_per_block = (kThreads / GR) * 2;
+      const int grid = (int)std::max<int64_t>(
+          1, std::min<int64_t>((rows + rows_per_block - 1) / rows_per_block, (int64_t)kNumSMs * std::max(per_sm, 1)));
+      kern<<<grid, kThreads, 0, ctx->stream>>>(rows, rank, ldr, A, Aold, G, u, v, Mk, Nk, (float)reg, (float)rate_i,
+                                               fb1, fomb1, fb2, fomb2, (float)eps, (float)lower,
+                                               ctx->flags.as<DevFlags>(), code);
+    };
+    switch (GR) {
+      case 1: launch(k_factor_update<1>); break;
+      case 2: launch(k_factor_update<2>); break;
+      case 4: launch(k_factor_update<4>); break;
+      case 8: launch(k_factor_update<8>); break;
+      case 16: launch(k_factor_update<16>); break;
+      default: launch(k_factor_update<32>); break;
+    }
+  } else {
+    const size_t smem = Mk ? (size_t)2 * rank * rank * 4 : 0;
+    auto launch = [&](auto kern) {
+      if (smem > 48 * 1024)
+        OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int64_t groups = kThreads / 32;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + groups - 1) / groups, kNumSMs * 4));
+      kern<<<grid, kThreads, smem, ctx->stream>>>(rows, rank, ldr, A, Aold, G, u, v, Mk, Nk, (float)reg,
+                                                  (float)rate_i, fb1, fomb1, fb2, fomb2, (float)eps, (float)lower,
+                                                  ctx->flags.as<DevFlags>(), code);
+    };
+    if (rank <= 64) launch(k_factor_update_wide<2>);
+    else if (rank <= 128) launch(k_factor_update_wide<4>);
+    else launch(k_factor_update_wide<8>);
   }
   ctx->count();
   check_launch();

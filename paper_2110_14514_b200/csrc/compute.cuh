@@ -46,6 +46,9 @@ void sum_partials_enqueue(Ctx* ctx, const double* partials, int nblk, int len, d
 // K4: out[R x R] = B' A over rows (fp64 accumulation), A/B rows x ldr.
 void gram_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* out,
                   DevBuf& scratch);
+// K4 pair: outP = A'A and (B != nullptr) outC = B'A in one pass over the rows.
+void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* outP,
+                   double* outC, DevBuf& scratch);
 // History coefficients: Mk = w*(hadamard_{m!=k} P_m) o S, Nk = w*(hadamard_{m!=k} C_m) o S  (float [d][R][R]).
 void hist_coeffs_enqueue(Ctx* ctx, int ndim, int rank, const double* P, const double* C, const double* S,
                          double w, float* Mk, float* Nk);

@@ -209,6 +209,14 @@ static void grams_enqueue(Ctx* ctx, const ModelP& M, float* const* other, double
   }
 }
 
+// P_m = A_m'A_m and C_m = Aold_m'A_m for every mode, one pass over each A_m.
+static void grams_pc_enqueue(Ctx* ctx, const ModelP& M, float* const* old, HistBufs& hb) {
+  const int RR = M.rank * M.rank;
+  for (int k = 0; k < M.ndim; ++k)
+    gram2_enqueue(ctx, M.A[k], old[k], M.dims[k], M.rank, M.ldr, hb.P.as<double>() + (int64_t)k * RR,
+                  hb.C.as<double>() + (int64_t)k * RR, hb.scratch);
+}
+
 // Device objective for a fixed sample set: returns data term + history + regs.
 struct ObjectiveParts {
   double data = 0, hist = 0, trace = 0;
@@ -396,13 +404,13 @@ static double factor_objective(Ctx* ctx, const Slice* X, const SamplesP& So, con
   const bool hist = cfg->hist_weight != 0.0 && H > 0;
   const bool reg = cfg->reg_factors != 0.0;
   if (hist || reg) {
-    grams_enqueue(ctx, M, nullptr, hb.P.as<double>(), hb, true);
+    if (hist) grams_pc_enqueue(ctx, M, old_factors, hb);
+    else grams_enqueue(ctx, M, nullptr, hb.P.as<double>(), hb, true);
     if (reg) {
       k_trace_sum<<<1, 1, 0, st>>>(M.ndim, M.rank, hb.P.as<double>(), dsc + 2);
       ctx->count();
     }
     if (hist) {
-      grams_enqueue(ctx, M, old_factors, hb.C.as<double>(), hb, false);
       hist_penalty_enqueue(ctx, M.ndim, M.rank, hb.Poo.as<double>(), hb.C.as<double>(), hb.P.as<double>(),
                            hb.Ws.as<double>(), hb.coef.as<double>(), H, dsc + 1);
     }
@@ -450,8 +458,7 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
   }
   sgrad_enqueue(ctx, Sg, M, s_f, L, gp, code_of(ev, 1));
   if (hist) {
-    grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true);
-    grams_enqueue(ctx, M, old_factors, W.hb.C.as<double>(), W.hb, false);
+    grams_pc_enqueue(ctx, M, old_factors, W.hb);
     hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), W.hb.C.as<double>(), W.hb.S.as<double>(),
                         cfg->hist_weight, W.hb.Mk.as<float>(), W.hb.Nk.as<float>());
   }
@@ -810,15 +817,12 @@ int ogcp_factor_gradients(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ord
     k_window_matrix<<<1, 256, 0, ctx->stream>>>(M.rank, H, W.hb.Ws.as<double>(), W.hb.coef.as<double>(),
                                                 W.hb.S.as<double>());
     ctx->count();
-    grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true);
-    grams_enqueue(ctx, M, old_factors, W.hb.C.as<double>(), W.hb, false);
+    grams_pc_enqueue(ctx, M, old_factors, W.hb);
     hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), W.hb.C.as<double>(), W.hb.S.as<double>(),
                         hist_weight, W.hb.Mk.as<float>(), W.hb.Nk.as<float>());
   }
-  // G += lambda A + history, via the K5 kernel with Adam disabled is not
-  // possible; use a dedicated pass: rate 0 Adam would still touch u/v, so we
-  // apply the terms with the same kernel on scratch moments and beta1 = 0,
-  // beta2 = 0, rate = 0: u' = g is the assembled gradient.
+  // G += lambda A + history: run the K5 kernel on scratch moments with
+  // beta1 = 0 and rate 0, so its first moment u' = g is the assembled gradient.
   for (int k = 0; k < M.ndim; ++k) {
     DevBuf& tmp = W.hb.tmp;
     const size_t n = (size_t)M.dims[k] * M.ldr;

@@ -10,7 +10,13 @@
 // "start column c -> number of elements emitted" (NCOL entries).  Maps compose
 // associatively, so one parallel scan gives every chunk its start column and
 // output offset, and a second pass re-generates the words and writes the
-// accepted values in place.  The nonzero stratum is the NCOL = 1 case.
+// accepted values.  The nonzero stratum is the NCOL = 1 case.
+//
+// Each block covers kScanThreads consecutive chunks.  Its first thread jumps
+// the LCG to the block's first word (O(log n) 128-bit multiply-adds against a
+// power-of-two table); every thread then applies a precomputed local jump of
+// tid*kChunkWords/2 steps.  Accepted values are staged in shared memory and
+// written to HBM with coalesced stores.
 //
 // Zero stratum (sampling.py:133-150): rejection rounds of `need` candidate
 // rows continue the same word stream, so the accepted zeros are exactly the
@@ -25,15 +31,21 @@
 
 namespace ogcp {
 
-constexpr int kChunkWords = 128;   // words per thread-chunk (CW)
+constexpr int kChunkWords = 32;    // words per thread-chunk
 constexpr int kScanThreads = 256;  // chunks per block
+constexpr int kBlockWords = kChunkWords * kScanThreads;
 constexpr int kMaxCols = 7;
+constexpr int kRowsPerThread = 8;  // zero-candidate rows per thread in the hit/compact passes
+constexpr int kRowsPerBlock = kRowsPerThread * kScanThreads;
 
 struct JumpTable {
   u128 A[64];
   u128 B[64];
 };
 __constant__ JumpTable c_jump;
+// local jumps by t * kChunkWords/2 LCG steps, t < kScanThreads
+__device__ u128 g_local_A[kScanThreads];
+__device__ u128 g_local_B[kScanThreads];
 
 void init_jump_table() {
   static bool done[64] = {false};
@@ -50,6 +62,14 @@ void init_jump_table() {
     cur = jump_compose(cur, cur);
   }
   OGCP_CUDA(cudaMemcpyToSymbol(c_jump, &h, sizeof(h)));
+  std::vector<u128> la(kScanThreads), lb(kScanThreads);
+  for (int t = 0; t < kScanThreads; ++t) {
+    Jump j = jump_pow((uint64_t)t * (kChunkWords / 2));
+    la[t] = j.A;
+    lb[t] = j.B;
+  }
+  OGCP_CUDA(cudaMemcpyToSymbol(g_local_A, la.data(), sizeof(u128) * kScanThreads));
+  OGCP_CUDA(cudaMemcpyToSymbol(g_local_B, lb.data(), sizeof(u128) * kScanThreads));
   if (dev >= 0 && dev < 64) done[dev] = true;
 }
 
@@ -60,25 +80,25 @@ struct StreamSpec {
   uint32_t thr[kMaxCols];
 };
 
-// Word generator positioned at word index w of a fresh Generator.
+// LCG state after `steps` steps from the seeded state (power-of-two table).
+__device__ __forceinline__ u128 state_after(const StreamSpec& sp, uint64_t steps) {
+  const u128 s0 = ((u128)sp.st_hi << 64) | sp.st_lo;
+  const u128 inc = ((u128)sp.inc_hi << 64) | sp.inc_lo;
+  u128 A = 1, B = 0;
+  for (int k = 0; steps; ++k, steps >>= 1)
+    if (steps & 1ull) {
+      A = A * c_jump.A[k];
+      B = B * c_jump.A[k] + c_jump.B[k];
+    }
+  return A * s0 + inc * B;
+}
+
+// Word generator for this thread's chunk.  Block base state is computed once
+// per block (thread 0) and shared; the thread applies its local jump.
 struct WordGen {
   u128 st, inc;
   uint64_t out;
   int half;
-  __device__ __forceinline__ void init(const StreamSpec& sp, uint64_t w) {
-    u128 s0 = ((u128)sp.st_hi << 64) | sp.st_lo;
-    inc = ((u128)sp.inc_hi << 64) | sp.inc_lo;
-    uint64_t n = (w >> 1) + 1;  // state after output (w>>1) = n steps
-    u128 A = 1, B = 0;
-    for (int k = 0; n; ++k, n >>= 1)
-      if (n & 1ull) {
-        A = A * c_jump.A[k];
-        B = B * c_jump.A[k] + c_jump.B[k];
-      }
-    st = A * s0 + inc * B;
-    out = pcg_output(st);
-    half = (int)(w & 1ull);
-  }
   __device__ __forceinline__ uint32_t next() {
     uint32_t r;
     if (half) {
@@ -92,6 +112,30 @@ struct WordGen {
     return r;
   }
 };
+
+__device__ __forceinline__ uint64_t block_word0(const long long* w0p) {
+  return (uint64_t)(w0p ? *w0p : 0) + (uint64_t)blockIdx.x * kBlockWords;
+}
+
+// All threads of the block call this (contains __syncthreads).
+__device__ __forceinline__ WordGen block_wordgen(const StreamSpec& sp, const long long* w0p) {
+  __shared__ unsigned long long base[2];
+  const uint64_t wb = block_word0(w0p);
+  if (threadIdx.x == 0) {
+    const u128 s = state_after(sp, (wb >> 1) + 1);
+    base[0] = (unsigned long long)(s >> 64);
+    base[1] = (unsigned long long)s;
+  }
+  __syncthreads();
+  WordGen g;
+  g.inc = ((u128)sp.inc_hi << 64) | sp.inc_lo;
+  const u128 sb = ((u128)base[0] << 64) | base[1];
+  const u128 A = g_local_A[threadIdx.x], B = g_local_B[threadIdx.x];
+  g.st = A * sb + g.inc * B;
+  g.out = pcg_output(g.st);
+  g.half = (int)(wb & 1ull);  // chunk starts share the block's word parity (kChunkWords even)
+  return g;
+}
 
 template <int NCOL>
 struct Map {
@@ -123,41 +167,61 @@ __device__ __forceinline__ Map<NCOL> identity_map() {
   return m;
 }
 
-// Block-wide scan of maps (Hillis-Steele over kScanThreads threads).
+template <int NCOL>
+__device__ __forceinline__ Map<NCOL> shfl_up_map(const Map<NCOL>& m, int d) {
+  Map<NCOL> r;
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) r.c[c] = __shfl_up_sync(0xffffffffu, m.c[c], d);
+  return r;
+}
+
+// Block-wide exclusive scan of maps: warp shuffles, then one warp scans the
+// 8 warp aggregates.
 template <int NCOL>
 __device__ void block_scan_maps(Map<NCOL> mine, Map<NCOL>& excl, Map<NCOL>& agg) {
-  __shared__ uint32_t buf[2][kScanThreads][NCOL];
-  int tid = threadIdx.x;
-  int cur = 0;
+  __shared__ uint32_t wagg[kScanThreads / 32][NCOL];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Map<NCOL> inc = mine;
 #pragma unroll
-  for (int c = 0; c < NCOL; ++c) buf[0][tid][c] = mine.c[c];
+  for (int d = 1; d < 32; d <<= 1) {
+    Map<NCOL> o = shfl_up_map<NCOL>(inc, d);
+    if (lane >= d) inc = compose<NCOL>(o, inc);
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) wagg[w][c] = inc.c[c];
+  }
   __syncthreads();
-  for (int off = 1; off < kScanThreads; off <<= 1) {
-    Map<NCOL> me, other;
+  // prefix over preceding warps (at most 7 compositions)
+  Map<NCOL> pre = identity_map<NCOL>();
+  for (int j = 0; j < w; ++j) {
+    Map<NCOL> a;
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) me.c[c] = buf[cur][tid][c];
-    if (tid >= off) {
-#pragma unroll
-      for (int c = 0; c < NCOL; ++c) other.c[c] = buf[cur][tid - off][c];
-      me = compose<NCOL>(other, me);
-    }
-#pragma unroll
-    for (int c = 0; c < NCOL; ++c) buf[cur ^ 1][tid][c] = me.c[c];
-    cur ^= 1;
-    __syncthreads();
+    for (int c = 0; c < NCOL; ++c) a.c[c] = wagg[j][c];
+    pre = compose<NCOL>(pre, a);
   }
-  if (tid == 0) excl = identity_map<NCOL>();
-  else {
+  Map<NCOL> incl = compose<NCOL>(pre, inc);
+  // exclusive = incl of lane-1 within the block
+  Map<NCOL> prev = shfl_up_map<NCOL>(incl, 1);
+  excl = lane == 0 ? pre : prev;
+  Map<NCOL> tot = identity_map<NCOL>();
+  for (int j = 0; j < kScanThreads / 32; ++j) {
+    Map<NCOL> a;
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) excl.c[c] = buf[cur][tid - 1][c];
+    for (int c = 0; c < NCOL; ++c) a.c[c] = wagg[j][c];
+    tot = compose<NCOL>(tot, a);
   }
-#pragma unroll
-  for (int c = 0; c < NCOL; ++c) agg.c[c] = buf[cur][kScanThreads - 1][c];
+  agg = tot;
   __syncthreads();
 }
 
-__device__ __forceinline__ uint64_t start_word(const long long* w0p, int64_t chunk) {
-  return (uint64_t)(w0p ? *w0p : 0) + (uint64_t)chunk * kChunkWords;
+template <int NCOL>
+__device__ __forceinline__ uint32_t map_at(const Map<NCOL>& m, int c) {
+  uint32_t v = m.c[0];
+#pragma unroll
+  for (int j = 1; j < NCOL; ++j)
+    if (j == c) v = m.c[j];
+  return v;
 }
 
 // Pass 1: per-chunk maps + per-block aggregate maps.
@@ -165,24 +229,24 @@ template <int NCOL>
 __global__ void __launch_bounds__(kScanThreads) k_draw_count(StreamSpec sp, const long long* w0p, int64_t nchunks,
                                                              uint8_t* __restrict__ tmaps,
                                                              uint32_t* __restrict__ bagg) {
-  int64_t chunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
+  const int64_t chunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
+  WordGen g = block_wordgen(sp, w0p);
   Map<NCOL> m = identity_map<NCOL>();
   if (chunk < nchunks) {
-    WordGen g;
-    g.init(sp, start_word(w0p, chunk));
     int col[NCOL];
 #pragma unroll
     for (int c = 0; c < NCOL; ++c) col[c] = c;
+#pragma unroll 4
     for (int i = 0; i < kChunkWords; ++i) {
-      uint32_t w = g.next();
+      const uint32_t w = g.next();
 #pragma unroll
       for (int c = 0; c < NCOL; ++c) {
-        int cc = col[c];
+        const int cc = col[c];
         uint32_t n = sp.n[0], thr = sp.thr[0];
 #pragma unroll
         for (int j = 1; j < NCOL; ++j)
           if (j == cc) { n = sp.n[j]; thr = sp.thr[j]; }
-        uint64_t prod = (uint64_t)w * n;
+        const uint64_t prod = (uint64_t)w * n;
         if ((uint32_t)prod >= thr) {
           m.c[c] += 1;
           col[c] = cc + 1 == NCOL ? 0 : cc + 1;
@@ -211,7 +275,7 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_scan_blocks(const uint32_
   if (threadIdx.x == 0) { carry_elem = 0; carry_col = 0; }
   __syncthreads();
   for (int64_t base = 0; base < nblocks; base += kScanThreads) {
-    int64_t b = base + threadIdx.x;
+    const int64_t b = base + threadIdx.x;
     Map<NCOL> m = identity_map<NCOL>();
     if (b < nblocks) {
 #pragma unroll
@@ -219,22 +283,16 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_scan_blocks(const uint32_
     }
     Map<NCOL> excl, agg;
     block_scan_maps<NCOL>(m, excl, agg);
-    long long ce = carry_elem;
-    int cc = carry_col;
+    const long long ce = carry_elem;
+    const int cc = carry_col;
     if (b < nblocks) {
-      uint32_t adv = excl.c[0];
-#pragma unroll
-      for (int j = 1; j < NCOL; ++j)
-        if (j == cc) adv = excl.c[j];
+      const uint32_t adv = map_at<NCOL>(excl, cc);
       bstart[b * 2 + 0] = (cc + adv) % NCOL;
       bstart[b * 2 + 1] = ce + adv;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      uint32_t adv = agg.c[0];
-#pragma unroll
-      for (int j = 1; j < NCOL; ++j)
-        if (j == cc) adv = agg.c[j];
+      const uint32_t adv = map_at<NCOL>(agg, cc);
       carry_elem = ce + adv;
       carry_col = (int)((cc + adv) % NCOL);
     }
@@ -243,8 +301,9 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_scan_blocks(const uint32_
   if (threadIdx.x == 0) *total_out = carry_elem;
 }
 
-// Pass 3: re-generate the words and write accepted values at their offsets.
-// NCOL == 1 (nonzero stratum): out[e] = value, end word of element target-1.
+// Pass 3: re-generate the words, stage accepted values in shared memory and
+// write the block's contiguous output range with coalesced stores.
+// NCOL == 1 (nonzero stratum): out[e] = value; records the end word of element target-1.
 // NCOL  > 1 (zero candidates):  out[e] = value (row-major [row][NCOL]).
 template <int NCOL>
 __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, const long long* w0p, int64_t nchunks,
@@ -252,7 +311,9 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
                                                              const long long* __restrict__ bstart,
                                                              int64_t target, int32_t* __restrict__ out,
                                                              long long* __restrict__ end_word) {
-  int64_t chunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
+  __shared__ int32_t stage[kBlockWords];
+  const int64_t chunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
+  WordGen g = block_wordgen(sp, w0p);
   Map<NCOL> m = identity_map<NCOL>();
   if (chunk < nchunks) {
 #pragma unroll
@@ -260,40 +321,33 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
   }
   Map<NCOL> excl, agg;
   block_scan_maps<NCOL>(m, excl, agg);
-  if (chunk >= nchunks) return;
-  int bcol = (int)bstart[blockIdx.x * 2 + 0];
-  long long e = bstart[blockIdx.x * 2 + 1];
-  uint32_t adv = excl.c[0];
-#pragma unroll
-  for (int j = 1; j < NCOL; ++j)
-    if (j == bcol) adv = excl.c[j];
-  e += adv;
+  const int bcol = (int)bstart[blockIdx.x * 2 + 0];
+  const long long eb = bstart[blockIdx.x * 2 + 1];
+  const uint32_t adv = map_at<NCOL>(excl, bcol);
+  const long long nblk = map_at<NCOL>(agg, bcol);
   int col = (int)((bcol + adv) % NCOL);
-  if (e >= target) return;
-  uint64_t w = start_word(w0p, chunk);
-  WordGen g;
-  g.init(sp, w);
-  for (int i = 0; i < kChunkWords && e < target; ++i, ++w) {
-    uint32_t word = g.next();
-    uint32_t n = sp.n[0], thr = sp.thr[0];
+  long long e = eb + adv;
+  int rel = (int)adv;
+  if (chunk < nchunks && e < target) {
+    uint64_t w = block_word0(w0p) + (uint64_t)threadIdx.x * kChunkWords;
+    for (int i = 0; i < kChunkWords && e < target; ++i, ++w) {
+      const uint32_t word = g.next();
+      uint32_t n = sp.n[0], thr = sp.thr[0];
 #pragma unroll
-    for (int j = 1; j < NCOL; ++j)
-      if (j == col) { n = sp.n[j]; thr = sp.thr[j]; }
-    uint64_t prod = (uint64_t)word * n;
-    if ((uint32_t)prod >= thr) {
-      out[e] = (int32_t)(prod >> 32);
-      if (e == target - 1 && end_word) *end_word = (long long)(w + 1);
-      ++e;
-      col = col + 1 == NCOL ? 0 : col + 1;
+      for (int j = 1; j < NCOL; ++j)
+        if (j == col) { n = sp.n[j]; thr = sp.thr[j]; }
+      const uint64_t prod = (uint64_t)word * n;
+      if ((uint32_t)prod >= thr) {
+        stage[rel++] = (int32_t)(prod >> 32);
+        if (e == target - 1 && end_word) *end_word = (long long)(w + 1);
+        ++e;
+        col = col + 1 == NCOL ? 0 : col + 1;
+      }
     }
   }
-}
-
-// Zero stratum: hit test of candidate rows against the nonzero hash; per-block
-// miss counts.
-__device__ __forceinline__ void assemble_row(const int32_t* __restrict__ cand, int64_t r, int ncol,
-                                             const int* colmap, int ndim, int32_t* c) {
-  for (int k = 0; k < ndim; ++k) c[k] = colmap[k] < 0 ? 0 : cand[r * ncol + colmap[k]];
+  __syncthreads();
+  const long long lim = min((long long)nblk, (long long)target - eb);
+  for (long long i = threadIdx.x; i < lim; i += kScanThreads) out[eb + i] = stage[i];
 }
 
 struct ZeroSpec {
@@ -302,100 +356,154 @@ struct ZeroSpec {
   Strides st;
 };
 
+__device__ __forceinline__ int64_t zero_rows_avail(const ZeroSpec& zs, const long long* elems_avail,
+                                                   int64_t rows_max) {
+  return zs.ncol ? min(rows_max, (int64_t)(*elems_avail / zs.ncol)) : rows_max;
+}
+
+// Zero stratum, pass A: hit test of kRowsPerThread consecutive candidate rows
+// per thread against the nonzero hash; per-thread miss mask, per-block miss count.
 __global__ void __launch_bounds__(kScanThreads) k_zero_hits(ZeroSpec zs, const int32_t* __restrict__ cand,
                                                             const long long* __restrict__ elems_avail,
                                                             int64_t rows_max,
                                                             const unsigned long long* __restrict__ table,
                                                             uint64_t mask, uint8_t* __restrict__ miss,
                                                             uint32_t* __restrict__ bcount) {
-  int64_t r = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
-  int64_t rows = zs.ncol ? min(rows_max, (int64_t)(*elems_avail / zs.ncol)) : rows_max;
-  uint32_t ms = 0;
-  if (r < rows) {
-    int32_t c[kMaxModes];
-    assemble_row(cand, r, zs.ncol, zs.colmap, zs.ndim, c);
-    uint64_t key = 0;
-    for (int k = 0; k < zs.ndim; ++k) key += (uint64_t)(uint32_t)c[k] * zs.st.s[k];
-    ms = table ? (hash_contains(table, mask, key) ? 0u : 1u) : 1u;
+  const int64_t rows = zero_rows_avail(zs, elems_avail, rows_max);
+  const int64_t t = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
+  const int64_t r0 = t * kRowsPerThread;
+  uint32_t bits = 0;
+  uint64_t key[kRowsPerThread];
+  bool live[kRowsPerThread];
+#pragma unroll
+  for (int j = 0; j < kRowsPerThread; ++j) {
+    const int64_t r = r0 + j;
+    live[j] = r < rows;
+    key[j] = 0;
+    if (live[j])
+      for (int k = 0; k < zs.ndim; ++k) {
+        const int cm = zs.colmap[k];
+        const uint32_t c = cm < 0 ? 0u : (uint32_t)__ldg(cand + r * zs.ncol + cm);
+        key[j] += (uint64_t)c * zs.st.s[k];
+      }
   }
-  if (r < rows_max) miss[r] = (uint8_t)ms;
-  uint32_t tot = __syncthreads_count(ms);
-  if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
+#pragma unroll
+  for (int j = 0; j < kRowsPerThread; ++j)
+    if (live[j] && !(table && hash_contains(table, mask, key[j]))) bits |= 1u << j;
+  if (r0 < rows_max) miss[t] = (uint8_t)bits;
+  const int cnt = __popc(bits);
+  __shared__ uint32_t wsum[kScanThreads / 32];
+  int v = cnt;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int j = 0; j < kScanThreads / 32; ++j) s += wsum[j];
+    bcount[blockIdx.x] = s;
+  }
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_zero_scan(const uint32_t* __restrict__ bcount, int64_t nblocks,
-                                                            long long* __restrict__ boff,
-                                                            long long* __restrict__ total) {
+// Pass B: exclusive scan of per-block miss counts (one block of 1024 threads).
+__global__ void __launch_bounds__(1024) k_zero_scan(const uint32_t* __restrict__ bcount, int64_t nblocks,
+                                                    long long* __restrict__ boff, long long* __restrict__ total) {
+  __shared__ long long wsum[32];
   __shared__ long long carry;
-  __shared__ long long tmp[kScanThreads];
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int64_t base = 0; base < nblocks; base += kScanThreads) {
-    int64_t b = base + threadIdx.x;
-    long long v = b < nblocks ? bcount[b] : 0;
-    tmp[threadIdx.x] = v;
-    __syncthreads();
-    for (int off = 1; off < kScanThreads; off <<= 1) {
-      long long o = threadIdx.x >= off ? tmp[threadIdx.x - off] : 0;
-      __syncthreads();
-      tmp[threadIdx.x] += o;
-      __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t base = 0; base < nblocks; base += 1024) {
+    const int64_t b = base + threadIdx.x;
+    const long long v = b < nblocks ? bcount[b] : 0;
+    long long inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += o;
     }
-    if (b < nblocks) boff[b] = carry + tmp[threadIdx.x] - v;
+    if (lane == 31) wsum[w] = inc;
     __syncthreads();
-    if (threadIdx.x == 0) carry += tmp[kScanThreads - 1];
+    long long pre = 0;
+    for (int j = 0; j < w; ++j) pre += wsum[j];
+    if (b < nblocks) boff[b] = carry + pre + inc - v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long s = 0;
+      for (int j = 0; j < 32; ++j) s += wsum[j];
+      carry += s;
+    }
     __syncthreads();
   }
   if (threadIdx.x == 0) *total = carry;
 }
 
-// Compact the first q misses into zero_subs (int32 [q x ndim]); the thread that
-// writes miss number q-1 records how many hits preceded it.
+// Pass C: compact the first q misses into zero_subs (int32 [q x ndim]) through
+// a shared-memory stage; the writer of miss number q-1 records how many hits
+// preceded it (the reference's rejection count at its last round).
 __global__ void __launch_bounds__(kScanThreads) k_zero_compact(ZeroSpec zs, const int32_t* __restrict__ cand,
                                                                int64_t rows_max, const uint8_t* __restrict__ miss,
                                                                const long long* __restrict__ boff, int64_t q,
                                                                int32_t* __restrict__ zero_subs,
                                                                long long* __restrict__ hits_before) {
-  __shared__ uint32_t tmp[kScanThreads];
-  int64_t r = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
-  uint32_t ms = r < rows_max ? miss[r] : 0;
-  tmp[threadIdx.x] = ms;
-  __syncthreads();
-  for (int off = 1; off < kScanThreads; off <<= 1) {
-    uint32_t o = threadIdx.x >= off ? tmp[threadIdx.x - off] : 0;
-    __syncthreads();
-    tmp[threadIdx.x] += o;
-    __syncthreads();
+  extern __shared__ int32_t zstage[];
+  __shared__ int wsum[kScanThreads / 32];
+  const int64_t t = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
+  const int64_t r0 = t * kRowsPerThread;
+  const uint32_t bits = r0 < rows_max ? miss[t] : 0u;
+  const int cnt = __popc(bits);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
   }
-  if (!ms) return;
-  long long rank = boff[blockIdx.x] + tmp[threadIdx.x] - 1;
-  if (rank >= q) return;
-  int32_t c[kMaxModes];
-  assemble_row(cand, r, zs.ncol, zs.colmap, zs.ndim, c);
-  for (int k = 0; k < zs.ndim; ++k) zero_subs[rank * zs.ndim + k] = c[k];
-  if (rank == q - 1) *hits_before = (long long)(r - rank);
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  int pre = 0;
+  for (int j = 0; j < w; ++j) pre += wsum[j];
+  int blk_total = 0;
+  for (int j = 0; j < kScanThreads / 32; ++j) blk_total += wsum[j];
+  const long long bo = boff[blockIdx.x];
+  int rel = pre + inc - cnt;
+  const int nd = zs.ndim;
+  for (int j = 0; j < kRowsPerThread; ++j) {
+    if (!(bits & (1u << j))) continue;
+    const long long rank = bo + rel;
+    if (rank < q) {
+      const int64_t r = r0 + j;
+      for (int k = 0; k < nd; ++k) {
+        const int cm = zs.colmap[k];
+        zstage[rel * nd + k] = cm < 0 ? 0 : __ldg(cand + r * zs.ncol + cm);
+      }
+      if (rank == q - 1) *hits_before = (long long)(r - rank);
+    }
+    ++rel;
+  }
+  __syncthreads();
+  const long long nrows = max(0LL, min((long long)blk_total, q - bo));
+  for (long long i = threadIdx.x; i < nrows * nd; i += kScanThreads) zero_subs[bo * nd + i] = zstage[i];
 }
 
 // Final status: shortfall (need more candidates) or budget exhaustion.
 __global__ void k_draw_status(int64_t p, const long long* nz_avail, int64_t q, const long long* z_misses,
-                              const long long* z_rows_total, int64_t rows_max, int ncol,
-                              const long long* z_elems, const long long* hits_before, long long budget,
-                              long long code, DevFlags* flags) {
+                              int64_t rows_max, int ncol, const long long* z_elems, const long long* hits_before,
+                              long long budget, long long code, DevFlags* flags) {
   if (threadIdx.x || blockIdx.x) return;
   bool shortfall = false, exhausted = false;
   if (p > 0 && nz_avail && *nz_avail < p) shortfall = true;
   if (q > 0) {
-    long long rows = ncol ? min((long long)rows_max, *z_elems / ncol) : rows_max;
-    long long misses = *z_misses;
+    const long long rows = ncol ? min((long long)rows_max, *z_elems / ncol) : rows_max;
+    const long long misses = *z_misses;
     if (misses >= q) {
       if (*hits_before > budget) exhausted = true;
     } else {
-      long long hits = rows - misses;
+      const long long hits = rows - misses;
       if (hits > budget) exhausted = true;
       else shortfall = true;
     }
   }
-  (void)z_rows_total;
   if (exhausted) atomicMin(&flags->first_code[kFlagSampling], code);
   else if (shortfall) atomicMin(&flags->first_code[kFlagShortfall], code);
 }
@@ -410,19 +518,18 @@ __global__ void k_set_ll(long long* p, long long v) { *p = v; }
 template <int NCOL>
 static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int64_t target, int64_t words,
                        int32_t* out, long long* end_word, long long* elems_total, DrawScratch& scr) {
-  int64_t nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
-  int64_t nblocks = (nchunks + kScanThreads - 1) / kScanThreads;
-  uint8_t* tmaps = scr.tmaps.as<uint8_t>();
-  scr.tmaps.ensure((size_t)nchunks * NCOL);
-  tmaps = scr.tmaps.as<uint8_t>();
+  const int64_t nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
+  const int64_t nblocks = (nchunks + kScanThreads - 1) / kScanThreads;
+  scr.tmaps.ensure((size_t)nblocks * kScanThreads * NCOL);
   scr.bagg.ensure((size_t)nblocks * NCOL * 4);
   scr.bstart.ensure((size_t)nblocks * 16);
   cudaStream_t s = ctx->stream;
-  k_draw_count<NCOL><<<(unsigned)nblocks, kScanThreads, 0, s>>>(sp, w0, nchunks, tmaps, scr.bagg.as<uint32_t>());
-  k_draw_scan_blocks<NCOL><<<1, kScanThreads, 0, s>>>(scr.bagg.as<uint32_t>(), nblocks,
-                                                      scr.bstart.as<long long>(), elems_total);
-  k_draw_write<NCOL><<<(unsigned)nblocks, kScanThreads, 0, s>>>(sp, w0, nchunks, tmaps,
-                                                                scr.bstart.as<long long>(), target, out, end_word);
+  k_draw_count<NCOL><<<(unsigned)nblocks, kScanThreads, 0, s>>>(sp, w0, nchunks, scr.tmaps.as<uint8_t>(),
+                                                               scr.bagg.as<uint32_t>());
+  k_draw_scan_blocks<NCOL><<<1, kScanThreads, 0, s>>>(scr.bagg.as<uint32_t>(), nblocks, scr.bstart.as<long long>(),
+                                                      elems_total);
+  k_draw_write<NCOL><<<(unsigned)nblocks, kScanThreads, 0, s>>>(sp, w0, nchunks, scr.tmaps.as<uint8_t>(),
+                                                               scr.bstart.as<long long>(), target, out, end_word);
   ctx->count(3);
   check_launch();
 }
@@ -478,10 +585,10 @@ void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q
       sp.ncol = 1;
       sp.n[0] = (uint32_t)eta;
       sp.thr[0] = lemire_threshold((uint32_t)eta);
-      double r = reject_rate((uint32_t)eta);
-      double exp_words = (double)p / (1.0 - r);
-      double sd = std::sqrt((double)p * r) / (1.0 - r);
-      int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
+      const double r = reject_rate((uint32_t)eta);
+      const double exp_words = (double)p / (1.0 - r);
+      const double sd = std::sqrt((double)p * r) / (1.0 - r);
+      const int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
       run_stream_dispatch(1, ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr);
       nz_stream = true;
     }
@@ -507,24 +614,25 @@ void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q
       }
     zs.ncol = ncol;
     sp.ncol = ncol;
-    double rho = X->omega_d > 0 ? (double)eta / X->omega_d : 0.0;
-    double exp_rows = rho < 1.0 ? (double)q / (1.0 - rho) : 1e30;
-    double sd_rows = rho < 1.0 ? std::sqrt((double)q * rho) / (1.0 - rho) : 1e30;
-    double want = (exp_rows + 10.0 * sd_rows + 64.0) * slack;
-    double cap = (double)q + (double)budget + 1.0;
+    const double rho = X->omega_d > 0 ? (double)eta / X->omega_d : 0.0;
+    const double exp_rows = rho < 1.0 ? (double)q / (1.0 - rho) : 1e30;
+    const double sd_rows = rho < 1.0 ? std::sqrt((double)q * rho) / (1.0 - rho) : 1e30;
+    const double want = (exp_rows + 10.0 * sd_rows + 64.0) * slack;
+    const double cap = (double)q + (double)budget + 1.0;
     rows_max = (int64_t)std::min(want, cap);
     if (rows_max < q) rows_max = q;
-    scr.miss.ensure((size_t)rows_max);
-    int64_t zblocks = (rows_max + kScanThreads - 1) / kScanThreads;
+    const int64_t nthreads = (rows_max + kRowsPerThread - 1) / kRowsPerThread;
+    const int64_t zblocks = (nthreads + kScanThreads - 1) / kScanThreads;
+    scr.miss.ensure((size_t)zblocks * kScanThreads);
     scr.zcount.ensure((size_t)zblocks * 4);
     scr.zoff.ensure((size_t)zblocks * 8);
     const unsigned long long* table = eta > 0 ? X->hash.as<unsigned long long>() : nullptr;
     if (ncol > 0) {
-      int64_t target = rows_max * ncol;
+      const int64_t target = rows_max * ncol;
       scr.cand.ensure((size_t)target * 4);
-      double exp_words = (double)target / (1.0 - rmax);
-      double sd = std::sqrt((double)target * rmax) / (1.0 - rmax);
-      int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
+      const double exp_words = (double)target / (1.0 - rmax);
+      const double sd = std::sqrt((double)target * rmax) / (1.0 - rmax);
+      const int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
       const long long* w0 = nz_stream ? nz_end : nullptr;
       run_stream_dispatch(ncol, ctx, sp, w0, target, words, scr.cand.as<int32_t>(), nullptr, z_elems, scr);
     } else {
@@ -535,14 +643,17 @@ void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q
     k_zero_hits<<<(unsigned)zblocks, kScanThreads, 0, s>>>(zs, scr.cand.as<int32_t>(), z_elems, rows_max, table,
                                                            X->table_mask, scr.miss.as<uint8_t>(),
                                                            scr.zcount.as<uint32_t>());
-    k_zero_scan<<<1, kScanThreads, 0, s>>>(scr.zcount.as<uint32_t>(), zblocks, scr.zoff.as<long long>(), z_misses);
-    k_zero_compact<<<(unsigned)zblocks, kScanThreads, 0, s>>>(zs, scr.cand.as<int32_t>(), rows_max,
-                                                              scr.miss.as<uint8_t>(), scr.zoff.as<long long>(), q,
-                                                              zero_subs, z_hits_before);
+    k_zero_scan<<<1, 1024, 0, s>>>(scr.zcount.as<uint32_t>(), zblocks, scr.zoff.as<long long>(), z_misses);
+    const size_t smem = (size_t)kRowsPerBlock * d * 4;
+    if (smem > 48 * 1024)
+      OGCP_CUDA(cudaFuncSetAttribute(k_zero_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_zero_compact<<<(unsigned)zblocks, kScanThreads, smem, s>>>(zs, scr.cand.as<int32_t>(), rows_max,
+                                                                 scr.miss.as<uint8_t>(), scr.zoff.as<long long>(), q,
+                                                                 zero_subs, z_hits_before);
     ctx->count(3);
   }
-  k_draw_status<<<1, 1, 0, s>>>(nz_stream ? p : 0, nz_avail, q, z_misses, nullptr, rows_max, ncol, z_elems,
-                                z_hits_before, (long long)budget, code, ctx->flags.as<DevFlags>());
+  k_draw_status<<<1, 1, 0, s>>>(nz_stream ? p : 0, nz_avail, q, z_misses, rows_max, ncol, z_elems, z_hits_before,
+                                (long long)budget, code, ctx->flags.as<DevFlags>());
   ctx->count();
   check_launch();
 }
