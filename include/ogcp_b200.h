@@ -135,6 +135,12 @@ int ogcp_ctx_profile_enable(ogcp_ctx* ctx, int32_t on);
  * count and milliseconds of one class. */
 int ogcp_ctx_profile_read(ogcp_ctx* ctx, int32_t cls, int64_t* brackets, double* total_ms);
 int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
+/* Engine options.  OGCP_OPT_MERGE_DRAWS (default 1): in the solves, merge dense
+ * nonzero draws (p >= eta/8) into distinct ordinals with multiplicities before
+ * evaluation -- the same merge sampled_gradient_tensor performs
+ * (sampling.py:233-237); 0 evaluates every draw separately. */
+enum { OGCP_OPT_MERGE_DRAWS = 1 };
+int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value);
 
 /* ----------------------------------------------------------------- slice */
 /* SparseTensor.from_zero_based (tensor.py:75-119): validates bounds,

@@ -71,6 +71,10 @@ _SIGS = {
     "ogcp_ctx_destroy": (C.c_int, [C.c_void_p]),
     "ogcp_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ogcp_ctx_launches": (C.c_int64, [C.c_void_p]),
+    "ogcp_ctx_profile_enable": (C.c_int, [C.c_void_p, C.c_int32]),
+    "ogcp_ctx_profile_read": (C.c_int, [C.c_void_p, C.c_int32, c_i64p, c_f64p]),
+    "ogcp_ctx_profile_reset": (C.c_int, [C.c_void_p]),
+    "ogcp_ctx_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
     "ogcp_slice_create": (C.c_int, [C.c_void_p, C.c_int32, c_i64p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
                                     C.POINTER(C.c_void_p)]),
     "ogcp_slice_create_i32": (C.c_int, [C.c_void_p, C.c_int32, c_i64p, C.c_int64, C.c_void_p, C.c_void_p,
@@ -201,3 +205,8 @@ def rng_integers(seed, key, highs, n):
     out = np.empty(int(n), dtype=np.int64)
     check(lib().ogcp_rng_integers(int(seed), kp, len(key), hp, len(h), int(n), out.ctypes.data_as(c_i64p)))
     return out
+
+
+def set_merge_draws(on: bool):
+    """Engine option OGCP_OPT_MERGE_DRAWS for the current device's context."""
+    check(lib().ogcp_ctx_set_option(ctx(), 1, int(bool(on))))

@@ -134,6 +134,7 @@ struct Ctx {
   int64_t launches = 0;
   Profiler prof;
   double slack = 1.0;           // sampler over-provisioning multiplier (grows on shortfall)
+  bool merge_draws = true;      // merged (count) form of dense nonzero draws in the solves
   // scratch
   DevBuf flags;                 // DevFlags
   DevBuf draw_a, draw_b, draw_c, draw_d, draw_e;   // sampler scratch

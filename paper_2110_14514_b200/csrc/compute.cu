@@ -76,6 +76,7 @@ struct Sample {
   float4 a[ND<D>::v][V];
   float x;
   float scale;
+  float cnt;  // multiplicity of a merged nonzero (1 otherwise)
   bool nz;
 };
 
@@ -92,18 +93,21 @@ struct SampleStream {
   static constexpr int RI = (D > 0 && D <= 3) ? 4 : 8;
   SamplesP S;
   const ModelP* M;
-  int64_t total, stride, b;
+  int64_t p, total, stride, b, end;
   int lane, gl, nd;
   int oB[U];
+  float cB[U], cC[U];
   int tC[U][RI];
 
   __device__ __forceinline__ int64_t nidx(int64_t base, int u) const { return base + u * SPW + lane / G; }
 
-  __device__ __forceinline__ void load_ord(int64_t base, int (&o)[U]) const {
+  __device__ __forceinline__ void load_ord(int64_t base, int (&o)[U], float (&c)[U]) const {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t n = nidx(base, u);
-      o[u] = n < S.p ? __ldg(S.ord + n) : 0;
+      const bool nz = n < p && n < end;
+      o[u] = nz ? __ldg(S.ord + n) : 0;
+      c[u] = (S.cnt && nz) ? (float)__ldg(S.cnt + n) : 1.0f;
     }
   }
 
@@ -113,7 +117,8 @@ struct SampleStream {
       const int64_t n = nidx(base, u);
 #pragma unroll
       for (int k = 0; k < RI; ++k) t[u][k] = 0;
-      if (n < S.p) {
+      if (n >= end) continue;
+      if (n < p) {
         const int4* r = reinterpret_cast<const int4*>(S.rec + (int64_t)o[u] * S.rec_ints);
         const int4 v0 = __ldg(r);
         t[u][0] = v0.x; t[u][1] = v0.y; t[u][2] = v0.z; t[u][3] = v0.w;
@@ -122,8 +127,8 @@ struct SampleStream {
           t[u][RI > 4 ? 4 : 0] = v1.x; t[u][RI > 4 ? 5 : 1] = v1.y;
           t[u][RI > 4 ? 6 : 2] = v1.z; t[u][RI > 4 ? 7 : 3] = v1.w;
         }
-      } else if (n < total) {
-        const int32_t* z = S.zsub + (n - S.p) * nd;
+      } else {
+        const int32_t* z = S.zsub + (n - p) * nd;
 #pragma unroll
         for (int k = 0; k < NDm; ++k)
           if (k < nd) t[u][k] = __ldg(z + k);
@@ -131,32 +136,48 @@ struct SampleStream {
     }
   }
 
+  // contiguous = true: warp w walks its own contiguous range of samples (keeps
+  // the ordinal order of a merged sample set, so consecutive samples of a group
+  // share mode-0 rows); false: grid-stride batches.
   __device__ __forceinline__ void init(const SamplesP& S_, const ModelP& M_, int lane_, int64_t warp,
-                                       int64_t nwarps) {
+                                       int64_t nwarps, bool contiguous = false) {
     S = S_;
     M = &M_;
-    total = S.p + S.q;
+    p = S.p_dev ? (int64_t)*S.p_dev : S.p;
+    total = p + S.q;
     lane = lane_;
     gl = lane & (G - 1);
     nd = D > 0 ? D : M_.ndim;
-    stride = nwarps * SPB;
-    b = warp * SPB;
+    if (contiguous) {
+      const int64_t per = ((total + nwarps - 1) / nwarps + SPB - 1) / SPB * SPB;
+      b = warp * per;
+      end = min(total, b + per);
+      stride = SPB;
+    } else {
+      stride = nwarps * SPB;
+      b = warp * SPB;
+      end = total;
+    }
     int o0[U];
-    load_ord(b, o0);
+    float c0[U];
+    load_ord(b, o0, c0);
     load_rec(b, o0, tC);
-    load_ord(b + stride, oB);
+#pragma unroll
+    for (int u = 0; u < U; ++u) cC[u] = c0[u];
+    load_ord(b + stride, oB, cB);
   }
 
   // Issue the row gathers of the current batch (and the next batches' earlier
   // stages); returns false when the warp has no batch left.
   __device__ __forceinline__ bool next(Sample<D, V> (&s)[U], bool (&valid)[U]) {
-    if (b >= total) return false;
+    if (b >= end) return false;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t n = nidx(b, u);
-      valid[u] = n < total;
-      s[u].nz = n < S.p;
-      s[u].scale = s[u].nz ? (float)S.nz_scale : (float)S.zero_scale;
+      valid[u] = n < end;
+      s[u].nz = n < p;
+      s[u].scale = s[u].nz ? (float)S.nz_scale * cC[u] : (float)S.zero_scale;
+      s[u].cnt = s[u].nz ? cC[u] : 1.0f;
       float x = 0.0f;
       if (D > 0) x = __int_as_float(tC[u][D < RI ? D : 0]);
       else {
@@ -182,7 +203,9 @@ struct SampleStream {
     // stage 2 for the next batch, stage 1 for the one after
     int tB[U][RI];
     load_rec(b + stride, oB, tB);
-    load_ord(b + 2 * stride, oB);
+#pragma unroll
+    for (int u = 0; u < U; ++u) cC[u] = cB[u];
+    load_ord(b + 2 * stride, oB, cB);
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -286,7 +309,11 @@ struct PrivP {
   int64_t len[kMaxModes];  // floats
 };
 
-template <int D, int G, int V>
+// SEG: the sample set is a merged (ordinal-sorted) one walked in contiguous
+// per-warp ranges; each lane group accumulates its mode-0 contributions in
+// registers while consecutive samples share the mode-0 row and issues one
+// reduction per row segment (sort-by-row segmented reduction for mode 0).
+template <int D, int G, int V, bool SEG>
 __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const float* __restrict__ s_f, LossP L,
                                                     GradPtrs GP, PrivP PV, DevFlags* flags, long long code) {
   extern __shared__ float smem[];
@@ -314,9 +341,14 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
   SampleStream<D, G, V, kU> stream;
-  stream.init(S, M, lane, warp, nwarps);
+  stream.init(S, M, lane, warp, nwarps, SEG);
   Sample<D, V> s[kU];
   bool valid[kU];
+  const bool seg0 = SEG && priv_slot[0] < 0;
+  int seg_row = -1;
+  float4 seg_acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) seg_acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
   while (stream.next(s, valid)) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -324,6 +356,15 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
       if (valid[u]) {
         bits |= domain_bits(L.kind, m);
         const float y = s[u].scale * dloss(L.kind, s[u].x, m, L.eps);
+        if (seg0 && s[u].idx[0] != seg_row) {
+          if (seg_row >= 0) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) red_add_v4(GP.g[0] + (int64_t)seg_row * M.ldr + (v * G + gl) * 4, seg_acc[v]);
+          }
+          seg_row = s[u].idx[0];
+#pragma unroll
+          for (int v = 0; v < V; ++v) seg_acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
         for (int k = 0; k < NDm; ++k) {
           if (k >= nd) break;
@@ -334,7 +375,12 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
             for (int j = 0; j < NDm; ++j)
               if (j != k && j < nd) c = mul4(c, s[u].a[j][v]);
             const int64_t off = (int64_t)s[u].idx[k] * M.ldr + (v * G + gl) * 4;
-            if (priv_slot[k] >= 0) {
+            if (k == 0 && seg0) {
+              seg_acc[v].x += c.x;
+              seg_acc[v].y += c.y;
+              seg_acc[v].z += c.z;
+              seg_acc[v].w += c.w;
+            } else if (priv_slot[k] >= 0) {
               float* p = smem + PV.off[priv_slot[k]] + off;
               atomicAdd(p + 0, c.x);
               atomicAdd(p + 1, c.y);
@@ -347,6 +393,10 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
         }
       }
     }
+  }
+  if (seg0 && seg_row >= 0) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) red_add_v4(GP.g[0] + (int64_t)seg_row * M.ldr + (v * G + gl) * 4, seg_acc[v]);
   }
   if (bits) report(flags, kFlagData, code, bits);
   if (PV.nmodes) {
@@ -382,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) k_wgrad(SamplesP S, ModelP M, const 
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
   SampleStream<D, G, V, kU> stream;
-  stream.init(S, M, lane, warp, nwarps);
+  stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr);
   Sample<D, V> s[kU];
   bool valid[kU];
   while (stream.next(s, valid)) {
@@ -457,7 +507,7 @@ __global__ void __launch_bounds__(kThreads) k_objective(SamplesP S, ModelP M, co
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
   SampleStream<D, G, V, kU> stream;
-  stream.init(S, M, lane, warp, nwarps);
+  stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr);
   Sample<D, V> s[kU];
   bool valid[kU];
   while (stream.next(s, valid)) {
@@ -468,7 +518,7 @@ __global__ void __launch_bounds__(kThreads) k_objective(SamplesP S, ModelP M, co
         bits |= domain_bits(L.kind, m);
         double f = floss(L.kind, (double)s[u].x, (double)m, L.eps_d);
         if (MODE == 1) f -= floss(L.kind, 0.0, (double)m, L.eps_d);
-        if (s[u].nz) acc_nz += f;
+        if (s[u].nz) acc_nz += f * (double)s[u].cnt;
         else acc_z += f;
       }
     }
@@ -939,10 +989,14 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
   ProfScope prof_scope(ctx, kProfSgrad);
   dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
-    auto kern = k_sgrad<D, G, V>;
-    if (smem > 48 * 1024) OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int grid = sample_grid(kern, smem, total, G);
-    kern<<<grid, kThreads, smem, ctx->stream>>>(S, M, s_f, L, GP, PV, ctx->flags.as<DevFlags>(), code);
+    auto launch = [&](auto kern) {
+      if (smem > 48 * 1024)
+        OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int grid = sample_grid(kern, smem, total, G);
+      kern<<<grid, kThreads, smem, ctx->stream>>>(S, M, s_f, L, GP, PV, ctx->flags.as<DevFlags>(), code);
+    };
+    if (S.cnt) launch(k_sgrad<D, G, V, true>);
+    else launch(k_sgrad<D, G, V, false>);
   });
   ctx->count();
   check_launch();

@@ -5,6 +5,10 @@ namespace ogcp {
 
 // One sample set on the device: p nonzero ordinals into the slice records and
 // q zero coordinates (int32 [q x ndim]); scales per sampling.py:99-105.
+// Merged (count) form: ord holds the distinct drawn ordinals in ascending
+// order, cnt their multiplicities, and the distinct count lives on the device
+// (p_dev); p is then an upper bound used only for launch sizing.  nz_scale is
+// always eta / (number of draws).
 struct SamplesP {
   const int32_t* ord;
   int64_t p;
@@ -13,6 +17,8 @@ struct SamplesP {
   const int* rec;
   int rec_ints;
   double nz_scale, zero_scale;
+  const long long* p_dev;   // nullable: distinct nonzero count (merged form)
+  const uint8_t* cnt;       // nullable: multiplicity per merged nonzero
 };
 
 struct GradPtrs {

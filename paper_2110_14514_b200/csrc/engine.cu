@@ -140,6 +140,8 @@ static SamplesP samples_of(const Slice* X, const int32_t* ord, int64_t p, const 
   S.nz_scale = p ? (double)X->nnz / (double)p : 0.0;
   S.zero_scale = q ? (X->omega_d - (double)X->nnz) / (double)q : 0.0;
   if (X->omega_fits && q) S.zero_scale = (double)(X->omega - X->nnz) / (double)q;
+  S.p_dev = nullptr;
+  S.cnt = nullptr;
   return S;
 }
 
@@ -160,14 +162,39 @@ static void resolve_counts(int64_t nonzeros, int64_t zeros, const Slice* X, int6
 struct SampleBufs {
   DevBuf ord, zero;
   DrawScratch scr;
+  MergedDraw md;
+  bool merged = false;
   int64_t p = 0, q = 0;
-  void size(int64_t p_, int64_t q_, int ndim) {
+  void size(int64_t p_, int64_t q_, int ndim, bool merged_ = false) {
     p = p_;
     q = q_;
-    ord.ensure((size_t)std::max<int64_t>(p, 1) * 4);
+    merged = merged_;
+    if (!merged) ord.ensure((size_t)std::max<int64_t>(p, 1) * 4);
     zero.ensure((size_t)std::max<int64_t>(q, 1) * ndim * 4);
   }
+  // Enqueue the draw of this buffer set and return its device sample set.
+  SamplesP draw(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t budget, long long code) {
+    draw_enqueue(ctx, X, g, p, q, budget, merged ? nullptr : ord.as<int32_t>(), zero.as<int32_t>(), code, scr,
+                 merged ? &md : nullptr);
+    return sample_set(X);
+  }
+  SamplesP sample_set(const Slice* X) const;
 };
+
+SamplesP SampleBufs::sample_set(const Slice* X) const {
+  if (!merged) return samples_of(X, ord.as<int32_t>(), p, zero.as<int32_t>(), q);
+  SamplesP S = samples_of(X, md.ord.as<int32_t>(), p, zero.as<int32_t>(), q);
+  S.p = std::min<int64_t>(p, X->nnz);  // upper bound of the distinct count
+  S.p_dev = md.count;
+  S.cnt = md.cnt.as<uint8_t>();
+  return S;                            // nz_scale stays eta / p (p draws)
+}
+
+// Merged (count) form pays off when the nonzero draws cover the slice densely
+// (p = "all" draws eta with replacement, sampling.py:71-77, 125).
+static bool use_merged(const Ctx* ctx, const Slice* X, int64_t p) {
+  return ctx->merge_draws && X->nnz >= 65536 && p >= X->nnz / 8 && p <= 4 * X->nnz;
+}
 
 // Synchronous draw with shortfall retry (used for objective sets).
 static void draw_sync(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t max_rejects,
@@ -258,7 +285,7 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   draw_sync(ctx, X, keyed(seed, {t, 2}), po, qo, cfg->samples.max_rejects, obj);
   SamplesP So = samples_of(X, obj.ord.as<int32_t>(), po, obj.zero.as<int32_t>(), qo);
   precheck_draw(X, p, q);
-  grad.size(p, q, X->ndim);
+  grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
   const int64_t budget = budget_of(q, cfg->samples.max_rejects);
   ctx->partials.ensure((size_t)kNumSMs * 8 * ldr * 8 + 64);
   double* part = ctx->partials.as<double>();
@@ -298,9 +325,7 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
       const long long ev0 = ev;
       for (int it = 0; it < cfg->iters_weights; ++it) {
         const long long e = ev++;
-        draw_enqueue(ctx, X, keyed(seed, {t, 1, epoch, it}), p, q, budget, grad.ord.as<int32_t>(),
-                     grad.zero.as<int32_t>(), code_of(e, 0), grad.scr);
-        SamplesP Sg = samples_of(X, grad.ord.as<int32_t>(), p, grad.zero.as<int32_t>(), q);
+        SamplesP Sg = grad.draw(ctx, X, keyed(seed, {t, 1, epoch, it}), budget, code_of(e, 0));
         int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1));
         const int64_t cnt = i + it + 1;
         const double rate_i = rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
@@ -447,9 +472,9 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
                              ogcp_adam_state* ad, double rate_i, const Pcg64& g, int64_t p, int64_t q,
                              int64_t budget, FactorWork& W, long long ev) {
   const int RR = M.rank * M.rank;
-  draw_enqueue(ctx, X, g, p, q, budget, W.grad.ord.as<int32_t>(), W.grad.zero.as<int32_t>(), code_of(ev, 0),
-               W.grad.scr);
-  SamplesP Sg = samples_of(X, W.grad.ord.as<int32_t>(), p, W.grad.zero.as<int32_t>(), q);
+  SamplesP Sg = W.grad.draw(ctx, X, g, budget, code_of(ev, 0));
+  (void)p;
+  (void)q;
   float* gp[kMaxModes];
   size_t off = 0;
   for (int k = 0; k < M.ndim; ++k) {
@@ -526,7 +551,7 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   draw_sync(ctx, X, keyed(seed, {t, 4}), po, qo, cfg->samples.max_rejects, W.obj);
   SamplesP So = samples_of(X, W.obj.ord.as<int32_t>(), po, W.obj.zero.as<int32_t>(), qo);
   precheck_draw(X, p, q);
-  W.grad.size(p, q, X->ndim);
+  W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
   const int64_t budget = budget_of(q, cfg->samples.max_rejects);
 
   long long ev = 1;
@@ -701,6 +726,13 @@ int ogcp_ctx_profile_read(ogcp_ctx* ctx, int32_t cls, int64_t* brackets, double*
 int ogcp_ctx_profile_reset(ogcp_ctx* ctx) {
   OGCP_API_BEGIN
   ctx->prof.reset();
+  OGCP_API_END
+}
+
+int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
+  OGCP_API_BEGIN
+  if (option == OGCP_OPT_MERGE_DRAWS) ctx->merge_draws = value != 0;
+  else throw Error(OGCP_E_USAGE, "unknown option");
   OGCP_API_END
 }
 

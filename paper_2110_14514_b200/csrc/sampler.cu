@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
                                                              const uint8_t* __restrict__ tmaps,
                                                              const long long* __restrict__ bstart,
                                                              int64_t target, int32_t* __restrict__ out,
-                                                             long long* __restrict__ end_word) {
+                                                             long long* __restrict__ end_word,
+                                                             uint32_t* __restrict__ hist) {
   __shared__ int32_t stage[kBlockWords];
   const int64_t chunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
   WordGen g = block_wordgen(sp, w0p);
@@ -338,13 +339,16 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
         if (j == col) { n = sp.n[j]; thr = sp.thr[j]; }
       const uint64_t prod = (uint64_t)word * n;
       if ((uint32_t)prod >= thr) {
-        stage[rel++] = (int32_t)(prod >> 32);
+        const uint32_t val = (uint32_t)(prod >> 32);
+        if (hist) atomicAdd(hist + (val >> 2), 1u << ((val & 3u) << 3));  // merged form: byte counters
+        else stage[rel++] = (int32_t)val;
         if (e == target - 1 && end_word) *end_word = (long long)(w + 1);
         ++e;
         col = col + 1 == NCOL ? 0 : col + 1;
       }
     }
   }
+  if (hist) return;
   __syncthreads();
   const long long lim = min((long long)nblk, (long long)target - eb);
   for (long long i = threadIdx.x; i < lim; i += kScanThreads) out[eb + i] = stage[i];
@@ -515,9 +519,78 @@ __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
 
 __global__ void k_set_ll(long long* p, long long v) { *p = v; }
 
+// Merged nonzero stratum: ordinals with a nonzero byte counter, in ascending
+// order, with their multiplicities (the np.unique + bincount merge of
+// sampled_gradient_tensor, sampling.py:233-237, restricted to the nonzero
+// stratum).  Pass 1 counts per block, pass 2 (k_zero_scan) scans, pass 3 writes.
+constexpr int kHistWordsPerThread = 4;
+constexpr int kHistPerBlock = kHistWordsPerThread * 4 * kScanThreads;
+
+__device__ __forceinline__ int bytes_nonzero(uint32_t w) {
+  return ((w & 0xffu) != 0) + ((w & 0xff00u) != 0) + ((w & 0xff0000u) != 0) + ((w & 0xff000000u) != 0);
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_hist_count(const uint32_t* __restrict__ hist, int64_t nwords,
+                                                             uint32_t* __restrict__ bcount) {
+  const int64_t w0 = (blockIdx.x * (int64_t)kScanThreads + threadIdx.x) * kHistWordsPerThread;
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < kHistWordsPerThread; ++j)
+    if (w0 + j < nwords) c += bytes_nonzero(__ldg(hist + w0 + j));
+  __shared__ int wsum[kScanThreads / 32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int j = 0; j < kScanThreads / 32; ++j) s += wsum[j];
+    bcount[blockIdx.x] = (uint32_t)s;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_hist_write(const uint32_t* __restrict__ hist, int64_t nwords,
+                                                             int64_t eta, const long long* __restrict__ boff,
+                                                             int32_t* __restrict__ ord, uint8_t* __restrict__ cnt) {
+  const int64_t w0 = (blockIdx.x * (int64_t)kScanThreads + threadIdx.x) * kHistWordsPerThread;
+  uint32_t w[kHistWordsPerThread];
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < kHistWordsPerThread; ++j) {
+    w[j] = w0 + j < nwords ? __ldg(hist + w0 + j) : 0u;
+    c += bytes_nonzero(w[j]);
+  }
+  __shared__ int wsum[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  int inc = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) wsum[wi] = inc;
+  __syncthreads();
+  int pre = 0;
+  for (int j = 0; j < wi; ++j) pre += wsum[j];
+  long long pos = boff[blockIdx.x] + pre + inc - c;
+#pragma unroll
+  for (int j = 0; j < kHistWordsPerThread; ++j)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t v = (w[j] >> (8 * b)) & 0xffu;
+      if (v) {
+        ord[pos] = (int32_t)((w0 + j) * 4 + b);
+        cnt[pos] = (uint8_t)v;
+        ++pos;
+      }
+    }
+  (void)eta;
+}
+
 template <int NCOL>
 static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int64_t target, int64_t words,
-                       int32_t* out, long long* end_word, long long* elems_total, DrawScratch& scr) {
+                       int32_t* out, long long* end_word, long long* elems_total, DrawScratch& scr,
+                       uint32_t* hist = nullptr) {
   const int64_t nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
   const int64_t nblocks = (nchunks + kScanThreads - 1) / kScanThreads;
   scr.tmaps.ensure((size_t)nblocks * kScanThreads * NCOL);
@@ -529,7 +602,8 @@ static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int6
   k_draw_scan_blocks<NCOL><<<1, kScanThreads, 0, s>>>(scr.bagg.as<uint32_t>(), nblocks, scr.bstart.as<long long>(),
                                                       elems_total);
   k_draw_write<NCOL><<<(unsigned)nblocks, kScanThreads, 0, s>>>(sp, w0, nchunks, scr.tmaps.as<uint8_t>(),
-                                                               scr.bstart.as<long long>(), target, out, end_word);
+                                                               scr.bstart.as<long long>(), target, out, end_word,
+                                                               hist);
   ctx->count(3);
   check_launch();
 }
@@ -554,7 +628,7 @@ static double reject_rate(uint32_t n) { return (double)lemire_threshold(n) / 429
 // Enqueue one stratified draw.  ordinals: int32 [p]; zero_subs: int32 [q x ndim].
 // code: event code (event*4) recorded on sampling errors / shortfall.
 void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
-                  int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr) {
+                  int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr, MergedDraw* merged) {
   init_jump_table();
   ProfScope prof_scope(ctx, kProfDraw);
   const int d = X->ndim;
@@ -577,6 +651,7 @@ void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q
 
   // ---- nonzero stratum: integers(0, eta, size=p)  (sampling.py:125)
   bool nz_stream = false;
+  if (merged && (p == 0 || eta < 2)) throw Error(OGCP_E_INTERNAL, "merged draw needs p > 0 and eta > 1");
   if (p > 0) {
     if (eta == 1) {
       k_fill_i32<<<std::min(ceil_div_i(p, 256), kNumSMs * 4), 256, 0, s>>>(ordinals, p, 0);
@@ -589,7 +664,29 @@ void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q
       const double exp_words = (double)p / (1.0 - r);
       const double sd = std::sqrt((double)p * r) / (1.0 - r);
       const int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
-      run_stream_dispatch(1, ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr);
+      if (merged) {
+        const int64_t nwords = (eta + 3) / 4;
+        merged->hist.ensure((size_t)nwords * 4);
+        merged->ord.ensure((size_t)std::min(p, eta) * 4);
+        merged->cnt.ensure((size_t)std::min(p, eta));
+        OGCP_CUDA(cudaMemsetAsync(merged->hist.ptr, 0, (size_t)nwords * 4, s));
+        run_stream<1>(ctx, sp, nullptr, p, words, nullptr, nz_end, nz_avail, scr, merged->hist.as<uint32_t>());
+        const int64_t hblocks = (nwords + (int64_t)kHistWordsPerThread * kScanThreads - 1) /
+                                ((int64_t)kHistWordsPerThread * kScanThreads);
+        merged->bcount.ensure((size_t)hblocks * 4);
+        merged->boff.ensure((size_t)hblocks * 8);
+        k_hist_count<<<(unsigned)hblocks, kScanThreads, 0, s>>>(merged->hist.as<uint32_t>(), nwords,
+                                                                merged->bcount.as<uint32_t>());
+        k_zero_scan<<<1, 1024, 0, s>>>(merged->bcount.as<uint32_t>(), hblocks, merged->boff.as<long long>(),
+                                       sc + 5);
+        k_hist_write<<<(unsigned)hblocks, kScanThreads, 0, s>>>(merged->hist.as<uint32_t>(), nwords, eta,
+                                                                merged->boff.as<long long>(),
+                                                                merged->ord.as<int32_t>(), merged->cnt.as<uint8_t>());
+        ctx->count(3);
+        merged->count = sc + 5;
+      } else {
+        run_stream_dispatch(1, ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr);
+      }
       nz_stream = true;
     }
   }

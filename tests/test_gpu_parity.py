@@ -201,3 +201,48 @@ def test_stream_fit_vs_reference(golden_dir, name):
     assert rel_err(np.vstack(st.weights_log), c("weights_log")) < 1e-3
     assert st.iteration == int(c("iteration"))
     assert st.window.step_ids() == c("window_ids").tolist()
+
+
+@pytest.mark.parametrize("merge", [True, False])
+def test_dense_draw_solve_vs_oracle(merge):
+    """p = all nonzeros on a 1e5-nnz slice: the merged (count) form and the
+    per-draw form of the solve both match the oracle's slice step."""
+    rng = np.random.default_rng(21)
+    dims = (300, 200, 40)
+    lin = rng.choice(int(np.prod(dims)), size=100_000, replace=False)
+    subs0 = np.array(np.unravel_index(np.sort(lin), dims)).T
+    vals = rng.integers(1, 4, size=lin.size).astype(float)
+    R = 6
+    init = [rng.uniform(0.2, 1.0, (d, R)) for d in dims]
+    _lib.set_merge_draws(merge)
+    try:
+        X = P.SparseTensor.from_zero_based(dims, subs0, vals)
+        cfg = P.SolverConfig(max_epochs_weights=1, max_epochs_factors=1, iters_weights=4, iters_factors=4,
+                             rate_weights=0.05, rate_factors=1e-2, hist_weight=1.0, warm_start_weights=True,
+                             samples=P.SamplerConfig(None, 5000, 20000, 20000, seed=3))
+        loss = P.make_loss("poisson")
+        st = P.fresh_state(dims, R, loss, cfg, factors=init)
+        st.window = P.HistoryWindow(capacity=2)
+        for h in (1, 2):
+            s_h = np.full(R, 1.0 + 0.1 * h)
+            st.weights_log.append(s_h)
+            st.window.observe(h, s_h, P.rng_at(3, h, 5))
+        st.t = 2
+        m = P.process_slice(st, X, loss, cfg, exact_loss=True)
+    finally:
+        _lib.set_merge_draws(True)
+    ocfg = O.Cfg(kappa_w=1, kappa_f=1, tau_w=4, tau_f=4, rate_w=0.05, rate_f=1e-2, hist_weight=1.0,
+                 warm_weights=True, p=None, q=5000, p_obj=20000, q_obj=20000, seed=3)
+    ost = O.new_stream(init, "poisson", ocfg, capacity=2)
+    for h in (1, 2):
+        s_h = np.full(R, 1.0 + 0.1 * h)
+        ost.weights_log.append(s_h)
+        O.window_observe(ost, h, s_h, 3)
+    ost.t = 2
+    Xo = O.Slice(dims, subs0, vals)
+    s_t = O.slice_step(ost, Xo, "poisson", ocfg)
+    want = O.exact_local_loss(Xo, ost.factors, s_t, "poisson")
+    assert m.local_loss_exact == pytest.approx(want, rel=1e-4)
+    for a, b in zip(st.factors, ost.factors):
+        assert rel_err(a, b) < 1e-4
+    assert rel_err(st.weights_log[-1], s_t) < 1e-4
