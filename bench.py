@@ -275,7 +275,12 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     sg = prof["sgrad"]
     sg_ms = sg["ms"] / max(sg["launches"], 1)
-    sg_bytes = B_f * (p + q)
+    # Algorithmic bytes per launch = B_f x |Y|, |Y| = entries of the merged sampled gradient tensor
+    # (sampling.py:233-239): distinct nonzero ordinals among p draws with replacement (expected
+    # eta*(1-(1-1/eta)^p), sd ~ 5e3 at c4) plus the q zero draws (distinct w.p. ~1 at omega = 1e15).
+    uniq_nz = p * (1.0 - math.exp(p * math.log1p(-1.0 / p))) if p > 1 else float(p)
+    y_entries = uniq_nz + q
+    sg_bytes = B_f * y_entries
     achieved = sg_bytes / (sg_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -336,7 +341,9 @@ def main():
             "slices_per_s": 1000.0 * args.steps / ms_max * world,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgrad (K2+K3 fused eval/scatter)",
-                         "algorithmic_bytes_per_launch": sg_bytes, "avg_launch_ms": sg_ms},
+                         "algorithmic_bytes_per_launch": sg_bytes, "avg_launch_ms": sg_ms,
+                         "bytes_model": "B_f = 8dR+4d+4 = 784 B per entry of the merged gradient tensor Y; "
+                                        f"|Y| = {y_entries:.4g} (distinct nonzero draws + zero draws)"},
             "kernel_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
             "kernel_launch_brackets": {k: v["launches"] for k, v in prof.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,

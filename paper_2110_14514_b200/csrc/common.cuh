@@ -69,6 +69,7 @@ struct DevFlags {
 };
 
 enum : int { kFlagSampling = 0, kFlagData = 1, kFlagDiverge = 2, kFlagShortfall = 3 };
+constexpr unsigned kMergeOverflowBit = 0x80000000u;  // DevFlags::data_bits: a merged-draw counter wrapped
 constexpr long long kNoEvent = 0x7fffffffffffffffLL;
 
 struct Slice {

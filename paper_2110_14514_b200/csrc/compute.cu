@@ -24,10 +24,6 @@ namespace ogcp {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;
-#ifndef OGCP_SAMPLE_U
-#define OGCP_SAMPLE_U 4
-#endif
-constexpr int kU = OGCP_SAMPLE_U;  // samples per lane group per pass
 
 template <int D>
 struct ND {
@@ -144,7 +140,7 @@ struct SampleStream {
     S = S_;
     M = &M_;
     p = S.p_dev ? (int64_t)*S.p_dev : S.p;
-    total = p + S.q;
+    total = p + (S.q_dev ? (int64_t)*S.q_dev : S.q);
     lane = lane_;
     gl = lane & (G - 1);
     nd = D > 0 ? D : M_.ndim;
@@ -174,8 +170,8 @@ struct SampleStream {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t n = nidx(b, u);
-      valid[u] = n < end;
       s[u].nz = n < p;
+      valid[u] = n < end && (s[u].nz || tC[u][0] >= 0);  // -1: rejected candidate (lazy zero layout)
       s[u].scale = s[u].nz ? (float)S.nz_scale * cC[u] : (float)S.zero_scale;
       s[u].cnt = s[u].nz ? cC[u] : 1.0f;
       float x = 0.0f;
@@ -313,12 +309,11 @@ struct PrivP {
 // per-warp ranges; each lane group accumulates its mode-0 contributions in
 // registers while consecutive samples share the mode-0 row and issues one
 // reduction per row segment (sort-by-row segmented reduction for mode 0).
-template <int D, int G, int V, bool SEG>
+template <int D, int G, int V, int U, bool SEG>
 __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const float* __restrict__ s_f, LossP L,
                                                     GradPtrs GP, PrivP PV, DevFlags* flags, long long code) {
   extern __shared__ float smem[];
   constexpr int NDm = ND<D>::v;
-  constexpr int SPB = (32 / G) * kU;
   const int nd = D > 0 ? D : M.ndim;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
@@ -340,10 +335,10 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
-  SampleStream<D, G, V, kU> stream;
+  SampleStream<D, G, V, U> stream;
   stream.init(S, M, lane, warp, nwarps, SEG);
-  Sample<D, V> s[kU];
-  bool valid[kU];
+  Sample<D, V> s[U];
+  bool valid[U];
   const bool seg0 = SEG && priv_slot[0] < 0;
   int seg_row = -1;
   float4 seg_acc[V];
@@ -351,7 +346,7 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
   for (int v = 0; v < V; ++v) seg_acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
   while (stream.next(s, valid)) {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const float m = model_value<D, G, V>(s[u], s4);
       if (valid[u]) {
         bits |= domain_bits(L.kind, m);
@@ -413,12 +408,11 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
 }
 
 // ------------------------------------------------------------------ K2 (weights)
-template <int D, int G, int V>
+template <int D, int G, int V, int U>
 __global__ void __launch_bounds__(kThreads) k_wgrad(SamplesP S, ModelP M, const float* __restrict__ s_f, LossP L,
                                                     double* __restrict__ partials, DevFlags* flags, long long code) {
   __shared__ double red[kThreads / 32][4 * V * G];
   constexpr int NDm = ND<D>::v;
-  constexpr int SPB = (32 / G) * kU;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   float4 s4[V];
@@ -431,16 +425,16 @@ __global__ void __launch_bounds__(kThreads) k_wgrad(SamplesP S, ModelP M, const 
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
-  SampleStream<D, G, V, kU> stream;
+  SampleStream<D, G, V, U> stream;
   stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr);
-  Sample<D, V> s[kU];
-  bool valid[kU];
+  Sample<D, V> s[U];
+  bool valid[U];
   while (stream.next(s, valid)) {
     float4 part[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) part[v] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const float m = model_value<D, G, V>(s[u], s4);
       if (valid[u]) {
         bits |= domain_bits(L.kind, m);
@@ -490,12 +484,11 @@ __global__ void __launch_bounds__(kThreads) k_wgrad(SamplesP S, ModelP M, const 
 
 // ------------------------------------------------------------------ K6
 // MODE 0: sum scale * f(x, m) (objective); MODE 1: sum f(x,m) - f(0,m) (exact-loss nonzero correction).
-template <int D, int G, int V, int MODE>
+template <int D, int G, int V, int U, int MODE>
 __global__ void __launch_bounds__(kThreads) k_objective(SamplesP S, ModelP M, const float* __restrict__ s_f,
                                                         LossP L, double* __restrict__ partials, DevFlags* flags,
                                                         long long code) {
   __shared__ double red[kThreads / 32];
-  constexpr int SPB = (32 / G) * kU;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   float4 s4[V];
@@ -506,13 +499,13 @@ __global__ void __launch_bounds__(kThreads) k_objective(SamplesP S, ModelP M, co
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
-  SampleStream<D, G, V, kU> stream;
+  SampleStream<D, G, V, U> stream;
   stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr);
-  Sample<D, V> s[kU];
-  bool valid[kU];
+  Sample<D, V> s[U];
+  bool valid[U];
   while (stream.next(s, valid)) {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < U; ++u) {
       const float m = model_value<D, G, V>(s[u], s4);
       if (valid[u] && gl == 0) {
         bits |= domain_bits(L.kind, m);
@@ -927,36 +920,60 @@ __global__ void k_hist_penalty(int ndim, int rank, const double* __restrict__ Po
 }
 
 // ==================================================================== host side
-#define OGCP_DISPATCH_LDR(D)                                                                                    \
-  switch (ldr) {                                                                                                \
-    case 4: f(std::integral_constant<int, D>(), std::integral_constant<int, 1>(), std::integral_constant<int, 1>()); break;   \
-    case 8: f(std::integral_constant<int, D>(), std::integral_constant<int, 2>(), std::integral_constant<int, 1>()); break;   \
-    case 16: f(std::integral_constant<int, D>(), std::integral_constant<int, 4>(), std::integral_constant<int, 1>()); break;  \
-    case 32: f(std::integral_constant<int, D>(), std::integral_constant<int, 8>(), std::integral_constant<int, 1>()); break;  \
-    case 64: f(std::integral_constant<int, D>(), std::integral_constant<int, 16>(), std::integral_constant<int, 1>()); break; \
-    case 128: f(std::integral_constant<int, D>(), std::integral_constant<int, 32>(), std::integral_constant<int, 1>()); break; \
-    case 256: f(std::integral_constant<int, D>(), std::integral_constant<int, 32>(), std::integral_constant<int, 2>()); break; \
-    default: throw Error(OGCP_E_USAGE, "unsupported padded rank " + std::to_string(ldr));                    \
-  }
+template <int N>
+using IC = std::integral_constant<int, N>;
+
+// Lane layout per kernel kind (G lanes per sample, V float4 chunks per lane, U
+// samples per group per pass), measured on B200 at R = 32 (profiles/): the
+// scatter kernel prefers 8 lanes x 1 chunk (one 16-byte reduction per lane per
+// mode), the reductions (weight gradient, objective) prefer 4 lanes x 2 chunks
+// (half the per-sample scalar work per warp instruction).  U = 2 keeps the
+// pipelined gathers below ~130 registers.
+enum class Layout { Scatter, Reduce };
 
 template <class F>
-static void dispatch_dgv(int ndim, int ldr, F&& f) {
+static void dispatch_layout(Layout kind, int ndim, int ldr, F&& f) {
+  auto by_ldr = [&](auto Dc) {
+    if (kind == Layout::Scatter) {
+      switch (ldr) {
+        case 4: f(Dc, IC<1>(), IC<1>(), IC<2>()); break;
+        case 8: f(Dc, IC<2>(), IC<1>(), IC<2>()); break;
+        case 16: f(Dc, IC<4>(), IC<1>(), IC<2>()); break;
+        case 32: f(Dc, IC<8>(), IC<1>(), IC<2>()); break;
+        case 64: f(Dc, IC<16>(), IC<1>(), IC<2>()); break;
+        case 128: f(Dc, IC<32>(), IC<1>(), IC<2>()); break;
+        case 256: f(Dc, IC<32>(), IC<2>(), IC<1>()); break;
+        default: throw Error(OGCP_E_USAGE, "unsupported padded rank " + std::to_string(ldr));
+      }
+    } else {
+      switch (ldr) {
+        case 4: f(Dc, IC<1>(), IC<1>(), IC<2>()); break;
+        case 8: f(Dc, IC<2>(), IC<1>(), IC<2>()); break;
+        case 16: f(Dc, IC<4>(), IC<1>(), IC<2>()); break;
+        case 32: f(Dc, IC<4>(), IC<2>(), IC<2>()); break;
+        case 64: f(Dc, IC<8>(), IC<2>(), IC<2>()); break;
+        case 128: f(Dc, IC<16>(), IC<2>(), IC<2>()); break;
+        case 256: f(Dc, IC<32>(), IC<2>(), IC<1>()); break;
+        default: throw Error(OGCP_E_USAGE, "unsupported padded rank " + std::to_string(ldr));
+      }
+    }
+  };
   switch (ndim) {
-    case 2: OGCP_DISPATCH_LDR(2); break;
-    case 3: OGCP_DISPATCH_LDR(3); break;
-    case 4: OGCP_DISPATCH_LDR(4); break;
-    default: OGCP_DISPATCH_LDR(0); break;
+    case 2: by_ldr(IC<2>()); break;
+    case 3: by_ldr(IC<3>()); break;
+    case 4: by_ldr(IC<4>()); break;
+    default: by_ldr(IC<0>()); break;
   }
 }
 
 // Grid for a grid-stride sample kernel: enough blocks to cover the samples once,
 // capped at the number that can be co-resident (occupancy API).
 template <class K>
-static int sample_grid(K kern, size_t smem, int64_t total, int G) {
+static int sample_grid(K kern, size_t smem, int64_t total, int G, int U) {
   int per_sm = 0;
   OGCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
   per_sm = std::max(per_sm, 1);
-  const int64_t per_block = (int64_t)(kThreads / G) * kU;
+  const int64_t per_block = (int64_t)(kThreads / G) * U;
   const int64_t need = (total + per_block - 1) / per_block;
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)kNumSMs * per_sm));
 }
@@ -987,16 +1004,17 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
   }
   const size_t smem = (size_t)used * 4;
   ProfScope prof_scope(ctx, kProfSgrad);
-  dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
+  dispatch_layout(Layout::Scatter, M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc, auto Uc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
+    constexpr int U = decltype(Uc)::value;
     auto launch = [&](auto kern) {
       if (smem > 48 * 1024)
         OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      const int grid = sample_grid(kern, smem, total, G);
+      const int grid = sample_grid(kern, smem, total, G, U);
       kern<<<grid, kThreads, smem, ctx->stream>>>(S, M, s_f, L, GP, PV, ctx->flags.as<DevFlags>(), code);
     };
-    if (S.cnt) launch(k_sgrad<D, G, V, true>);
-    else launch(k_sgrad<D, G, V, false>);
+    if (S.cnt) launch(k_sgrad<D, G, V, U, true>);
+    else launch(k_sgrad<D, G, V, U, false>);
   });
   ctx->count();
   check_launch();
@@ -1007,10 +1025,11 @@ int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f
   const int64_t total = S.p + S.q;
   int grid = 1;
   ProfScope prof_scope(ctx, kProfWgrad);
-  dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
+  dispatch_layout(Layout::Reduce, M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc, auto Uc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
-    auto kern = k_wgrad<D, G, V>;
-    grid = sample_grid(kern, 0, std::max<int64_t>(total, 1), G);
+    constexpr int U = decltype(Uc)::value;
+    auto kern = k_wgrad<D, G, V, U>;
+    grid = sample_grid(kern, 0, std::max<int64_t>(total, 1), G, U);
     kern<<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(), code);
   });
   ctx->count();
@@ -1024,10 +1043,11 @@ static int objective_like(Ctx* ctx, const SamplesP& S, const ModelP& M, const fl
   const int64_t total = S.p + S.q;
   int grid = 1;
   ProfScope prof_scope(ctx, kProfObjective);
-  dispatch_dgv(M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc) {
+  dispatch_layout(Layout::Reduce, M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc, auto Uc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
-    auto kern = k_objective<D, G, V, MODE>;
-    grid = sample_grid(kern, 0, std::max<int64_t>(total, 1), G);
+    constexpr int U = decltype(Uc)::value;
+    auto kern = k_objective<D, G, V, U, MODE>;
+    grid = sample_grid(kern, 0, std::max<int64_t>(total, 1), G, U);
     kern<<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(), code);
   });
   ctx->count();

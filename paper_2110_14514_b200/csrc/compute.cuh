@@ -19,6 +19,7 @@ struct SamplesP {
   double nz_scale, zero_scale;
   const long long* p_dev;   // nullable: distinct nonzero count (merged form)
   const uint8_t* cnt;       // nullable: multiplicity per merged nonzero
+  const long long* q_dev;   // nullable: lazy zero layout, rows [0, *q_dev) with -1-flagged rows skipped
 };
 
 struct GradPtrs {

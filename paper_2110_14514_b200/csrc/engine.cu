@@ -68,6 +68,7 @@ static void precheck_draw(const Slice* X, int64_t p, int64_t q) {
 // Returns 0 (clean), 1 (shortfall: redo with more candidates) or throws.
 static int check_flags(Ctx* ctx, const Slice* X, int kind, int64_t budget, const std::string& what, int64_t t) {
   const DevFlags& f = *ctx->host_flags;
+  if (f.data_bits & kMergeOverflowBit) return 2;  // redo without merging the draws
   long long e_min = kNoEvent;
   int which = -1;
   for (int i = 0; i < 3; ++i)
@@ -142,6 +143,7 @@ static SamplesP samples_of(const Slice* X, const int32_t* ord, int64_t p, const 
   if (X->omega_fits && q) S.zero_scale = (double)(X->omega - X->nnz) / (double)q;
   S.p_dev = nullptr;
   S.cnt = nullptr;
+  S.q_dev = nullptr;
   return S;
 }
 
@@ -164,6 +166,8 @@ struct SampleBufs {
   DrawScratch scr;
   MergedDraw md;
   bool merged = false;
+  const int32_t* zsub = nullptr;   // where the last draw left the zero coordinates
+  const long long* q_dev = nullptr;  // lazy zero layout row count (device)
   int64_t p = 0, q = 0;
   void size(int64_t p_, int64_t q_, int ndim, bool merged_ = false) {
     p = p_;
@@ -174,16 +178,23 @@ struct SampleBufs {
   }
   // Enqueue the draw of this buffer set and return its device sample set.
   SamplesP draw(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t budget, long long code) {
-    draw_enqueue(ctx, X, g, p, q, budget, merged ? nullptr : ord.as<int32_t>(), zero.as<int32_t>(), code, scr,
-                 merged ? &md : nullptr);
+    const DrawOut o = draw_enqueue(ctx, X, g, p, q, budget, merged ? nullptr : ord.as<int32_t>(),
+                                   zero.as<int32_t>(), code, scr, merged ? &md : nullptr, /*lazy=*/true);
+    zsub = o.zsub;
+    q_dev = o.q_dev;
     return sample_set(X);
   }
   SamplesP sample_set(const Slice* X) const;
 };
 
 SamplesP SampleBufs::sample_set(const Slice* X) const {
-  if (!merged) return samples_of(X, ord.as<int32_t>(), p, zero.as<int32_t>(), q);
-  SamplesP S = samples_of(X, md.ord.as<int32_t>(), p, zero.as<int32_t>(), q);
+  if (!merged) {
+    SamplesP S = samples_of(X, ord.as<int32_t>(), p, zsub, q);
+    S.q_dev = q_dev;
+    return S;
+  }
+  SamplesP S = samples_of(X, md.ord.as<int32_t>(), p, zsub, q);
+  S.q_dev = q_dev;
   S.p = std::min<int64_t>(p, X->nnz);  // upper bound of the distinct count
   S.p_dev = md.count;
   S.cnt = md.cnt.as<uint8_t>();
@@ -193,7 +204,9 @@ SamplesP SampleBufs::sample_set(const Slice* X) const {
 // Merged (count) form pays off when the nonzero draws cover the slice densely
 // (p = "all" draws eta with replacement, sampling.py:71-77, 125).
 static bool use_merged(const Ctx* ctx, const Slice* X, int64_t p) {
-  return ctx->merge_draws && X->nnz >= 65536 && p >= X->nnz / 8 && p <= 4 * X->nnz;
+  // 4-bit counters: with p <= 1.25 eta a counter reaches 16 with probability
+  // ~5e-13 per ordinal; the count-sum check catches it and the epoch is redone.
+  return ctx->merge_draws && X->nnz >= 65536 && p >= X->nnz / 8 && p <= X->nnz + X->nnz / 4;
 }
 
 // Synchronous draw with shortfall retry (used for objective sets).
@@ -204,7 +217,10 @@ static void draw_sync(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64
   const int64_t budget = budget_of(q, max_rejects);
   for (int attempt = 0;; ++attempt) {
     reset_flags(ctx);
-    draw_enqueue(ctx, X, g, p, q, budget, b.ord.as<int32_t>(), b.zero.as<int32_t>(), 0, b.scr);
+    const DrawOut o = draw_enqueue(ctx, X, g, p, q, budget, b.ord.as<int32_t>(), b.zero.as<int32_t>(), 0, b.scr,
+                                   nullptr, /*lazy=*/true);
+    b.zsub = o.zsub;
+    b.q_dev = o.q_dev;
     fetch_flags(ctx);
     OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
     int r = check_flags(ctx, X, OGCP_GAUSSIAN, budget, "draw", 0);
@@ -283,7 +299,7 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   if (po > 0 || p > 0) x_domain_check(X, L.kind);
   static thread_local SampleBufs obj, grad;
   draw_sync(ctx, X, keyed(seed, {t, 2}), po, qo, cfg->samples.max_rejects, obj);
-  SamplesP So = samples_of(X, obj.ord.as<int32_t>(), po, obj.zero.as<int32_t>(), qo);
+  SamplesP So = obj.sample_set(X);
   precheck_draw(X, p, q);
   grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
   const int64_t budget = budget_of(q, cfg->samples.max_rejects);
@@ -338,7 +354,9 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
       int r = check_flags(ctx, X, L.kind, budget, "temporal weight solve", t);
       if (r == 0) break;
       // shortfall: restore the epoch-start snapshot and redo with more candidates
-      ctx->slack *= 4.0;
+      // (r == 2: a merged-draw counter wrapped; redo with per-draw evaluation)
+      if (r == 2) grad.size(p, q, X->ndim, false);
+      else ctx->slack *= 4.0;
       OGCP_CUDA(cudaMemcpyAsync(ws, ws + 3 * ldr, 3 * ldr * 8, cudaMemcpyDeviceToDevice, st));
       OGCP_CUDA(cudaMemcpyAsync(hsc, ws, ldr * 8, cudaMemcpyDeviceToHost, st));
       OGCP_CUDA(cudaStreamSynchronize(st));
@@ -549,7 +567,7 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
   if (po > 0 || p > 0) x_domain_check(X, L.kind);
   draw_sync(ctx, X, keyed(seed, {t, 4}), po, qo, cfg->samples.max_rejects, W.obj);
-  SamplesP So = samples_of(X, W.obj.ord.as<int32_t>(), po, W.obj.zero.as<int32_t>(), qo);
+  SamplesP So = W.obj.sample_set(X);
   precheck_draw(X, p, q);
   W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
   const int64_t budget = budget_of(q, cfg->samples.max_rejects);
@@ -576,7 +594,8 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
       OGCP_CUDA(cudaStreamSynchronize(st));
       int r = check_flags(ctx, X, L.kind, budget, "factor solve", t);
       if (r == 0) break;
-      ctx->slack *= 4.0;
+      if (r == 2) W.grad.size(p, q, X->ndim, false);
+      else ctx->slack *= 4.0;
       adam_epoch(ctx, M, A, ad, false);  // restore the epoch-start state (no rate decay)
       ev = ev0;
       if (attempt > 8) throw Error(OGCP_E_INTERNAL, "sampler could not provision enough candidates");
@@ -785,7 +804,9 @@ int ogcp_draw_samples(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const i
   static thread_local DrawScratch scr;
   for (int attempt = 0;; ++attempt) {
     reset_flags(ctx);
-    draw_enqueue(ctx, s, g, p, q, budget, ordinals_dev, zero_subs_dev, 0, scr);
+    const int32_t* z = draw_enqueue(ctx, s, g, p, q, budget, ordinals_dev, zero_subs_dev, 0, scr).zsub;
+    if (q > 0 && z != zero_subs_dev)
+      OGCP_CUDA(cudaMemcpyAsync(zero_subs_dev, z, (size_t)q * s->ndim * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     fetch_flags(ctx);
     OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
     if (check_flags(ctx, s, OGCP_GAUSSIAN, budget, "draw", 0) == 0) break;
@@ -1029,7 +1050,7 @@ int ogcp_local_loss(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m, con
     for (int i = 0; i < nkey; ++i) k[i] = (uint64_t)key[i];
     static thread_local SampleBufs b;
     draw_sync(ctx, s, seedseq_pcg64(seed, k, nkey), pp, qq, max_rejects, b);
-    SamplesP S = samples_of(s, b.ord.as<int32_t>(), pp, b.zero.as<int32_t>(), qq);
+    SamplesP S = b.sample_set(s);
     reset_flags(ctx);
     int nb = objective_enqueue(ctx, S, M, s_f, L, part, code_of(1, 1));
     sum_partials_enqueue(ctx, part, nb, 1, dsc);

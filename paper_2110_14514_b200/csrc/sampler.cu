@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
                                                              const long long* __restrict__ bstart,
                                                              int64_t target, int32_t* __restrict__ out,
                                                              long long* __restrict__ end_word,
-                                                             uint32_t* __restrict__ hist) {
+                                                             uint32_t* __restrict__ hist, DevFlags* flags) {
   __shared__ int32_t stage[kBlockWords];
   const int64_t chunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
   WordGen g = block_wordgen(sp, w0p);
@@ -340,8 +340,11 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
       const uint64_t prod = (uint64_t)word * n;
       if ((uint32_t)prod >= thr) {
         const uint32_t val = (uint32_t)(prod >> 32);
-        if (hist) atomicAdd(hist + (val >> 2), 1u << ((val & 3u) << 3));  // merged form: byte counters
-        else stage[rel++] = (int32_t)val;
+        if (hist) {  // merged form: byte counters (a wrap is caught by the count-sum check)
+          atomicAdd(hist + (val >> 3), 1u << ((val & 7u) << 2));
+        } else {
+          stage[rel++] = (int32_t)val;
+        }
         if (e == target - 1 && end_word) *end_word = (long long)(w + 1);
         ++e;
         col = col + 1 == NCOL ? 0 : col + 1;
@@ -372,7 +375,9 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_hits(ZeroSpec zs, const i
                                                             int64_t rows_max,
                                                             const unsigned long long* __restrict__ table,
                                                             uint64_t mask, uint8_t* __restrict__ miss,
-                                                            uint32_t* __restrict__ bcount) {
+                                                            uint32_t* __restrict__ bcount, int64_t q,
+                                                            unsigned long long* __restrict__ hit_in_q,
+                                                            int mark_hits) {
   const int64_t rows = zero_rows_avail(zs, elems_avail, rows_max);
   const int64_t t = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
   const int64_t r0 = t * kRowsPerThread;
@@ -395,6 +400,18 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_hits(ZeroSpec zs, const i
   for (int j = 0; j < kRowsPerThread; ++j)
     if (live[j] && !(table && hash_contains(table, mask, key[j]))) bits |= 1u << j;
   if (r0 < rows_max) miss[t] = (uint8_t)bits;
+  if (hit_in_q) {  // any of the first q candidate rows not a miss -> the slow (compacting) path
+    bool hit = false;
+#pragma unroll
+    for (int j = 0; j < kRowsPerThread; ++j)
+      if (r0 + j < q && !((bits >> j) & 1u)) hit = true;
+    if (hit) atomicOr(hit_in_q, 1ull);
+  }
+  if (mark_hits) {  // lazy layout: a hit row keeps its slot, flagged by coordinate -1
+#pragma unroll
+    for (int j = 0; j < kRowsPerThread; ++j)
+      if (live[j] && !((bits >> j) & 1u)) const_cast<int32_t*>(cand)[(r0 + j) * zs.ncol] = -1;
+  }
   const int cnt = __popc(bits);
   __shared__ uint32_t wsum[kScanThreads / 32];
   int v = cnt;
@@ -449,9 +466,13 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_compact(ZeroSpec zs, cons
                                                                int64_t rows_max, const uint8_t* __restrict__ miss,
                                                                const long long* __restrict__ boff, int64_t q,
                                                                int32_t* __restrict__ zero_subs,
-                                                               long long* __restrict__ hits_before) {
+                                                               long long* __restrict__ hits_before,
+                                                               const unsigned long long* __restrict__ hit_in_q) {
   extern __shared__ int32_t zstage[];
   __shared__ int wsum[kScanThreads / 32];
+  // fast path: the first q candidates all miss, so the candidate buffer already
+  // holds the accepted zeros in order and nothing precedes the q-th miss
+  if (hit_in_q && *hit_in_q == 0ull) return;
   const int64_t t = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
   const int64_t r0 = t * kRowsPerThread;
   const uint32_t bits = r0 < rows_max ? miss[t] : 0u;
@@ -490,6 +511,64 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_compact(ZeroSpec zs, cons
   for (long long i = threadIdx.x; i < nrows * nd; i += kScanThreads) zero_subs[bo * nd + i] = zstage[i];
 }
 
+// Lazy layout: locate the q-th miss.  The accepted zeros are then candidate rows
+// [0, R) minus the rows flagged -1, R = row of the q-th miss + 1, and the
+// reference's rejection count at its last round is R - q (sampling.py:137-150).
+__global__ void __launch_bounds__(kScanThreads) k_zero_locate(const uint32_t* __restrict__ bcount,
+                                                              const long long* __restrict__ boff, int64_t nblocks,
+                                                              const uint8_t* __restrict__ miss, int64_t rows_max,
+                                                              int64_t q, long long* __restrict__ rows_used,
+                                                              long long* __restrict__ hits_before) {
+  __shared__ int64_t sb;
+  __shared__ int wsum[kScanThreads / 32];
+  if (threadIdx.x == 0) {
+    // last block whose exclusive offset is <= q-1
+    int64_t lo = 0, hi = nblocks - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (boff[mid] <= q - 1) lo = mid;
+      else hi = mid - 1;
+    }
+    sb = (boff[lo] + (long long)bcount[lo] > q - 1) ? lo : -1;
+    if (sb < 0) *rows_used = rows_max;  // fewer than q misses: the status pass reports it
+  }
+  __syncthreads();
+  if (sb < 0) return;
+  const int64_t t = sb * kScanThreads + threadIdx.x;
+  const int64_t r0 = t * kRowsPerThread;
+  const uint32_t bits = r0 < rows_max ? miss[t] : 0u;
+  const int cnt = __popc(bits);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  int pre = 0;
+  for (int j = 0; j < w; ++j) pre += wsum[j];
+  const long long target = q - 1 - boff[sb];  // rank of the q-th miss within the block
+  long long rank = pre + inc - cnt;
+  for (int j = 0; j < kRowsPerThread; ++j) {
+    if (!(bits & (1u << j))) continue;
+    if (rank == target) {
+      *rows_used = r0 + j + 1;
+      *hits_before = (r0 + j) - (q - 1);
+    }
+    ++rank;
+  }
+}
+
+// Slow path of the in-place layout: copy the compacted zeros back over the candidates.
+__global__ void k_zero_copyback(const unsigned long long* __restrict__ hit_in_q, const int32_t* __restrict__ src,
+                                int32_t* __restrict__ dst, int64_t n) {
+  if (*hit_in_q == 0ull) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 // Final status: shortfall (need more candidates) or budget exhaustion.
 __global__ void k_draw_status(int64_t p, const long long* nz_avail, int64_t q, const long long* z_misses,
                               int64_t rows_max, int ncol, const long long* z_elems, const long long* hits_before,
@@ -523,30 +602,67 @@ __global__ void k_set_ll(long long* p, long long v) { *p = v; }
 // order, with their multiplicities (the np.unique + bincount merge of
 // sampled_gradient_tensor, sampling.py:233-237, restricted to the nonzero
 // stratum).  Pass 1 counts per block, pass 2 (k_zero_scan) scans, pass 3 writes.
+// Counters are 4-bit nibbles, 8 per word: at c4 the 1e8 counters take 50 MB and
+// stay L2-resident while the draw's atomics land on them.
 constexpr int kHistWordsPerThread = 4;
-constexpr int kHistPerBlock = kHistWordsPerThread * 4 * kScanThreads;
+constexpr int kHistPerBlock = kHistWordsPerThread * 8 * kScanThreads;
 
-__device__ __forceinline__ int bytes_nonzero(uint32_t w) {
-  return ((w & 0xffu) != 0) + ((w & 0xff00u) != 0) + ((w & 0xff0000u) != 0) + ((w & 0xff000000u) != 0);
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_hist_count(const uint32_t* __restrict__ hist, int64_t nwords,
-                                                             uint32_t* __restrict__ bcount) {
-  const int64_t w0 = (blockIdx.x * (int64_t)kScanThreads + threadIdx.x) * kHistWordsPerThread;
+__device__ __forceinline__ int bytes_nonzero(uint32_t w) {  // nonzero nibbles
   int c = 0;
 #pragma unroll
-  for (int j = 0; j < kHistWordsPerThread; ++j)
-    if (w0 + j < nwords) c += bytes_nonzero(__ldg(hist + w0 + j));
-  __shared__ int wsum[kScanThreads / 32];
+  for (int b = 0; b < 8; ++b) c += ((w >> (4 * b)) & 0xfu) != 0;
+  return c;
+}
+
+__device__ __forceinline__ uint32_t bytes_sum(uint32_t w) {  // sum of nibbles
+  uint32_t s = 0;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  for (int b = 0; b < 8; ++b) s += (w >> (4 * b)) & 0xfu;
+  return s;
+}
+
+// Per-block count of nonzero counters, plus the sum of all counters: a wrapped
+// byte loses 256 from that sum, so sum == p certifies the counts exactly.
+__global__ void __launch_bounds__(kScanThreads) k_hist_count(const uint32_t* __restrict__ hist, int64_t nwords,
+                                                             uint32_t* __restrict__ bcount,
+                                                             unsigned long long* __restrict__ cnt_sum) {
+  const int64_t w0 = (blockIdx.x * (int64_t)kScanThreads + threadIdx.x) * kHistWordsPerThread;
+  int c = 0;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int j = 0; j < kHistWordsPerThread; ++j)
+    if (w0 + j < nwords) {
+      const uint32_t w = __ldg(hist + w0 + j);
+      c += bytes_nonzero(w);
+      sum += bytes_sum(w);
+    }
+  __shared__ int wsum[kScanThreads / 32];
+  __shared__ uint32_t ssum[kScanThreads / 32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    wsum[threadIdx.x >> 5] = c;
+    ssum[threadIdx.x >> 5] = sum;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int s = 0;
-    for (int j = 0; j < kScanThreads / 32; ++j) s += wsum[j];
+    unsigned long long t = 0;
+    for (int j = 0; j < kScanThreads / 32; ++j) {
+      s += wsum[j];
+      t += ssum[j];
+    }
     bcount[blockIdx.x] = (uint32_t)s;
+    atomicAdd(cnt_sum, t);
   }
+}
+
+__global__ void k_hist_verify(const unsigned long long* __restrict__ cnt_sum, long long p, DevFlags* flags) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && *cnt_sum != (unsigned long long)p)
+    atomicOr(&flags->data_bits, kMergeOverflowBit);
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_hist_write(const uint32_t* __restrict__ hist, int64_t nwords,
@@ -570,20 +686,32 @@ __global__ void __launch_bounds__(kScanThreads) k_hist_write(const uint32_t* __r
   }
   if (lane == 31) wsum[wi] = inc;
   __syncthreads();
-  int pre = 0;
-  for (int j = 0; j < wi; ++j) pre += wsum[j];
-  long long pos = boff[blockIdx.x] + pre + inc - c;
+  int pre = 0, tot = 0;
+  for (int j = 0; j < kScanThreads / 32; ++j) {
+    if (j < wi) pre += wsum[j];
+    tot += wsum[j];
+  }
+  // stage the block's entries in shared memory, then write them coalesced
+  __shared__ int32_t s_ord[kHistPerBlock];
+  __shared__ uint8_t s_cnt[kHistPerBlock];
+  int rel = pre + inc - c;
 #pragma unroll
   for (int j = 0; j < kHistWordsPerThread; ++j)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const uint32_t v = (w[j] >> (8 * b)) & 0xffu;
+    for (int b = 0; b < 8; ++b) {
+      const uint32_t v = (w[j] >> (4 * b)) & 0xfu;
       if (v) {
-        ord[pos] = (int32_t)((w0 + j) * 4 + b);
-        cnt[pos] = (uint8_t)v;
-        ++pos;
+        s_ord[rel] = (int32_t)((w0 + j) * 8 + b);
+        s_cnt[rel] = (uint8_t)v;
+        ++rel;
       }
     }
+  __syncthreads();
+  const long long base = boff[blockIdx.x];
+  for (int i = threadIdx.x; i < tot; i += kScanThreads) {
+    ord[base + i] = s_ord[i];
+    cnt[base + i] = s_cnt[i];
+  }
   (void)eta;
 }
 
@@ -603,7 +731,7 @@ static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int6
                                                       elems_total);
   k_draw_write<NCOL><<<(unsigned)nblocks, kScanThreads, 0, s>>>(sp, w0, nchunks, scr.tmaps.as<uint8_t>(),
                                                                scr.bstart.as<long long>(), target, out, end_word,
-                                                               hist);
+                                                               hist, ctx->flags.as<DevFlags>());
   ctx->count(3);
   check_launch();
 }
@@ -627,8 +755,12 @@ static double reject_rate(uint32_t n) { return (double)lemire_threshold(n) / 429
 
 // Enqueue one stratified draw.  ordinals: int32 [p]; zero_subs: int32 [q x ndim].
 // code: event code (event*4) recorded on sampling errors / shortfall.
-void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
-                  int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr, MergedDraw* merged) {
+DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
+                     int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr, MergedDraw* merged,
+                     bool lazy) {
+  DrawOut out;
+  out.zsub = zero_subs;
+  out.q_dev = nullptr;
   init_jump_table();
   ProfScope prof_scope(ctx, kProfDraw);
   const int d = X->ndim;
@@ -665,7 +797,7 @@ void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q
       const double sd = std::sqrt((double)p * r) / (1.0 - r);
       const int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
       if (merged) {
-        const int64_t nwords = (eta + 3) / 4;
+        const int64_t nwords = (eta + 7) / 8;
         merged->hist.ensure((size_t)nwords * 4);
         merged->ord.ensure((size_t)std::min(p, eta) * 4);
         merged->cnt.ensure((size_t)std::min(p, eta));
@@ -675,8 +807,11 @@ void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q
                                 ((int64_t)kHistWordsPerThread * kScanThreads);
         merged->bcount.ensure((size_t)hblocks * 4);
         merged->boff.ensure((size_t)hblocks * 8);
+        unsigned long long* cnt_sum = reinterpret_cast<unsigned long long*>(sc + 7);
         k_hist_count<<<(unsigned)hblocks, kScanThreads, 0, s>>>(merged->hist.as<uint32_t>(), nwords,
-                                                                merged->bcount.as<uint32_t>());
+                                                                merged->bcount.as<uint32_t>(), cnt_sum);
+        k_hist_verify<<<1, 32, 0, s>>>(cnt_sum, (long long)p, ctx->flags.as<DevFlags>());
+        ctx->count();
         k_zero_scan<<<1, 1024, 0, s>>>(merged->bcount.as<uint32_t>(), hblocks, merged->boff.as<long long>(),
                                        sc + 5);
         k_hist_write<<<(unsigned)hblocks, kScanThreads, 0, s>>>(merged->hist.as<uint32_t>(), nwords, eta,
@@ -737,22 +872,46 @@ void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q
       k_set_ll<<<1, 1, 0, s>>>(z_elems, 0);
       ctx->count();
     }
+    // In-place layout when no mode has size 1: the candidate rows are already
+    // [row][d] coordinates, so when the first q candidates all miss (the usual
+    // case for sparse slices) they are the accepted zeros and no compaction runs.
+    const bool in_place = ncol == d;
+    const bool mark = lazy && in_place;
+    unsigned long long* hit_in_q =
+        (in_place && !lazy) ? reinterpret_cast<unsigned long long*>(sc + 6) : nullptr;
     k_zero_hits<<<(unsigned)zblocks, kScanThreads, 0, s>>>(zs, scr.cand.as<int32_t>(), z_elems, rows_max, table,
                                                            X->table_mask, scr.miss.as<uint8_t>(),
-                                                           scr.zcount.as<uint32_t>());
+                                                           scr.zcount.as<uint32_t>(), q, hit_in_q, mark ? 1 : 0);
     k_zero_scan<<<1, 1024, 0, s>>>(scr.zcount.as<uint32_t>(), zblocks, scr.zoff.as<long long>(), z_misses);
-    const size_t smem = (size_t)kRowsPerBlock * d * 4;
-    if (smem > 48 * 1024)
-      OGCP_CUDA(cudaFuncSetAttribute(k_zero_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_zero_compact<<<(unsigned)zblocks, kScanThreads, smem, s>>>(zs, scr.cand.as<int32_t>(), rows_max,
-                                                                 scr.miss.as<uint8_t>(), scr.zoff.as<long long>(), q,
-                                                                 zero_subs, z_hits_before);
-    ctx->count(3);
+    ctx->count(2);
+    if (mark) {
+      // lazy layout: the kernels walk candidate rows [0, R) and skip the flagged hits
+      k_zero_locate<<<1, kScanThreads, 0, s>>>(scr.zcount.as<uint32_t>(), scr.zoff.as<long long>(), zblocks,
+                                               scr.miss.as<uint8_t>(), rows_max, q, sc + 8, z_hits_before);
+      ctx->count();
+      out.zsub = scr.cand.as<int32_t>();
+      out.q_dev = sc + 8;
+    } else {
+      const size_t smem = (size_t)kRowsPerBlock * d * 4;
+      if (smem > 48 * 1024)
+        OGCP_CUDA(cudaFuncSetAttribute(k_zero_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_zero_compact<<<(unsigned)zblocks, kScanThreads, smem, s>>>(zs, scr.cand.as<int32_t>(), rows_max,
+                                                                   scr.miss.as<uint8_t>(), scr.zoff.as<long long>(),
+                                                                   q, zero_subs, z_hits_before, hit_in_q);
+      ctx->count();
+      if (in_place) {
+        k_zero_copyback<<<std::min(ceil_div_i(q * d, 256), kNumSMs * 4), 256, 0, s>>>(hit_in_q, zero_subs,
+                                                                                     scr.cand.as<int32_t>(), q * d);
+        ctx->count();
+        out.zsub = scr.cand.as<int32_t>();
+      }
+    }
   }
   k_draw_status<<<1, 1, 0, s>>>(nz_stream ? p : 0, nz_avail, q, z_misses, rows_max, ncol, z_elems, z_hits_before,
                                 (long long)budget, code, ctx->flags.as<DevFlags>());
   ctx->count();
   check_launch();
+  return out;
 }
 
 }  // namespace ogcp

@@ -17,8 +17,18 @@ struct MergedDraw {
 };
 
 void init_jump_table();
-void draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
-                  int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr,
-                  MergedDraw* merged = nullptr);
+// Where a draw left its zero stratum: zsub points at [rows x ndim] int32
+// coordinates -- zero_subs, or the candidate scratch of `scr` (valid until the
+// next draw with the same scratch).  Lazy layout (q_dev != nullptr): the rows
+// are candidate rows [0, *q_dev) and rows whose first coordinate is -1 are
+// rejected candidates to skip; otherwise exactly q accepted rows.
+struct DrawOut {
+  const int32_t* zsub;
+  const long long* q_dev;
+};
+
+DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
+                     int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr,
+                     MergedDraw* merged = nullptr, bool lazy = false);
 
 }  // namespace ogcp
