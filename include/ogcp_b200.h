@@ -142,6 +142,14 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
 enum { OGCP_OPT_MERGE_DRAWS = 1 };
 int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value);
 
+/* Multi-GPU (the reference is single-process): the
+ * ranks that share one stream each hold the slice and the model; the solves
+ * evaluate each rank's contiguous 1/world of every sample set and sum the
+ * factor gradients, the temporal-row gradient and the objective with NCCL
+ * (loaded at run time).  Rank 0 creates the id, the caller broadcasts it. */
+int ogcp_nccl_unique_id(uint8_t out[128]);
+int ogcp_ctx_init_comm(ogcp_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t world);
+
 /* ----------------------------------------------------------------- slice */
 /* SparseTensor.from_zero_based (tensor.py:75-119): validates bounds,
  * finiteness, stored zeros (unless allow_zero) and duplicates with the

@@ -75,6 +75,8 @@ _SIGS = {
     "ogcp_ctx_profile_read": (C.c_int, [C.c_void_p, C.c_int32, c_i64p, c_f64p]),
     "ogcp_ctx_profile_reset": (C.c_int, [C.c_void_p]),
     "ogcp_ctx_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
+    "ogcp_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "ogcp_ctx_init_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32]),
     "ogcp_slice_create": (C.c_int, [C.c_void_p, C.c_int32, c_i64p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
                                     C.POINTER(C.c_void_p)]),
     "ogcp_slice_create_i32": (C.c_int, [C.c_void_p, C.c_int32, c_i64p, C.c_int64, C.c_void_p, C.c_void_p,

@@ -1,0 +1,129 @@
+// NCCL communicator for the sample-sharded solves.  NCCL is loaded with dlopen
+// (libnccl.so.2 -- the copy torch already mapped, or the system one), so the
+// engine library itself has no link-time NCCL dependency; the unique id is
+// exchanged by the caller (torch.distributed broadcast, 128 bytes).
+//
+// Per factor iteration the ranks exchange the d factor-gradient matrices
+// (sum, one allreduce over the contiguous gradient buffer); per weight
+// iteration the R-vector gradient; per objective evaluation one fp64 partial;
+// per epoch the error word.  Adam then runs replicated on identical inputs, so
+// the factors stay bitwise identical across ranks.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "comm.cuh"
+
+namespace ogcp {
+
+namespace {
+
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& api() {
+  static NcclApi a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      a.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (a.lib) break;
+    }
+    if (!a.lib) return;
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(a.lib, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(a.lib, "ncclCommInitRank"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(a.lib, "ncclAllReduce"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.lib, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(a.lib, "ncclGetErrorString"));
+  });
+  if (!a.lib || !a.GetUniqueId || !a.CommInitRank || !a.AllReduce)
+    throw Error(OGCP_E_INTERNAL, "NCCL (libnccl.so.2) is not available for the multi-GPU path");
+  return a;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Error(OGCP_E_CUDA, std::string(what) + ": " + (api().GetErrorString ? api().GetErrorString(r) : "nccl"));
+}
+
+__global__ void k_flags_pack(const DevFlags* f, long long* pk) {
+  if (threadIdx.x || blockIdx.x) return;
+  for (int i = 0; i < 4; ++i) pk[i] = f->first_code[i];
+  pk[4] = (f->data_bits & 1u) ? 1 : 0;
+  pk[5] = (f->data_bits & 2u) ? 1 : 0;
+  pk[6] = (f->data_bits & kMergeOverflowBit) ? 1 : 0;
+  pk[7] = 0;
+}
+
+__global__ void k_flags_unpack(DevFlags* f, const long long* pk) {
+  if (threadIdx.x || blockIdx.x) return;
+  for (int i = 0; i < 4; ++i) f->first_code[i] = pk[i];
+  f->data_bits = (pk[4] ? 1u : 0u) | (pk[5] ? 2u : 0u) | (pk[6] ? kMergeOverflowBit : 0u);
+}
+
+}  // namespace
+
+void comm_allreduce_sum(Ctx* ctx, float* p, size_t n) {
+  if (ctx->world <= 1 || n == 0) return;
+  nccl_check(api().AllReduce(p, p, n, ncclFloat32, ncclSum, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");
+}
+
+void comm_allreduce_sum(Ctx* ctx, double* p, size_t n) {
+  if (ctx->world <= 1 || n == 0) return;
+  nccl_check(api().AllReduce(p, p, n, ncclFloat64, ncclSum, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");
+}
+
+void comm_sync_flags(Ctx* ctx) {
+  if (ctx->world <= 1) return;
+  long long* pk = static_cast<long long*>(ctx->flagpack.ensure(8 * sizeof(long long)));
+  k_flags_pack<<<1, 1, 0, ctx->stream>>>(ctx->flags.as<DevFlags>(), pk);
+  nccl_check(api().AllReduce(pk, pk, 4, ncclInt64, ncclMin, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");
+  nccl_check(api().AllReduce(pk + 4, pk + 4, 4, ncclInt64, ncclMax, (ncclComm_t)ctx->comm, ctx->stream),
+             "ncclAllReduce");
+  k_flags_unpack<<<1, 1, 0, ctx->stream>>>(ctx->flags.as<DevFlags>(), pk);
+  ctx->count(2);
+  check_launch();
+}
+
+void comm_init(Ctx* ctx, const uint8_t* id, int rank, int world) {
+  if (world < 1 || rank < 0 || rank >= world) throw Error(OGCP_E_USAGE, "bad rank / world size");
+  if (world == 1) {
+    ctx->rank = 0;
+    ctx->world = 1;
+    return;
+  }
+  ncclUniqueId uid;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm;
+  OGCP_CUDA(cudaSetDevice(ctx->device));
+  nccl_check(api().CommInitRank(&comm, world, uid, rank), "ncclCommInitRank");
+  ctx->comm = comm;
+  ctx->rank = rank;
+  ctx->world = world;
+}
+
+void comm_unique_id(uint8_t* out) {
+  ncclUniqueId uid;
+  nccl_check(api().GetUniqueId(&uid), "ncclGetUniqueId");
+  memcpy(out, &uid, sizeof(uid));
+}
+
+void comm_destroy(Ctx* ctx) {
+  if (ctx->comm && api().CommDestroy) api().CommDestroy((ncclComm_t)ctx->comm);
+  ctx->comm = nullptr;
+  ctx->world = 1;
+  ctx->rank = 0;
+}
+
+}  // namespace ogcp

@@ -136,6 +136,10 @@ struct Ctx {
   Profiler prof;
   double slack = 1.0;           // sampler over-provisioning multiplier (grows on shortfall)
   bool merge_draws = true;      // merged (count) form of dense nonzero draws in the solves
+  // multi-GPU: NCCL communicator over the ranks that share one stream of slices
+  void* comm = nullptr;         // ncclComm_t
+  int rank = 0, world = 1;
+  DevBuf flagpack;
   // scratch
   DevBuf flags;                 // DevFlags
   DevBuf draw_a, draw_b, draw_c, draw_d, draw_e;   // sampler scratch

@@ -144,15 +144,20 @@ struct SampleStream {
     lane = lane_;
     gl = lane & (G - 1);
     nd = D > 0 ? D : M_.ndim;
+    int64_t lo = 0, hi = total;
+    if (S.shard_world > 1) {  // sample-sharded multi-GPU solve: this rank's contiguous share
+      lo = total * S.shard_rank / S.shard_world;
+      hi = total * (S.shard_rank + 1) / S.shard_world;
+    }
     if (contiguous) {
-      const int64_t per = ((total + nwarps - 1) / nwarps + SPB - 1) / SPB * SPB;
-      b = warp * per;
-      end = min(total, b + per);
+      const int64_t per = ((hi - lo + nwarps - 1) / nwarps + SPB - 1) / SPB * SPB;
+      b = lo + warp * per;
+      end = min(hi, b + per);
       stride = SPB;
     } else {
       stride = nwarps * SPB;
-      b = warp * SPB;
-      end = total;
+      b = lo + warp * SPB;
+      end = hi;
     }
     int o0[U];
     float c0[U];

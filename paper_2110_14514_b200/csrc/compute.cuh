@@ -20,6 +20,7 @@ struct SamplesP {
   const long long* p_dev;   // nullable: distinct nonzero count (merged form)
   const uint8_t* cnt;       // nullable: multiplicity per merged nonzero
   const long long* q_dev;   // nullable: lazy zero layout, rows [0, *q_dev) with -1-flagged rows skipped
+  int shard_rank, shard_world;  // multi-GPU: this rank evaluates its contiguous 1/world of the samples
 };
 
 struct GradPtrs {

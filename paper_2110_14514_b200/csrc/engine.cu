@@ -13,6 +13,7 @@
 #include <memory>
 #include <string>
 
+#include "comm.cuh"
 #include "common.cuh"
 #include "compute.cuh"
 #include "sampler.cuh"
@@ -144,6 +145,15 @@ static SamplesP samples_of(const Slice* X, const int32_t* ord, int64_t p, const 
   S.p_dev = nullptr;
   S.cnt = nullptr;
   S.q_dev = nullptr;
+  S.shard_rank = 0;
+  S.shard_world = 1;
+  return S;
+}
+
+// Solve-time sample sets are evaluated sharded across the context's ranks.
+static SamplesP sharded(const Ctx* ctx, SamplesP S) {
+  S.shard_rank = ctx->rank;
+  S.shard_world = ctx->world;
   return S;
 }
 
@@ -299,14 +309,15 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   if (po > 0 || p > 0) x_domain_check(X, L.kind);
   static thread_local SampleBufs obj, grad;
   draw_sync(ctx, X, keyed(seed, {t, 2}), po, qo, cfg->samples.max_rejects, obj);
-  SamplesP So = obj.sample_set(X);
+  SamplesP So = sharded(ctx, obj.sample_set(X));
   precheck_draw(X, p, q);
   grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
   const int64_t budget = budget_of(q, cfg->samples.max_rejects);
   ctx->partials.ensure((size_t)kNumSMs * 8 * ldr * 8 + 64);
   double* part = ctx->partials.as<double>();
-  ctx->scalars.ensure(64 * 8);
+  ctx->scalars.ensure(64 * 8 + ldr * 8);
   double* dsc = ctx->scalars.as<double>();
+  double* gsum = dsc + 64;  // multi-GPU: the R-vector gradient summed across ranks
   double* hsc = ctx->host_scalars;
 
   long long ev = 1;
@@ -315,8 +326,10 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     const long long c = code_of(ev++, 1);
     int nb = objective_enqueue(ctx, So, M, s_f, L, part, c);
     sum_partials_enqueue(ctx, part, nb, 1, dsc);
+    comm_allreduce_sum(ctx, dsc, 1);
     OGCP_CUDA(cudaMemcpyAsync(hsc, dsc, 8, cudaMemcpyDeviceToHost, st));
     OGCP_CUDA(cudaMemcpyAsync(hsc + 8, ws, R * 8, cudaMemcpyDeviceToHost, st));
+    comm_sync_flags(ctx);
     fetch_flags(ctx);
     OGCP_CUDA(cudaStreamSynchronize(st));
     check_flags(ctx, X, L.kind, budget, "temporal weight solve", t);
@@ -341,14 +354,22 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
       const long long ev0 = ev;
       for (int it = 0; it < cfg->iters_weights; ++it) {
         const long long e = ev++;
-        SamplesP Sg = grad.draw(ctx, X, keyed(seed, {t, 1, epoch, it}), budget, code_of(e, 0));
+        SamplesP Sg = sharded(ctx, grad.draw(ctx, X, keyed(seed, {t, 1, epoch, it}), budget, code_of(e, 0)));
         int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1));
         const int64_t cnt = i + it + 1;
         const double rate_i = rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
                               (1.0 - std::pow(cfg->beta1, (double)cnt));
-        weight_step_enqueue(ctx, part, nb, R, ldr, ws, s_f, cfg->reg_weights, rate_i, cfg->beta1, cfg->beta2,
+        const double* gparts = part;
+        if (ctx->world > 1) {  // sum the shard gradients across ranks, then the replicated step
+          sum_partials_enqueue(ctx, part, nb, ldr, gsum);
+          comm_allreduce_sum(ctx, gsum, (size_t)ldr);
+          gparts = gsum;
+          nb = 1;
+        }
+        weight_step_enqueue(ctx, gparts, nb, R, ldr, ws, s_f, cfg->reg_weights, rate_i, cfg->beta1, cfg->beta2,
                             cfg->adam_eps, cfg->lower_bound, code_of(e, 2));
       }
+      comm_sync_flags(ctx);
       fetch_flags(ctx);
       OGCP_CUDA(cudaStreamSynchronize(st));
       int r = check_flags(ctx, X, L.kind, budget, "temporal weight solve", t);
@@ -444,6 +465,8 @@ static double factor_objective(Ctx* ctx, const Slice* X, const SamplesP& So, con
   reset_flags(ctx);
   int nb = objective_enqueue(ctx, So, M, s_f, L, part, code);
   sum_partials_enqueue(ctx, part, nb, 1, dsc);
+  const bool collective = So.shard_world > 1;
+  if (collective) comm_allreduce_sum(ctx, dsc, 1);  // the data term is per-shard; Grams are replicated
   const bool hist = cfg->hist_weight != 0.0 && H > 0;
   const bool reg = cfg->reg_factors != 0.0;
   if (hist || reg) {
@@ -460,6 +483,7 @@ static double factor_objective(Ctx* ctx, const Slice* X, const SamplesP& So, con
   }
   (void)RR;
   OGCP_CUDA(cudaMemcpyAsync(hsc, dsc, 3 * 8, cudaMemcpyDeviceToHost, st));
+  if (collective) comm_sync_flags(ctx);
   fetch_flags(ctx);
   OGCP_CUDA(cudaStreamSynchronize(st));
   check_flags(ctx, X, L.kind, budget, "factor solve", t);
@@ -490,7 +514,7 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
                              ogcp_adam_state* ad, double rate_i, const Pcg64& g, int64_t p, int64_t q,
                              int64_t budget, FactorWork& W, long long ev) {
   const int RR = M.rank * M.rank;
-  SamplesP Sg = W.grad.draw(ctx, X, g, budget, code_of(ev, 0));
+  SamplesP Sg = sharded(ctx, W.grad.draw(ctx, X, g, budget, code_of(ev, 0)));
   (void)p;
   (void)q;
   float* gp[kMaxModes];
@@ -500,6 +524,7 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
     off += (size_t)M.dims[k] * M.ldr;
   }
   sgrad_enqueue(ctx, Sg, M, s_f, L, gp, code_of(ev, 1));
+  comm_allreduce_sum(ctx, W.grads.as<float>(), off);  // multi-GPU: sum of the shard gradients
   if (hist) {
     grams_pc_enqueue(ctx, M, old_factors, W.hb);
     hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), W.hb.C.as<double>(), W.hb.S.as<double>(),
@@ -567,7 +592,7 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
   if (po > 0 || p > 0) x_domain_check(X, L.kind);
   draw_sync(ctx, X, keyed(seed, {t, 4}), po, qo, cfg->samples.max_rejects, W.obj);
-  SamplesP So = W.obj.sample_set(X);
+  SamplesP So = sharded(ctx, W.obj.sample_set(X));
   precheck_draw(X, p, q);
   W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
   const int64_t budget = budget_of(q, cfg->samples.max_rejects);
@@ -590,6 +615,7 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
         factor_iteration(ctx, X, M, A, s_f, L, old_factors, hist, cfg, ad, rate_i, keyed(seed, {t, 3, epoch, it}),
                          p, q, budget, W, ev++);
       }
+      comm_sync_flags(ctx);
       fetch_flags(ctx);
       OGCP_CUDA(cudaStreamSynchronize(st));
       int r = check_flags(ctx, X, L.kind, budget, "factor solve", t);
@@ -712,6 +738,7 @@ int ogcp_ctx_destroy(ogcp_ctx* ctx) {
   OGCP_API_BEGIN
   if (ctx) {
     cudaStreamSynchronize(ctx->stream);
+    comm_destroy(ctx);
     if (ctx->host_scalars) cudaFreeHost(ctx->host_scalars);
     if (ctx->host_flags) cudaFreeHost(ctx->host_flags);
     delete ctx;
@@ -745,6 +772,18 @@ int ogcp_ctx_profile_read(ogcp_ctx* ctx, int32_t cls, int64_t* brackets, double*
 int ogcp_ctx_profile_reset(ogcp_ctx* ctx) {
   OGCP_API_BEGIN
   ctx->prof.reset();
+  OGCP_API_END
+}
+
+int ogcp_nccl_unique_id(uint8_t out[128]) {
+  OGCP_API_BEGIN
+  comm_unique_id(out);
+  OGCP_API_END
+}
+
+int ogcp_ctx_init_comm(ogcp_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t world) {
+  OGCP_API_BEGIN
+  comm_init(ctx, id, rank, world);
   OGCP_API_END
 }
 
