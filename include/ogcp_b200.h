@@ -61,6 +61,10 @@ typedef struct {
   int64_t obj_zeros;
   uint64_t seed;
   int64_t max_rejects;
+  /* Extension (not in the reference; BASELINE configs[2]):
+   * semi-stratified estimator -- nonzero stratum (eta/p)(g(x,m) - g(0,m)),
+   * uniform stratum (omega/q) g(0,m) over the whole box, no rejection. */
+  int32_t semi_stratified;
 } ogcp_sampler_config;
 
 /* solvers.py:40-69 SolverConfig (gradient_mode "sampled", temporal_solver "sgd");
@@ -176,6 +180,10 @@ int ogcp_slice_contains(ogcp_ctx* ctx, const ogcp_slice* s, const int64_t* subs0
 int ogcp_draw_samples(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const int64_t* key,
                       int32_t nkey, int64_t p, int64_t q, int64_t max_rejects,
                       int32_t* ordinals_dev, int32_t* zero_subs_dev);
+/* flags bit 0: semi-stratified draw (q uniform cells, no rejection). */
+int ogcp_draw_samples_ex(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const int64_t* key,
+                         int32_t nkey, int64_t p, int64_t q, int64_t max_rejects, int32_t flags,
+                         int32_t* ordinals_dev, int32_t* zero_subs_dev);
 
 /* ------------------------------------------------------------- estimators */
 /* Data part of factor_gradients (solvers.py:139-140 = sampled_mttkrp(Y,k)*s,
@@ -187,6 +195,27 @@ int ogcp_sampled_gradient(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ord
                           int64_t p, const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m,
                           const double* weights, const ogcp_loss* loss, float* const* grads_dev,
                           double* gw_dev);
+
+/* flags bit 0: the sample set is a semi-stratified one (ogcp_draw_samples_ex). */
+int ogcp_sampled_gradient_ex(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev,
+                             int64_t p, const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m,
+                             const double* weights, const ogcp_loss* loss, int32_t flags,
+                             float* const* grads_dev, double* gw_dev);
+
+/* sampled_gradient_tensor (sampling.py:209-239) in parity form: the merged Y of
+ * a replayed sample set, bit-exact in layout -- unique coordinates in
+ * ascending linear order (np.unique), each taken from its first draw, values
+ * summed in draw order (np.bincount) in fp64.  coords_out: device int32
+ * [(p+q) x ndim], vals_out: device fp64 [p+q]; *n_out = number of entries. */
+int ogcp_gradient_tensor(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev, int64_t p,
+                         const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m, const double* weights,
+                         const ogcp_loss* loss, int32_t* coords_out, double* vals_out, int64_t* n_out);
+/* Row-segment layout of mode `mode` of a COO coordinate list (device int32
+ * [n x ndim]): perm_out = stable argsort of column `mode`
+ * (np.argsort(..., kind="stable")), offsets_out[r] = start of row r, r = 0..dim
+ * (cumsum of bincount) -- the layout a sort-by-row MTTKRP walks. */
+int ogcp_segment_layout(ogcp_ctx* ctx, const int32_t* coords_dev, int64_t n, int32_t ndim, int32_t mode,
+                        int64_t dim, int32_t* perm_out, int64_t* offsets_out);
 
 /* Full factor_gradients (solvers.py:127-142, 159-179): data term + lambda*A
  * + history Gram term.  old_factors may be NULL when H == 0 or hist_weight == 0.

@@ -32,7 +32,8 @@ class LossC(C.Structure):
 
 class SamplerC(C.Structure):
     _fields_ = [("grad_nonzeros", C.c_int64), ("grad_zeros", C.c_int64), ("obj_nonzeros", C.c_int64),
-                ("obj_zeros", C.c_int64), ("seed", C.c_uint64), ("max_rejects", C.c_int64)]
+                ("obj_zeros", C.c_int64), ("seed", C.c_uint64), ("max_rejects", C.c_int64),
+                ("semi_stratified", C.c_int32)]
 
 
 class SolverC(C.Structure):
@@ -75,6 +76,14 @@ _SIGS = {
     "ogcp_ctx_profile_read": (C.c_int, [C.c_void_p, C.c_int32, c_i64p, c_f64p]),
     "ogcp_ctx_profile_reset": (C.c_int, [C.c_void_p]),
     "ogcp_ctx_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
+    "ogcp_sampled_gradient_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                           C.POINTER(ModelC), c_f64p, C.POINTER(LossC), C.c_int32,
+                                           C.POINTER(C.c_void_p), C.c_void_p]),
+    "ogcp_gradient_tensor": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                       C.POINTER(ModelC), c_f64p, C.POINTER(LossC), C.c_void_p, C.c_void_p,
+                                       c_i64p]),
+    "ogcp_segment_layout": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int64,
+                                      C.c_void_p, C.c_void_p]),
     "ogcp_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "ogcp_ctx_init_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32]),
     "ogcp_slice_create": (C.c_int, [C.c_void_p, C.c_int32, c_i64p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
@@ -86,6 +95,8 @@ _SIGS = {
     "ogcp_slice_contains": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "ogcp_draw_samples": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, c_i64p, C.c_int32, C.c_int64, C.c_int64,
                                     C.c_int64, C.c_void_p, C.c_void_p]),
+    "ogcp_draw_samples_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, c_i64p, C.c_int32, C.c_int64,
+                                       C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
     "ogcp_sampled_gradient": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                         C.POINTER(ModelC), c_f64p, C.POINTER(LossC), C.POINTER(C.c_void_p),
                                         C.c_void_p]),

@@ -355,7 +355,9 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
       const float m = model_value<D, G, V>(s[u], s4);
       if (valid[u]) {
         bits |= domain_bits(L.kind, m);
-        const float y = s[u].scale * dloss(L.kind, s[u].x, m, L.eps);
+        float y = dloss(L.kind, s[u].x, m, L.eps);
+        if (S.semi && s[u].nz) y -= dloss(L.kind, 0.0f, m, L.eps);  // semi-stratified nonzero stratum
+        y *= s[u].scale;
         if (seg0 && s[u].idx[0] != seg_row) {
           if (seg_row >= 0) {
 #pragma unroll
@@ -443,7 +445,9 @@ __global__ void __launch_bounds__(kThreads) k_wgrad(SamplesP S, ModelP M, const 
       const float m = model_value<D, G, V>(s[u], s4);
       if (valid[u]) {
         bits |= domain_bits(L.kind, m);
-        const float y = s[u].scale * dloss(L.kind, s[u].x, m, L.eps);
+        float y = dloss(L.kind, s[u].x, m, L.eps);
+        if (S.semi && s[u].nz) y -= dloss(L.kind, 0.0f, m, L.eps);  // semi-stratified nonzero stratum
+        y *= s[u].scale;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           float4 pr = s[u].a[0][v];
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(kThreads) k_objective(SamplesP S, ModelP M, co
       if (valid[u] && gl == 0) {
         bits |= domain_bits(L.kind, m);
         double f = floss(L.kind, (double)s[u].x, (double)m, L.eps_d);
-        if (MODE == 1) f -= floss(L.kind, 0.0, (double)m, L.eps_d);
+        if (MODE == 1 || (S.semi && s[u].nz)) f -= floss(L.kind, 0.0, (double)m, L.eps_d);
         if (s[u].nz) acc_nz += f * (double)s[u].cnt;
         else acc_z += f;
       }

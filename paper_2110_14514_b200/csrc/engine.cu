@@ -16,6 +16,7 @@
 #include "comm.cuh"
 #include "common.cuh"
 #include "compute.cuh"
+#include "hash.cuh"
 #include "sampler.cuh"
 
 namespace ogcp {
@@ -23,6 +24,10 @@ namespace ogcp {
 template <class CT, class VT>
 Slice* slice_create_impl(Ctx* ctx, int ndim, const int64_t* dims, int64_t nnz, const CT* subs, const VT* vals,
                          int allow_zero);
+int64_t gradient_tensor_impl(Ctx* ctx, const SamplesP& S, const ModelP& M, const double* w_dev, const LossP& L,
+                             const Strides& st, int32_t* ycoords, double* yvals, unsigned int* bad_host);
+void segment_layout_impl(Ctx* ctx, const int32_t* coords, int64_t n, int ndim, int mode, int64_t dim, int32_t* perm,
+                         int64_t* offsets);
 void slice_contains_impl(Ctx* ctx, const Slice* s, const int64_t* subs, int64_t n, uint8_t* hit);
 
 static thread_local std::string g_last_error;
@@ -147,6 +152,16 @@ static SamplesP samples_of(const Slice* X, const int32_t* ord, int64_t p, const 
   S.q_dev = nullptr;
   S.shard_rank = 0;
   S.shard_world = 1;
+  S.semi = 0;
+  return S;
+}
+
+// Semi-stratified extension: uniform stratum scale omega/q, nonzero draws corrected by -g(0, m).
+static SamplesP semi_of(const Slice* X, SamplesP S, bool semi) {
+  if (!semi) return S;
+  S.semi = 1;
+  S.zero_scale = S.q ? X->omega_d / (double)S.q : 0.0;
+  if (X->omega_fits && S.q) S.zero_scale = (double)X->omega / (double)S.q;
   return S;
 }
 
@@ -176,6 +191,7 @@ struct SampleBufs {
   DrawScratch scr;
   MergedDraw md;
   bool merged = false;
+  bool semi = false;  // semi-stratified extension
   const int32_t* zsub = nullptr;   // where the last draw left the zero coordinates
   const long long* q_dev = nullptr;  // lazy zero layout row count (device)
   int64_t p = 0, q = 0;
@@ -189,7 +205,7 @@ struct SampleBufs {
   // Enqueue the draw of this buffer set and return its device sample set.
   SamplesP draw(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t budget, long long code) {
     const DrawOut o = draw_enqueue(ctx, X, g, p, q, budget, merged ? nullptr : ord.as<int32_t>(),
-                                   zero.as<int32_t>(), code, scr, merged ? &md : nullptr, /*lazy=*/true);
+                                   zero.as<int32_t>(), code, scr, merged ? &md : nullptr, /*lazy=*/true, semi);
     zsub = o.zsub;
     q_dev = o.q_dev;
     return sample_set(X);
@@ -199,11 +215,11 @@ struct SampleBufs {
 
 SamplesP SampleBufs::sample_set(const Slice* X) const {
   if (!merged) {
-    SamplesP S = samples_of(X, ord.as<int32_t>(), p, zsub, q);
+    SamplesP S = semi_of(X, samples_of(X, ord.as<int32_t>(), p, zsub, q), semi);
     S.q_dev = q_dev;
     return S;
   }
-  SamplesP S = samples_of(X, md.ord.as<int32_t>(), p, zsub, q);
+  SamplesP S = semi_of(X, samples_of(X, md.ord.as<int32_t>(), p, zsub, q), semi);
   S.q_dev = q_dev;
   S.p = std::min<int64_t>(p, X->nnz);  // upper bound of the distinct count
   S.p_dev = md.count;
@@ -221,14 +237,15 @@ static bool use_merged(const Ctx* ctx, const Slice* X, int64_t p) {
 
 // Synchronous draw with shortfall retry (used for objective sets).
 static void draw_sync(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t max_rejects,
-                      SampleBufs& b) {
-  precheck_draw(X, p, q);
+                      SampleBufs& b, bool semi = false) {
+  precheck_draw(X, p, semi ? 0 : q);
   b.size(p, q, X->ndim);
+  b.semi = semi;
   const int64_t budget = budget_of(q, max_rejects);
   for (int attempt = 0;; ++attempt) {
     reset_flags(ctx);
     const DrawOut o = draw_enqueue(ctx, X, g, p, q, budget, b.ord.as<int32_t>(), b.zero.as<int32_t>(), 0, b.scr,
-                                   nullptr, /*lazy=*/true);
+                                   nullptr, /*lazy=*/true, semi);
     b.zsub = o.zsub;
     b.q_dev = o.q_dev;
     fetch_flags(ctx);
@@ -308,10 +325,12 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
   if (po > 0 || p > 0) x_domain_check(X, L.kind);
   static thread_local SampleBufs obj, grad;
-  draw_sync(ctx, X, keyed(seed, {t, 2}), po, qo, cfg->samples.max_rejects, obj);
+  const bool semi = cfg->samples.semi_stratified != 0;
+  draw_sync(ctx, X, keyed(seed, {t, 2}), po, qo, cfg->samples.max_rejects, obj, semi);
   SamplesP So = sharded(ctx, obj.sample_set(X));
-  precheck_draw(X, p, q);
+  precheck_draw(X, p, semi ? 0 : q);
   grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+  grad.semi = semi;
   const int64_t budget = budget_of(q, cfg->samples.max_rejects);
   ctx->partials.ensure((size_t)kNumSMs * 8 * ldr * 8 + 64);
   double* part = ctx->partials.as<double>();
@@ -591,10 +610,12 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   resolve_counts(cfg->samples.obj_nonzeros, cfg->samples.obj_zeros, X, &po, &qo);
   resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
   if (po > 0 || p > 0) x_domain_check(X, L.kind);
-  draw_sync(ctx, X, keyed(seed, {t, 4}), po, qo, cfg->samples.max_rejects, W.obj);
+  const bool semi = cfg->samples.semi_stratified != 0;
+  draw_sync(ctx, X, keyed(seed, {t, 4}), po, qo, cfg->samples.max_rejects, W.obj, semi);
   SamplesP So = sharded(ctx, W.obj.sample_set(X));
-  precheck_draw(X, p, q);
+  precheck_draw(X, p, semi ? 0 : q);
   W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+  W.grad.semi = semi;
   const int64_t budget = budget_of(q, cfg->samples.max_rejects);
 
   long long ev = 1;
@@ -775,6 +796,35 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx) {
   OGCP_API_END
 }
 
+int ogcp_gradient_tensor(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev, int64_t p,
+                         const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m, const double* weights,
+                         const ogcp_loss* loss, int32_t* coords_out, double* vals_out, int64_t* n_out) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  check_model_slice(M, s);
+  LossP L = loss_of(loss);
+  if (p > 0) x_domain_check(s, L.kind);
+  SamplesP S = samples_of(s, ordinals_dev, p, zero_subs_dev, q);
+  static thread_local DevBuf wdev;
+  wdev.ensure((size_t)M.rank * 8);
+  OGCP_CUDA(cudaMemcpyAsync(wdev.ptr, weights, (size_t)M.rank * 8, cudaMemcpyHostToDevice, ctx->stream));
+  Strides st;
+  for (int k = 0; k < kMaxModes; ++k) st.s[k] = k < s->ndim ? s->strides[k] : 0;
+  unsigned int bad = 0;
+  *n_out = gradient_tensor_impl(ctx, S, M, wdev.as<double>(), L, st, coords_out, vals_out, &bad);
+  if (bad & 1u) throw Error(OGCP_E_DATA, std::string(kind_name(L.kind)) + " loss: non-finite input");
+  if (bad & 2u) throw Error(OGCP_E_DATA, std::string(kind_name(L.kind)) + " loss requires m >= 0");
+  OGCP_API_END
+}
+
+int ogcp_segment_layout(ogcp_ctx* ctx, const int32_t* coords_dev, int64_t n, int32_t ndim, int32_t mode, int64_t dim,
+                        int32_t* perm_out, int64_t* offsets_out) {
+  OGCP_API_BEGIN
+  if (mode < 0 || mode >= ndim) throw Error(OGCP_E_USAGE, "mode out of range");
+  segment_layout_impl(ctx, coords_dev, n, ndim, mode, dim, perm_out, offsets_out);
+  OGCP_API_END
+}
+
 int ogcp_nccl_unique_id(uint8_t out[128]) {
   OGCP_API_BEGIN
   comm_unique_id(out);
@@ -832,18 +882,26 @@ int ogcp_slice_contains(ogcp_ctx* ctx, const ogcp_slice* s, const int64_t* subs0
 
 int ogcp_draw_samples(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const int64_t* key, int32_t nkey, int64_t p,
                       int64_t q, int64_t max_rejects, int32_t* ordinals_dev, int32_t* zero_subs_dev) {
+  return ogcp_draw_samples_ex(ctx, s, seed, key, nkey, p, q, max_rejects, 0, ordinals_dev, zero_subs_dev);
+}
+
+int ogcp_draw_samples_ex(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const int64_t* key, int32_t nkey,
+                         int64_t p, int64_t q, int64_t max_rejects, int32_t flags, int32_t* ordinals_dev,
+                         int32_t* zero_subs_dev) {
   OGCP_API_BEGIN
   if (p < 0 || q < 0) throw Error(OGCP_E_USAGE, "counts must be >= 0");
+  const bool semi = (flags & 1) != 0;
   uint64_t k[16];
   if (nkey < 0 || nkey > 16) throw Error(OGCP_E_USAGE, "key too long");
   for (int i = 0; i < nkey; ++i) k[i] = (uint64_t)key[i];
   Pcg64 g = seedseq_pcg64(seed, k, nkey);
-  precheck_draw(s, p, q);
+  precheck_draw(s, p, semi ? 0 : q);
   const int64_t budget = budget_of(q, max_rejects);
   static thread_local DrawScratch scr;
   for (int attempt = 0;; ++attempt) {
     reset_flags(ctx);
-    const int32_t* z = draw_enqueue(ctx, s, g, p, q, budget, ordinals_dev, zero_subs_dev, 0, scr).zsub;
+    const int32_t* z =
+        draw_enqueue(ctx, s, g, p, q, budget, ordinals_dev, zero_subs_dev, 0, scr, nullptr, false, semi).zsub;
     if (q > 0 && z != zero_subs_dev)
       OGCP_CUDA(cudaMemcpyAsync(zero_subs_dev, z, (size_t)q * s->ndim * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     fetch_flags(ctx);
@@ -858,6 +916,12 @@ int ogcp_draw_samples(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const i
 int ogcp_sampled_gradient(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev, int64_t p,
                           const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m, const double* weights,
                           const ogcp_loss* loss, float* const* grads_dev, double* gw_dev) {
+  return ogcp_sampled_gradient_ex(ctx, s, ordinals_dev, p, zero_subs_dev, q, m, weights, loss, 0, grads_dev, gw_dev);
+}
+
+int ogcp_sampled_gradient_ex(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ordinals_dev, int64_t p,
+                             const int32_t* zero_subs_dev, int64_t q, const ogcp_model* m, const double* weights,
+                             const ogcp_loss* loss, int32_t flags, float* const* grads_dev, double* gw_dev) {
   OGCP_API_BEGIN
   ModelP M = model_of(m);
   check_model_slice(M, s);
@@ -866,7 +930,7 @@ int ogcp_sampled_gradient(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ord
   ctx->wsolve.ensure((size_t)M.ldr * (6 * 8 + 4));
   float* s_f = reinterpret_cast<float*>(ctx->wsolve.as<double>() + 6 * M.ldr);
   upload_weights(ctx, weights, M.rank, M.ldr, s_f);
-  SamplesP S = samples_of(s, ordinals_dev, p, zero_subs_dev, q);
+  SamplesP S = semi_of(s, samples_of(s, ordinals_dev, p, zero_subs_dev, q), (flags & 1) != 0);
   reset_flags(ctx);
   if (grads_dev) sgrad_enqueue(ctx, S, M, s_f, L, grads_dev, code_of(1, 1));
   if (gw_dev) {

@@ -561,6 +561,20 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_locate(const uint32_t* __
   }
 }
 
+// Semi-stratified uniform stratum with size-1 modes: [row][ncol] -> [row][d] (zeros inserted).
+__global__ void k_expand_rows(ZeroSpec zs, const int32_t* __restrict__ cand, int64_t rows, int32_t* __restrict__ out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < zs.ndim; ++k) out[r * zs.ndim + k] = zs.colmap[k] < 0 ? 0 : cand[r * zs.ncol + zs.colmap[k]];
+}
+
+__global__ void k_semi_status(int64_t p, const long long* nz_avail, long long need_elems, const long long* z_elems,
+                              long long code, DevFlags* flags) {
+  if (threadIdx.x || blockIdx.x) return;
+  const bool short_nz = p > 0 && nz_avail && *nz_avail < p;
+  const bool short_z = need_elems > 0 && *z_elems < need_elems;
+  if (short_nz || short_z) atomicMin(&flags->first_code[kFlagShortfall], code);
+}
+
 // Slow path of the in-place layout: copy the compacted zeros back over the candidates.
 __global__ void k_zero_copyback(const unsigned long long* __restrict__ hit_in_q, const int32_t* __restrict__ src,
                                 int32_t* __restrict__ dst, int64_t n) {
@@ -757,7 +771,7 @@ static double reject_rate(uint32_t n) { return (double)lemire_threshold(n) / 429
 // code: event code (event*4) recorded on sampling errors / shortfall.
 DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
                      int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr, MergedDraw* merged,
-                     bool lazy) {
+                     bool lazy, bool semi) {
   DrawOut out;
   out.zsub = zero_subs;
   out.q_dev = nullptr;
@@ -846,6 +860,33 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
       }
     zs.ncol = ncol;
     sp.ncol = ncol;
+    if (semi) {
+      // semi-stratified: the first q uniform cells of the box, no rejection
+      if (ncol > 0) {
+        const int64_t target = q * ncol;
+        scr.cand.ensure((size_t)target * 4);
+        const double exp_words = (double)target / (1.0 - rmax);
+        const double sd = std::sqrt((double)target * rmax) / (1.0 - rmax);
+        const int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
+        const long long* w0 = nz_stream ? nz_end : nullptr;
+        run_stream_dispatch(ncol, ctx, sp, w0, target, words, scr.cand.as<int32_t>(), nullptr, z_elems, scr);
+      } else {
+        k_set_ll<<<1, 1, 0, s>>>(z_elems, 0);
+        ctx->count();
+      }
+      if (ncol == d) {
+        out.zsub = scr.cand.as<int32_t>();
+      } else {
+        k_expand_rows<<<std::min(ceil_div_i(q, 256), kNumSMs * 4), 256, 0, s>>>(zs, scr.cand.as<int32_t>(), q,
+                                                                               zero_subs);
+        ctx->count();
+      }
+      k_semi_status<<<1, 1, 0, s>>>(nz_stream ? p : 0, nz_avail, (long long)q * ncol, z_elems, code,
+                                    ctx->flags.as<DevFlags>());
+      ctx->count();
+      check_launch();
+      return out;
+    }
     const double rho = X->omega_d > 0 ? (double)eta / X->omega_d : 0.0;
     const double exp_rows = rho < 1.0 ? (double)q / (1.0 - rho) : 1e30;
     const double sd_rows = rho < 1.0 ? std::sqrt((double)q * rho) / (1.0 - rho) : 1e30;

@@ -27,8 +27,10 @@ struct DrawOut {
   const long long* q_dev;
 };
 
+// semi = true: the semi-stratified extension -- the q zero-stratum rows are the
+// first q uniform cells of the box (no rejection), exactly q rows at zsub.
 DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
                      int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr,
-                     MergedDraw* merged = nullptr, bool lazy = false);
+                     MergedDraw* merged = nullptr, bool lazy = false, bool semi = false);
 
 }  // namespace ogcp

@@ -68,6 +68,10 @@ class SamplerConfig:
     obj_zeros: int = 10000
     seed: int = 0
     max_rejects: Optional[int] = None
+    # Extension (not in the reference): semi-stratified estimator --
+    # q cells drawn uniformly from the whole box (no rejection), nonzero draws
+    # corrected by -g(0, m).  See oracle/ogcp_oracle.py draw_semi for the restatement.
+    semi_stratified: bool = False
 
     def __post_init__(self):
         for name in ("grad_nonzeros", "grad_zeros", "obj_nonzeros", "obj_zeros"):
@@ -86,7 +90,8 @@ class SamplerConfig:
     def _c(self):
         neg = lambda v: -1 if v is None else int(v)
         return _lib.SamplerC(neg(self.grad_nonzeros), int(self.grad_zeros), neg(self.obj_nonzeros),
-                             int(self.obj_zeros), int(self.seed), neg(self.max_rejects))
+                             int(self.obj_zeros), int(self.seed), neg(self.max_rejects),
+                             int(bool(self.semi_stratified)))
 
 
 def resolve_counts(nonzeros: Optional[int], zeros: int, X: SparseTensor) -> tuple:
@@ -146,18 +151,65 @@ def _key_of(rng) -> RngKey:
     raise TypeError("pass a generator made by rng_at(seed, *key); the engine replays that keyed stream")
 
 
-def draw_samples(X: SparseTensor, p: int, q: int, rng, max_rejects: Optional[int] = None) -> SampleSet:
-    """Draw p nonzeros and q zeros uniformly with replacement (sampling.py:108-153)."""
+def draw_samples(X: SparseTensor, p: int, q: int, rng, max_rejects: Optional[int] = None,
+                 semi_stratified: bool = False) -> SampleSet:
+    """Draw p nonzeros and q zeros uniformly with replacement (sampling.py:108-153).
+
+    semi_stratified (extension): the q cells are drawn uniformly from the whole box
+    without rejection (oracle/ogcp_oracle.py draw_semi)."""
     import torch
     k = _key_of(rng)
     ords = torch.empty(max(int(p), 0), dtype=torch.int32, device="cuda")
     zs = torch.empty((max(int(q), 0), X.ndim), dtype=torch.int32, device="cuda")
     key, kp = _lib.i64arr(list(k.key) or [0])
-    _lib.check(_lib.lib().ogcp_draw_samples(_lib.ctx(), X._handle, k.seed, kp, len(k.key), int(p), int(q),
-                                             -1 if max_rejects is None else int(max_rejects),
-                                             C.c_void_p(ords.data_ptr() if p else None),
-                                             C.c_void_p(zs.data_ptr() if q else None)))
-    return SampleSet(X, ords, zs)
+    _lib.check(_lib.lib().ogcp_draw_samples_ex(_lib.ctx(), X._handle, k.seed, kp, len(k.key), int(p), int(q),
+                                                -1 if max_rejects is None else int(max_rejects),
+                                                1 if semi_stratified else 0,
+                                                C.c_void_p(ords.data_ptr() if p else None),
+                                                C.c_void_p(zs.data_ptr() if q else None)))
+    s = SampleSet(X, ords, zs)
+    s.semi_stratified = bool(semi_stratified)
+    return s
+
+
+def sampled_gradient_tensor(X: SparseTensor, factors: Sequence[np.ndarray], weights: np.ndarray,
+                            loss: LossFunction, p: int, q: int, rng, max_rejects: Optional[int] = None
+                            ) -> SparseTensor:
+    """Sparse stratified approximation of the dense gradient tensor Y (sampling.py:209-239).
+
+    Draws on the GPU sampler (bit-exact), evaluates scale * f'(x, m) per draw in fp64 and
+    merges repeated coordinates exactly like np.unique + np.bincount (parity form; the
+    solves never materialise Y)."""
+    import torch
+    s = draw_samples(X, p, q, rng, max_rejects)
+    n = s.p + s.q
+    d = X.ndim
+    model = factors if isinstance(factors, DeviceModel) else DeviceModel.from_numpy(factors)
+    coords = torch.empty((max(n, 1), d), dtype=torch.int32, device="cuda")
+    vals = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    w, wp = _lib.f64arr(weights)
+    nu = C.c_int64(0)
+    _lib.check(_lib.lib().ogcp_gradient_tensor(
+        _lib.ctx(), X._handle, C.c_void_p(s.ord_dev.data_ptr() if s.p else None), s.p,
+        C.c_void_p(s.zero_dev.data_ptr() if s.q else None), s.q, C.byref(model.c()), wp, C.byref(loss._c()),
+        C.c_void_p(coords.data_ptr()), C.c_void_p(vals.data_ptr()), C.byref(nu)))
+    k = int(nu.value)
+    return SparseTensor.from_zero_based(X.dims, coords[:k].cpu().numpy().astype(np.int64),
+                                        vals[:k].cpu().numpy(), allow_zero_values=True)
+
+
+def segment_layout(Y: SparseTensor, mode: int) -> tuple:
+    """(perm, offsets) of mode ``mode``: the stable argsort of Y's mode coordinates and the
+    row offsets (cumsum of bincount) that a sort-by-row MTTKRP walks."""
+    import torch
+    coords = torch.from_numpy(np.ascontiguousarray(Y.subs0, dtype=np.int32)).cuda()
+    n = Y.nnz
+    dim = Y.dims[mode]
+    perm = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    offs = torch.empty(dim + 1, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().ogcp_segment_layout(_lib.ctx(), C.c_void_p(coords.data_ptr()), n, Y.ndim, int(mode), dim,
+                                               C.c_void_p(perm.data_ptr()), C.c_void_p(offs.data_ptr())))
+    return perm[:n].cpu().numpy().astype(np.int64), offs.cpu().numpy()
 
 
 def _window_arrays(window, rank):

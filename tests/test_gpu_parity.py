@@ -246,3 +246,39 @@ def test_dense_draw_solve_vs_oracle(merge):
     for a, b in zip(st.factors, ost.factors):
         assert rel_err(a, b) < 1e-4
     assert rel_err(st.weights_log[-1], s_t) < 1e-4
+
+
+def test_gradient_tensor_layout_bit_exact(golden_dir):
+    """Row A6: merged Y (np.unique + bincount, sampling.py:233-239) and the per-mode
+    row-segment layouts are bit-exact; values within fp32-factor tolerance."""
+    g = load(golden_dir, "grads.npz")
+    for ci in range(int(g["ncases"])):
+        c = lambda k: g[f"c{ci}_{k}"]
+        dims = tuple(int(d) for d in c("dims"))
+        X = P.SparseTensor.from_zero_based(dims, c("subs0"), c("vals"))
+        A = [c(f"A{k}") for k in range(len(dims))]
+        Y = P.sampled_gradient_tensor(X, A, c("weights"), P.make_loss(str(c("kind"))), int(c("p")), int(c("q")),
+                                      P.rng_at(13, 5, 3, 0, ci))
+        np.testing.assert_array_equal(Y.subs0, c("Y_subs0"))
+        assert rel_err(Y.vals, c("Y_vals")) < GRAD_RTOL
+        for k in range(len(dims)):
+            perm, offs = P.segment_layout(Y, k)
+            np.testing.assert_array_equal(perm, np.argsort(c("Y_subs0")[:, k], kind="stable"))
+            want = np.concatenate([[0], np.cumsum(np.bincount(c("Y_subs0")[:, k], minlength=dims[k]))])
+            np.testing.assert_array_equal(offs, want)
+
+
+def test_gradient_tensor_large_merge_vs_oracle():
+    rng = np.random.default_rng(12)
+    dims = (2000, 1500, 30)
+    lin = rng.choice(int(np.prod(dims)), size=300_000, replace=False)
+    subs0 = np.array(np.unravel_index(lin, dims)).T
+    vals = rng.integers(1, 5, size=lin.size).astype(float)
+    R = 5
+    A = [rng.uniform(0.1, 1.0, (d, R)) for d in dims]
+    w = rng.uniform(0.5, 1.5, R)
+    X = P.SparseTensor.from_zero_based(dims, subs0, vals)
+    Y = P.sampled_gradient_tensor(X, A, w, P.make_loss("poisson"), 600_000, 200_000, P.rng_at(2, 9, 3, 1, 4))
+    _, ys, yv = O.sampled_y(O.Slice(dims, subs0, vals), A, w, "poisson", 600_000, 200_000, O.keyed_rng(2, 9, 3, 1, 4))
+    np.testing.assert_array_equal(Y.subs0, ys)
+    assert rel_err(Y.vals, yv) < GRAD_RTOL
