@@ -806,17 +806,19 @@ __global__ void __launch_bounds__(kThreads) k_factor_update_wide(int64_t rows, i
                                                                  const float* __restrict__ Nk, float reg,
                                                                  float rate_i, float b1, float omb1, float b2,
                                                                  float omb2, float eps, float lower, DevFlags* flags,
-                                                                 long long code) {
+                                                                 long long code, int stage) {
   extern __shared__ float sm[];
   const bool hist = Mk != nullptr;
   const int RR = rank * rank;
-  if (hist) {
+  if (hist && stage) {  // Mk / Nk staged in shared memory when they fit, else read through L1/L2
     for (int i = threadIdx.x; i < RR; i += blockDim.x) {
       sm[i] = Mk[i];
       sm[RR + i] = Nk[i];
     }
   }
   __syncthreads();
+  const float* mm = stage ? sm : Mk;
+  const float* nn = stage ? sm + RR : Nk;
   const int lane = threadIdx.x & 31;
   const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
   const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / 32;
@@ -845,7 +847,7 @@ __global__ void __launch_bounds__(kThreads) k_factor_update_wide(int64_t rows, i
 #pragma unroll
             for (int j = 0; j < CPL; ++j) {
               const int cc = lane + j * 32;
-              if (cc < rank) h[j] += ar * sm[r * rank + cc] - aor * sm[RR + r * rank + cc];
+              if (cc < rank) h[j] += ar * mm[r * rank + cc] - aor * nn[r * rank + cc];
             }
           }
         }
@@ -886,15 +888,18 @@ __global__ void k_weight_step(const double* __restrict__ partials, int nblk, int
   ws[ldr + r] = u;
   ws[2 * ldr + r] = v;
   s_f[r] = (float)sn;
-  if (!isfinite(sn)) report(flags, kFlagDiverge, code, 0);
+  // the sample kernels evaluate in fp32: an iterate beyond fp32 range has diverged for this engine
+  if (!isfinite(sn) || !isfinite((float)sn)) report(flags, kFlagDiverge, code, 0);
 }
 
 // ------------------------------------------------------------------ history penalty
 // out[0] = sum_h coef_h * max(s_h' Q s_h, 0), Q = Poo - (Pon + Pon') + Pnn (all-mode Grams).
 __global__ void k_hist_penalty(int ndim, int rank, const double* __restrict__ Poo, const double* __restrict__ Pon,
                                const double* __restrict__ Pnn, const double* __restrict__ Ws,
-                               const double* __restrict__ coef, int H, double* __restrict__ out) {
-  extern __shared__ double q[];
+                               const double* __restrict__ coef, int H, double* __restrict__ out,
+                               double* __restrict__ qglobal) {
+  extern __shared__ double qs[];
+  double* q = qglobal ? qglobal : qs;  // Q in shared memory when it fits (R <= 160)
   const int RR = rank * rank;
   for (int e = threadIdx.x; e < RR; e += blockDim.x) {
     const int i = e / rank, j = e % rank;
@@ -1167,7 +1172,9 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
       default: launch(k_factor_update<32>); break;
     }
   } else {
-    const size_t smem = Mk ? (size_t)2 * rank * rank * 4 : 0;
+    const size_t need = Mk ? (size_t)2 * rank * rank * 4 : 0;
+    const bool stage = need > 0 && need <= 200 * 1024;
+    const size_t smem = stage ? need : 0;
     auto launch = [&](auto kern) {
       if (smem > 48 * 1024)
         OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1175,7 +1182,7 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + groups - 1) / groups, kNumSMs * 4));
       kern<<<grid, kThreads, smem, ctx->stream>>>(rows, rank, ldr, A, Aold, G, u, v, Mk, Nk, (float)reg,
                                                   (float)rate_i, fb1, fomb1, fb2, fomb2, (float)eps, (float)lower,
-                                                  ctx->flags.as<DevFlags>(), code);
+                                                  ctx->flags.as<DevFlags>(), code, stage ? 1 : 0);
     };
     if (rank <= 64) launch(k_factor_update_wide<2>);
     else if (rank <= 128) launch(k_factor_update_wide<4>);
@@ -1197,10 +1204,17 @@ void weight_step_enqueue(Ctx* ctx, const double* partials, int nblk, int rank, i
 
 void hist_penalty_enqueue(Ctx* ctx, int ndim, int rank, const double* Poo, const double* Pon, const double* Pnn,
                           const double* window_s, const double* window_coef, int H, double* out) {
-  const size_t smem = (size_t)rank * rank * 8;
+  const size_t need = (size_t)rank * rank * 8;
+  double* qglobal = nullptr;
+  size_t smem = need;
+  if (need > 200 * 1024) {
+    static thread_local DevBuf qbuf;
+    qglobal = static_cast<double*>(qbuf.ensure(need));
+    smem = 0;
+  }
   if (smem > 48 * 1024)
     OGCP_CUDA(cudaFuncSetAttribute(k_hist_penalty, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_hist_penalty<<<1, 256, smem, ctx->stream>>>(ndim, rank, Poo, Pon, Pnn, window_s, window_coef, H, out);
+  k_hist_penalty<<<1, 256, smem, ctx->stream>>>(ndim, rank, Poo, Pon, Pnn, window_s, window_coef, H, out, qglobal);
   ctx->count();
   check_launch();
 }
