@@ -143,7 +143,9 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * nonzero draws (p >= eta/8) into distinct ordinals with multiplicities before
  * evaluation -- the same merge sampled_gradient_tensor performs
  * (sampling.py:233-237); 0 evaluates every draw separately. */
-enum { OGCP_OPT_MERGE_DRAWS = 1 };
+/* OGCP_OPT_SPLIT_SCATTER (default 1): for merged sets, scatter the largest
+ * random-access mode in a second pass from stored per-sample values. */
+enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2 };
 int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value);
 
 /* Multi-GPU (the reference is single-process): the

@@ -223,3 +223,8 @@ def rng_integers(seed, key, highs, n):
 def set_merge_draws(on: bool):
     """Engine option OGCP_OPT_MERGE_DRAWS for the current device's context."""
     check(lib().ogcp_ctx_set_option(ctx(), 1, int(bool(on))))
+
+
+def set_split_scatter(on: bool):
+    """Engine option OGCP_OPT_SPLIT_SCATTER for the current device's context."""
+    check(lib().ogcp_ctx_set_option(ctx(), 2, int(bool(on))))

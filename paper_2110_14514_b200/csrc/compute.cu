@@ -24,6 +24,13 @@ namespace ogcp {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = 256;
+// minimum resident CTAs per SM for the sample kernels (register budget); tuned on B200
+#ifndef OGCP_SGRAD_MINB
+#define OGCP_SGRAD_MINB 1
+#endif
+#ifndef OGCP_WGRAD_MINB
+#define OGCP_WGRAD_MINB 1
+#endif
 
 template <int D>
 struct ND {
@@ -73,6 +80,7 @@ struct Sample {
   float x;
   float scale;
   float cnt;  // multiplicity of a merged nonzero (1 otherwise)
+  int64_t n;  // index in the sample set
   bool nz;
 };
 
@@ -91,6 +99,7 @@ struct SampleStream {
   const ModelP* M;
   int64_t p, total, stride, b, end;
   int lane, gl, nd;
+  int skip = -1;  // mode whose rows are not gathered (split scatter, pass 2)
   int oB[U];
   float cB[U], cC[U];
   int tC[U][RI];
@@ -187,10 +196,11 @@ struct SampleStream {
           if (k == nd) x = __int_as_float(tC[u][k]);
       }
       s[u].x = s[u].nz ? x : 0.0f;
+      s[u].n = n;
 #pragma unroll
       for (int k = 0; k < NDm; ++k) {
         s[u].idx[k] = tC[u][k < RI ? k : 0];
-        if (k < nd) {
+        if (k < nd && k != skip) {
           const float4* row = reinterpret_cast<const float4*>(M->A[k] + (int64_t)s[u].idx[k] * M->ldr);
 #pragma unroll
           for (int v = 0; v < V; ++v)
@@ -314,9 +324,13 @@ struct PrivP {
 // per-warp ranges; each lane group accumulates its mode-0 contributions in
 // registers while consecutive samples share the mode-0 row and issues one
 // reduction per row segment (sort-by-row segmented reduction for mode 0).
+//
+// split >= 0 (split scatter, pass 1): mode `split` is not scattered here; the
+// sample's y is stored in ybuf[n] for k_sgrad_split.
 template <int D, int G, int V, int U, bool SEG>
-__global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const float* __restrict__ s_f, LossP L,
-                                                    GradPtrs GP, PrivP PV, DevFlags* flags, long long code) {
+__global__ void __launch_bounds__(kThreads, OGCP_SGRAD_MINB) k_sgrad(SamplesP S, ModelP M, const float* __restrict__ s_f, LossP L,
+                                                    GradPtrs GP, PrivP PV, DevFlags* flags, long long code,
+                                                    int split, float* __restrict__ ybuf) {
   extern __shared__ float smem[];
   constexpr int NDm = ND<D>::v;
   const int nd = D > 0 ? D : M.ndim;
@@ -358,6 +372,7 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
         float y = dloss(L.kind, s[u].x, m, L.eps);
         if (S.semi && s[u].nz) y -= dloss(L.kind, 0.0f, m, L.eps);  // semi-stratified nonzero stratum
         y *= s[u].scale;
+        if (split >= 0 && gl == 0) ybuf[s[u].n] = y;
         if (seg0 && s[u].idx[0] != seg_row) {
           if (seg_row >= 0) {
 #pragma unroll
@@ -370,6 +385,7 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
 #pragma unroll
         for (int k = 0; k < NDm; ++k) {
           if (k >= nd) break;
+          if (k == split) continue;
 #pragma unroll
           for (int v = 0; v < V; ++v) {
             float4 c = make_float4(y * s4[v].x, y * s4[v].y, y * s4[v].z, y * s4[v].w);
@@ -414,9 +430,47 @@ __global__ void __launch_bounds__(kThreads) k_sgrad(SamplesP S, ModelP M, const 
   }
 }
 
+// Split scatter, pass 2: the contributions of mode `split` from the stored y,
+// without that mode's row gathers; run separately so the 16-byte reductions
+// into G_split meet an L2 that holds G_split instead of the gathered rows.
+template <int D, int G, int V, int U>
+__global__ void __launch_bounds__(kThreads) k_sgrad_split(SamplesP S, ModelP M, const float* __restrict__ s_f,
+                                                          const float* __restrict__ ybuf, float* __restrict__ Gs,
+                                                          int split) {
+  constexpr int NDm = ND<D>::v;
+  const int nd = D > 0 ? D : M.ndim;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  float4 s4[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) s4[v] = __ldg(reinterpret_cast<const float4*>(s_f) + v * G + gl);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  SampleStream<D, G, V, U> stream;
+  stream.skip = split;
+  stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr);
+  Sample<D, V> s[U];
+  bool valid[U];
+  while (stream.next(s, valid)) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!valid[u]) continue;
+      const float y = __ldg(ybuf + s[u].n);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        float4 c = make_float4(y * s4[v].x, y * s4[v].y, y * s4[v].z, y * s4[v].w);
+#pragma unroll
+        for (int j = 0; j < NDm; ++j)
+          if (j != split && j < nd) c = mul4(c, s[u].a[j][v]);
+        red_add_v4(Gs + (int64_t)s[u].idx[split] * M.ldr + (v * G + gl) * 4, c);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K2 (weights)
 template <int D, int G, int V, int U>
-__global__ void __launch_bounds__(kThreads) k_wgrad(SamplesP S, ModelP M, const float* __restrict__ s_f, LossP L,
+__global__ void __launch_bounds__(kThreads, OGCP_WGRAD_MINB) k_wgrad(SamplesP S, ModelP M, const float* __restrict__ s_f, LossP L,
                                                     double* __restrict__ partials, DevFlags* flags, long long code) {
   __shared__ double red[kThreads / 32][4 * V * G];
   constexpr int NDm = ND<D>::v;
@@ -1017,6 +1071,22 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
     }
   }
   const size_t smem = (size_t)used * 4;
+  // Split scatter for merged sets whose largest random-access gradient (a mode
+  // other than the segmented mode 0) is too big to share L2 with the gathers.
+  int split = -1;
+  if (S.cnt && ctx->split_scatter) {
+    int64_t best = 0;
+    for (int k = 1; k < M.ndim; ++k) {
+      bool priv = false;
+      for (int j = 0; j < PV.nmodes; ++j) priv = priv || PV.mode[j] == k;
+      const int64_t bytes = M.dims[k] * M.ldr * 4;
+      if (!priv && bytes >= (int64_t)32 << 20 && bytes > best) {
+        best = bytes;
+        split = k;
+      }
+    }
+  }
+  float* ybuf = split >= 0 ? static_cast<float*>(ctx->ybuf.ensure((size_t)total * 4)) : nullptr;
   ProfScope prof_scope(ctx, kProfSgrad);
   dispatch_layout(Layout::Scatter, M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc, auto Uc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
@@ -1025,10 +1095,17 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
       if (smem > 48 * 1024)
         OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const int grid = sample_grid(kern, smem, total, G, U);
-      kern<<<grid, kThreads, smem, ctx->stream>>>(S, M, s_f, L, GP, PV, ctx->flags.as<DevFlags>(), code);
+      kern<<<grid, kThreads, smem, ctx->stream>>>(S, M, s_f, L, GP, PV, ctx->flags.as<DevFlags>(), code, split,
+                                                  ybuf);
     };
     if (S.cnt) launch(k_sgrad<D, G, V, U, true>);
     else launch(k_sgrad<D, G, V, U, false>);
+    if (split >= 0) {
+      auto kern2 = k_sgrad_split<D, G, V, U>;
+      const int grid2 = sample_grid(kern2, 0, total, G, U);
+      kern2<<<grid2, kThreads, 0, ctx->stream>>>(S, M, s_f, ybuf, GP.g[split], split);
+      ctx->count();
+    }
   });
   ctx->count();
   check_launch();

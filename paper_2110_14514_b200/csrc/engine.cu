@@ -840,6 +840,7 @@ int ogcp_ctx_init_comm(ogcp_ctx* ctx, const uint8_t id[128], int32_t rank, int32
 int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   OGCP_API_BEGIN
   if (option == OGCP_OPT_MERGE_DRAWS) ctx->merge_draws = value != 0;
+  else if (option == OGCP_OPT_SPLIT_SCATTER) ctx->split_scatter = value != 0;
   else throw Error(OGCP_E_USAGE, "unknown option");
   OGCP_API_END
 }
