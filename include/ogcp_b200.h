@@ -263,6 +263,17 @@ int ogcp_solve_factors(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_con
                        const int64_t* window_ids, int32_t H, ogcp_adam_state* adam,
                        int64_t* iteration, ogcp_trace* trace);
 
+/* solve_static (solvers.py:371-493, sampled mode, one restart): joint GCP-SGD
+ * over the weights and every factor of a (d+1)-way block, keyed (seed,
+ * seed_key, PHASE_STATIC_*).  m->factors (device, updated in place) hold the
+ * initial factors, weights (host [rank], in/out) the initial weights; adam
+ * holds zeroed factor moments and the rate (decayed on rejections).  The
+ * epoch loop runs max_epochs x iters at tolerance tol. */
+int ogcp_solve_static(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_config* cfg,
+                      const ogcp_loss* loss, int64_t seed_key, const ogcp_model* m, double* weights,
+                      ogcp_adam_state* adam, int32_t max_epochs, int32_t iters, double tol,
+                      ogcp_trace* trace);
+
 /* local_loss (metrics.py:36-70): mode 0 exact (every cell, <= max_elements),
  * mode 1 sampled on rng_at(seed, *key) with (p, q) (p < 0: all nonzeros).
  * Returns the loss total divided by ||X||^2 when that is > 0; *normalized says which. */

@@ -117,6 +117,9 @@ _SIGS = {
     "ogcp_solve_factors": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SolverC), C.POINTER(LossC), C.c_int64,
                                      C.POINTER(ModelC), C.POINTER(C.c_void_p), c_f64p, c_f64p, c_i64p, C.c_int32,
                                      C.POINTER(AdamC), c_i64p, C.POINTER(TraceC)]),
+    "ogcp_solve_static": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SolverC), C.POINTER(LossC), C.c_int64,
+                                    C.POINTER(ModelC), c_f64p, C.POINTER(AdamC), C.c_int32, C.c_int32, C.c_double,
+                                    C.POINTER(TraceC)]),
     "ogcp_local_loss": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(ModelC), c_f64p, C.POINTER(LossC), C.c_int32,
                                   C.c_int64, C.c_int64, C.c_uint64, c_i64p, C.c_int32, C.c_int64, C.c_int64, c_f64p,
                                   C.POINTER(C.c_int32)]),

@@ -475,7 +475,8 @@ __global__ void k_trace_sum(int ndim, int R, const double* __restrict__ P, doubl
 // F(factors) = data term on the fixed objective set + (w/2) history + (lambda/2) sum ||A||^2
 static double factor_objective(Ctx* ctx, const Slice* X, const SamplesP& So, const ModelP& M, const float* s_f,
                                const LossP& L, float* const* old_factors, int H, const ogcp_solver_config* cfg,
-                               HistBufs& hb, long long code, int64_t budget, int64_t t) {
+                               HistBufs& hb, long long code, int64_t budget, int64_t t,
+                               const char* what = "factor solve") {
   cudaStream_t st = ctx->stream;
   const int RR = M.rank * M.rank;
   double* part = ctx->partials.as<double>();
@@ -505,7 +506,7 @@ static double factor_objective(Ctx* ctx, const Slice* X, const SamplesP& So, con
   if (collective) comm_sync_flags(ctx);
   fetch_flags(ctx);
   OGCP_CUDA(cudaStreamSynchronize(st));
-  check_flags(ctx, X, L.kind, budget, "factor solve", t);
+  check_flags(ctx, X, L.kind, budget, what, t);
   double val = hsc[0];
   if (hist) val += 0.5 * cfg->hist_weight * hsc[1];
   if (reg) val += 0.5 * cfg->reg_factors * hsc[2];
@@ -667,6 +668,160 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   if (trace) {
     trace->n_objective = 0;
     for (size_t j = 0; j < objv.size() && (int)j <= cfg->max_epochs_factors; ++j)
+      trace->objective[trace->n_objective++] = objv[j];
+    trace->epochs = epochs;
+    trace->rejections = rejections;
+  }
+}
+
+// ============================================================== solve_static
+// Static GCP-SGD over weights and every factor jointly (solvers.py:371-493):
+// one draw per iteration feeds both the factor scatter (K3) and the weight
+// MTTKRP (K3w); the weights keep the fp64 temporal-row Adam, the factors the
+// fp32 row Adam, both on one step counter and one (decaying) rate.
+static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config* cfg, const ogcp_loss* loss,
+                              int64_t seed_key, const ogcp_model* mdl, double* weights, ogcp_adam_state* ad,
+                              int32_t max_epochs, int32_t iters, double tol, ogcp_trace* trace) {
+  ModelP M = model_of(mdl);
+  check_model_slice(M, X);
+  LossP L = loss_of(loss);
+  const int R = M.rank, ldr = M.ldr;
+  cudaStream_t st = ctx->stream;
+  const uint64_t seed = cfg->samples.seed;
+  FactorWork& W = factor_work();
+  float* const* A = mdl->factors;
+  // weight state: s u v s_o u_o v_o (double ldr each) + s_f float ldr; u = v = 0
+  ctx->wsolve.ensure((size_t)ldr * (6 * 8 + 4));
+  double* ws = ctx->wsolve.as<double>();
+  float* s_f = reinterpret_cast<float*>(ws + 6 * ldr);
+  {
+    std::vector<double> h(6 * ldr, 0.0);
+    for (int r = 0; r < R; ++r) h[r] = h[3 * ldr + r] = weights[r];
+    OGCP_CUDA(cudaMemcpyAsync(ws, h.data(), 6 * ldr * 8, cudaMemcpyHostToDevice, st));
+    upload_weights(ctx, weights, R, ldr, s_f);
+  }
+  ctx->partials.ensure((size_t)kNumSMs * 8 * ldr * 8 + 64);
+  ctx->scalars.ensure(64 * 8 + ldr * 8);
+  double* part = ctx->partials.as<double>();
+  double* gsum = ctx->scalars.as<double>() + 64;
+  double* hsc = ctx->host_scalars;
+  size_t gtot = 0;
+  for (int k = 0; k < M.ndim; ++k) gtot += (size_t)M.dims[k] * ldr;
+  W.grads.ensure(gtot * 4);
+  hist_alloc(W.hb, M.ndim, R);
+  adam_epoch(ctx, M, A, ad, true);  // adam.update(variables, True) at entry
+
+  int64_t po, qo, p, q;
+  resolve_counts(cfg->samples.obj_nonzeros, cfg->samples.obj_zeros, X, &po, &qo);
+  resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
+  if (po > 0 || p > 0) x_domain_check(X, L.kind);
+  const bool semi = cfg->samples.semi_stratified != 0;
+  draw_sync(ctx, X, keyed(seed, {seed_key, 8}), po, qo, cfg->samples.max_rejects, W.obj, semi);
+  SamplesP So = sharded(ctx, W.obj.sample_set(X));
+  precheck_draw(X, p, semi ? 0 : q);
+  W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+  W.grad.semi = semi;
+  const int64_t budget = budget_of(q, cfg->samples.max_rejects);
+  const char* what = "static solve";
+
+  long long ev = 1;
+  auto fest_fn = [&]() -> double {
+    double v = factor_objective(ctx, X, So, M, s_f, L, nullptr, 0, cfg, W.hb, code_of(ev++, 1), budget, seed_key,
+                                what);
+    if (cfg->reg_weights) {
+      OGCP_CUDA(cudaMemcpyAsync(hsc + 8, ws, R * 8, cudaMemcpyDeviceToHost, st));
+      OGCP_CUDA(cudaStreamSynchronize(st));
+      double ss = 0.0;
+      for (int r = 0; r < R; ++r) ss += hsc[8 + r] * hsc[8 + r];
+      v += 0.5 * cfg->reg_weights * ss;
+    }
+    return v;
+  };
+  auto weights_epoch = [&](bool passed) {
+    if (passed) OGCP_CUDA(cudaMemcpyAsync(ws + 3 * ldr, ws, 3 * ldr * 8, cudaMemcpyDeviceToDevice, st));
+    else OGCP_CUDA(cudaMemcpyAsync(ws, ws + 3 * ldr, 3 * ldr * 8, cudaMemcpyDeviceToDevice, st));
+    OGCP_CUDA(cudaMemcpyAsync(hsc, ws, ldr * 8, cudaMemcpyDeviceToHost, st));
+    OGCP_CUDA(cudaStreamSynchronize(st));
+    upload_weights(ctx, hsc, R, ldr, s_f);
+  };
+
+  double fest = fest_fn();
+  std::vector<double> objv{fest};
+  int64_t iter = 0;
+  int epochs = 0, rejections = 0;
+  float* gp[kMaxModes];
+  {
+    size_t off = 0;
+    for (int k = 0; k < M.ndim; ++k) {
+      gp[k] = W.grads.as<float>() + off;
+      off += (size_t)M.dims[k] * ldr;
+    }
+  }
+  for (int epoch = 0; epoch < max_epochs; ++epoch) {
+    if (!(fest > tol)) break;
+    const double fold = fest;
+    for (int attempt = 0;; ++attempt) {
+      reset_flags(ctx);
+      const long long ev0 = ev;
+      for (int it = 0; it < iters; ++it) {
+        const long long e = ev++;
+        const int64_t cnt = iter + it + 1;
+        const double rate_i = ad->rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
+                              (1.0 - std::pow(cfg->beta1, (double)cnt));
+        SamplesP Sg = sharded(ctx, W.grad.draw(ctx, X, keyed(seed, {seed_key, 7, epoch, it}), budget, code_of(e, 0)));
+        // both gradients at the current iterate, before either update
+        sgrad_enqueue(ctx, Sg, M, s_f, L, gp, code_of(e, 1));
+        int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1));
+        comm_allreduce_sum(ctx, W.grads.as<float>(), gtot);
+        const double* gparts = part;
+        if (ctx->world > 1) {
+          sum_partials_enqueue(ctx, part, nb, ldr, gsum);
+          comm_allreduce_sum(ctx, gsum, (size_t)ldr);
+          gparts = gsum;
+          nb = 1;
+        }
+        weight_step_enqueue(ctx, gparts, nb, R, ldr, ws, s_f, cfg->reg_weights, rate_i, cfg->beta1, cfg->beta2,
+                            cfg->adam_eps, cfg->lower_bound, code_of(e, 2));
+        for (int k = 0; k < M.ndim; ++k)
+          factor_update_enqueue(ctx, M.dims[k], R, ldr, A[k], nullptr, gp[k], ad->u[k], ad->v[k], nullptr, nullptr,
+                                cfg->reg_factors, rate_i, cfg->beta1, cfg->beta2, cfg->adam_eps, cfg->lower_bound,
+                                code_of(e, 2));
+      }
+      comm_sync_flags(ctx);
+      fetch_flags(ctx);
+      OGCP_CUDA(cudaStreamSynchronize(st));
+      int r = check_flags(ctx, X, L.kind, budget, what, seed_key);
+      if (r == 0) break;
+      if (r == 2) W.grad.size(p, q, X->ndim, false);
+      else ctx->slack *= 4.0;
+      adam_epoch(ctx, M, A, ad, false);
+      weights_epoch(false);
+      ev = ev0;
+      if (attempt > 8) throw Error(OGCP_E_INTERNAL, "sampler could not provision enough candidates");
+    }
+    iter += iters;
+    fest = fest_fn();
+    if (!std::isfinite(fest)) throw Error(OGCP_E_DIVERGENCE, "static solve diverged");
+    if (fest > fold) {
+      adam_epoch(ctx, M, A, ad, false);
+      weights_epoch(false);
+      ad->rate *= cfg->rate_decay;
+      fest = fold;
+      iter -= iters;
+      ++rejections;
+    } else {
+      adam_epoch(ctx, M, A, ad, true);
+      weights_epoch(true);
+    }
+    ++epochs;
+    objv.push_back(fest);
+  }
+  OGCP_CUDA(cudaMemcpyAsync(hsc, ws, ldr * 8, cudaMemcpyDeviceToHost, st));
+  OGCP_CUDA(cudaStreamSynchronize(st));
+  for (int r = 0; r < R; ++r) weights[r] = hsc[r];
+  if (trace) {
+    trace->n_objective = 0;
+    for (size_t j = 0; j < objv.size() && (int)j <= max_epochs; ++j)
       trace->objective[trace->n_objective++] = objv[j];
     trace->epochs = epochs;
     trace->rejections = rejections;
@@ -1099,6 +1254,15 @@ int ogcp_solve_factors(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_con
                        int64_t* iteration, ogcp_trace* trace) {
   OGCP_API_BEGIN
   solve_factors_impl(ctx, s, cfg, loss, t, m, old_factors, weights, window_s, window_ids, H, adam, iteration, trace);
+  OGCP_API_END
+}
+
+int ogcp_solve_static(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_config* cfg, const ogcp_loss* loss,
+                      int64_t seed_key, const ogcp_model* m, double* weights, ogcp_adam_state* adam,
+                      int32_t max_epochs, int32_t iters, double tol, ogcp_trace* trace) {
+  OGCP_API_BEGIN
+  if (max_epochs < 0 || iters < 1) throw Error(OGCP_E_USAGE, "epoch and iteration counts must be >= 1");
+  solve_static_impl(ctx, s, cfg, loss, seed_key, m, weights, adam, max_epochs, iters, tol, trace);
   OGCP_API_END
 }
 

@@ -20,7 +20,7 @@ from .adam import Adam
 from .exceptions import DataError
 from .losses import LossFunction
 from .sampling import SamplerConfig, _window_arrays
-from .tensor import DeviceModel, SparseTensor
+from .tensor import DeviceModel, KTensor, SparseTensor
 
 TEMPORAL_SOLVERS = ("sgd", "least-squares")
 GRADIENT_MODES = ("sampled", "dense-gaussian")
@@ -203,3 +203,74 @@ def factor_gradients(Y: SparseTensor, factors: Sequence[np.ndarray], weights: np
         ws.ctypes.data_as(_lib.c_f64p), ids.ctypes.data_as(_lib.c_i64p), len(window), float(hist_weight),
         float(hist_decay), int(t), float(reg_factors), C.cast(gp, C.POINTER(C.c_void_p))))
     return grads.to_numpy()
+
+
+@dataclass
+class StaticSolve:
+    model: KTensor
+    trace: EpochTrace
+
+
+def _host_generator(seed: int, *key: int) -> np.random.Generator:
+    """Host numpy stream for initial values, rng_at(seed, *key) (sampling.py:39-42)."""
+    return np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=tuple(int(k) for k in key)))
+
+
+def solve_static_device(X: SparseTensor, model: DeviceModel, weights: np.ndarray, loss: LossFunction,
+                        cfg: SolverConfig, *, max_epochs: int, iters: int, rate: float, tol: float,
+                        seed_key: int = 0):
+    """Static fit updating ``model`` in place on the device; returns (weights, trace)."""
+    _check_gradient_mode(cfg, loss)
+    w = np.ascontiguousarray(np.array(weights, dtype=np.float64))
+    if w.shape != (model.rank,):
+        raise DataError("weights must match the model rank")
+    adam = cfg.make_adam(rate, loss)
+    adam.init_device(model.dims, model.rank)
+    st = adam.c()
+    tr = _Trace(max_epochs)
+    _lib.check(_lib.lib().ogcp_solve_static(
+        _lib.ctx(), X._handle, C.byref(cfg._c(loss)), C.byref(loss._c()), int(seed_key), C.byref(model.c()),
+        w.ctypes.data_as(_lib.c_f64p), C.byref(st), int(max_epochs), int(iters), float(tol), C.byref(tr.c)))
+    return w, tr.result()
+
+
+def solve_static(X: SparseTensor, rank: int, loss: LossFunction, cfg: SolverConfig, init: Optional[KTensor] = None,
+                 *, max_epochs: Optional[int] = None, iters_per_epoch: Optional[int] = None,
+                 rate: Optional[float] = None, tol: Optional[float] = None, restarts: int = 1,
+                 seed_key: int = 0) -> StaticSolve:
+    """Static GCP-SGD fit of weights and all factor matrices jointly (solvers.py:371-493).
+
+    Initialization is uniform(0, 1) keyed (seed, seed_key, PHASE_INIT) unless
+    given; with ``restarts`` > 1 the candidate with the lowest objective on the
+    shared (seed, seed_key, PHASE_RESTART_EVAL) sample set is returned."""
+    from .sampling import PHASE_INIT, PHASE_RESTART_EVAL, draw_samples, estimate_objective, rng_at
+    if restarts > 1:
+        if init is not None:
+            raise DataError("restarts > 1 and an explicit init conflict")
+        cands = [solve_static(X, rank, loss, cfg, max_epochs=max_epochs, iters_per_epoch=iters_per_epoch,
+                              rate=rate, tol=tol, seed_key=seed_key + r) for r in range(restarts)]
+        if cfg.gradient_mode == "dense-gaussian":
+            raise DataError("gradient_mode 'dense-gaussian' is not implemented by the GPU engine yet")
+        p_eval, q_eval = cfg.samples.objective_counts(X)
+        ev = draw_samples(X, p_eval, q_eval, rng_at(cfg.samples.seed, seed_key, PHASE_RESTART_EVAL),
+                          cfg.samples.max_rejects)
+        scores = [estimate_objective(X, c.model.factors, c.model.weights, loss, ev, reg_factors=cfg.reg_factors,
+                                     reg_weights=cfg.reg_weights) for c in cands]
+        return cands[int(np.argmin(scores))]
+    _check_gradient_mode(cfg, loss)
+    max_epochs = cfg.max_epochs_factors if max_epochs is None else max_epochs
+    iters = cfg.iters_factors if iters_per_epoch is None else iters_per_epoch
+    rate = cfg.rate_factors if rate is None else rate
+    tol = cfg.tol_factors if tol is None else tol
+    if init is None:
+        g0 = _host_generator(cfg.samples.seed, seed_key, PHASE_INIT)
+        factors = [g0.uniform(size=(d, rank)) for d in X.dims]
+        weights = g0.uniform(size=rank)
+    else:
+        if init.dims != X.dims or init.rank != rank:
+            raise DataError("init model does not match tensor dims/rank")
+        factors, weights = list(init.factors), np.array(init.weights)
+    model = DeviceModel.from_numpy(factors)
+    w, trace = solve_static_device(X, model, weights, loss, cfg, max_epochs=max_epochs, iters=iters, rate=rate,
+                                   tol=tol, seed_key=seed_key)
+    return StaticSolve(KTensor(w, model.to_numpy()), trace)

@@ -183,8 +183,62 @@ def main():
             streams[f"{name}_{k}"] = v
     streams["names"] = np.array(json.dumps([c[0] for c in scases]))
     np.savez_compressed(os.path.join(OUT, "streams.npz"), **streams)
+    make_static()
     print("golden fixtures written to", os.path.abspath(OUT))
 
 
+def make_static():
+    """solve_static / warm_start fixtures (solvers.py:371-493, streaming.py:113-151)."""
+    sys.path.insert(0, REF)
+    import ogcp
+    from ogcp import sampling, solvers, streaming
+
+    static = {}
+    cases = [
+        # name, kind, dims (last = time), R, density, cfg kwargs, restarts, capacity
+        ("gauss", "gaussian", (6, 5, 4, 3), 3, None,
+         dict(max_epochs_factors=3, iters_factors=20, rate_factors=1e-2, reg_factors=0.01, reg_weights=0.02,
+              samples=sampling.SamplerConfig(200, 0, 300, 0, seed=3)), 1, 2),
+        ("pois", "poisson", (8, 9, 5, 4), 3, 0.2,
+         dict(max_epochs_factors=2, iters_factors=15, rate_factors=1e-2,
+              samples=sampling.SamplerConfig(None, 60, None, 200, seed=7)), 2, 3),
+        ("bern", "bernoulli", (7, 6, 8, 3), 2, 0.15,
+         dict(max_epochs_factors=3, iters_factors=10, rate_factors=5e-2, rate_decay=0.5,
+              samples=sampling.SamplerConfig(30, 40, 60, 80, seed=5)), 1, 2),
+    ]
+    for name, kind, dims, R, dens, kw, restarts, cap in cases:
+        if kind == "gaussian":
+            X, _ = ogcp.gen_gaussian(ogcp.SyntheticSpec("gaussian", dims=dims, rank=R, noise=0.1, seed=11))
+        else:
+            X, _ = ogcp.gen_poisson(ogcp.SyntheticSpec("poisson", dims=dims, rank=R, density=dens, seed=11))
+            if kind == "bernoulli":
+                X = ogcp.SparseTensor.from_zero_based(X.dims, X.subs0, np.ones(X.nnz))
+        loss = ogcp.make_loss(kind)
+        cfg = solvers.SolverConfig(**kw)
+        res = solvers.solve_static(X, R, loss, cfg, seed_key=4)
+        state = streaming.warm_start(X, R, loss, cfg, cap, restarts=restarts)
+        rec = dict(kind=np.array(kind), dims=np.array(dims), subs0=X.subs0, vals=X.vals, R=np.array(R),
+                   restarts=np.array(restarts), capacity=np.array(cap),
+                   cfg=np.array(json.dumps({k: v for k, v in kw.items() if k != "samples"})),
+                   samples=np.array(json.dumps(dict(p=kw["samples"].grad_nonzeros, q=kw["samples"].grad_zeros,
+                                                    p_obj=kw["samples"].obj_nonzeros,
+                                                    q_obj=kw["samples"].obj_zeros, seed=kw["samples"].seed))),
+                   static_weights=res.model.weights, static_trace=np.array(res.trace.objective),
+                   static_epochs=np.array(res.trace.epochs), static_rejections=np.array(res.trace.rejections),
+                   warm_weights_log=np.vstack(state.weights_log), warm_window_ids=np.array(state.window.step_ids()),
+                   warm_t=np.array(state.t))
+        for k, a in enumerate(res.model.factors):
+            rec[f"static_A{k}"] = a
+        for k, a in enumerate(state.factors):
+            rec[f"warm_A{k}"] = a
+        for k, v in rec.items():
+            static[f"{name}_{k}"] = v
+    static["names"] = np.array(json.dumps([c[0] for c in cases]))
+    np.savez_compressed(os.path.join(OUT, "static.npz"), **static)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["static"]:
+        make_static()
+    else:
+        main()

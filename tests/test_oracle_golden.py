@@ -117,3 +117,33 @@ def test_stream_matches_reference(golden_dir, name):
     ftr = json.loads(str(c("ftrace")))
     for (_, _, f), ref in zip(st.traces, ftr):
         np.testing.assert_allclose(f, ref, rtol=1e-9)
+
+
+def static_case(g, name):
+    c = lambda k: g[f"{name}_{k}"]
+    kw = json.loads(str(c("cfg")))
+    sm = json.loads(str(c("samples")))
+    cfg = O.Cfg(kappa_f=kw["max_epochs_factors"], tau_f=kw["iters_factors"], rate_f=kw["rate_factors"],
+                reg_factors=kw.get("reg_factors", 0.0), reg_weights=kw.get("reg_weights", 0.0),
+                rate_decay=kw.get("rate_decay", 0.1), p=sm["p"], q=sm["q"], p_obj=sm["p_obj"],
+                q_obj=sm["q_obj"], seed=sm["seed"])
+    X = O.Slice(tuple(int(d) for d in c("dims")), c("subs0"), c("vals"))
+    return c, str(c("kind")), int(c("R")), cfg, X
+
+
+@pytest.mark.parametrize("name", ["gauss", "pois", "bern"])
+def test_static_and_warm_start_match_reference(golden_dir, name):
+    g = load(golden_dir, "static.npz")
+    c, kind, R, cfg, X = static_case(g, name)
+    w, fs, trace, epochs, rej = O.static_solve(X, R, kind, cfg, seed_key=4)
+    np.testing.assert_allclose(w, c("static_weights"), rtol=1e-9, atol=1e-12)
+    for k, a in enumerate(fs):
+        np.testing.assert_allclose(a, c(f"static_A{k}"), rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(trace, c("static_trace"), rtol=1e-9)
+    assert (epochs, rej) == (int(c("static_epochs")), int(c("static_rejections")))
+    st = O.warm_start(X, R, kind, cfg, int(c("capacity")), restarts=int(c("restarts")))
+    for k, a in enumerate(st.factors):
+        np.testing.assert_allclose(a, c(f"warm_A{k}"), rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(np.vstack(st.weights_log), c("warm_weights_log"), rtol=1e-9, atol=1e-12)
+    assert [h for h, _ in st.window] == c("warm_window_ids").tolist()
+    assert st.t == int(c("warm_t"))
