@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define OGCP_ABI_VERSION 1
+#define OGCP_ABI_VERSION 2
 
 enum {
   OGCP_OK = 0,
@@ -67,7 +67,7 @@ typedef struct {
   int32_t semi_stratified;
 } ogcp_sampler_config;
 
-/* solvers.py:40-69 SolverConfig (gradient_mode "sampled", temporal_solver "sgd");
+/* solvers.py:40-69 SolverConfig;
  * lower_bound is already resolved against the loss (solvers.py:86-87). */
 typedef struct {
   double tol_weights, tol_factors;
@@ -78,6 +78,8 @@ typedef struct {
   double rate_weights, rate_factors, beta1, beta2, adam_eps, rate_decay;
   double lower_bound;
   ogcp_sampler_config samples;
+  int32_t gradient_mode;    /* 0 "sampled", 1 "dense-gaussian" (solvers.py:35, 145-185) */
+  int32_t temporal_solver;  /* 0 "sgd", 1 "least-squares" (solvers.py:34, 271-288; streaming.py:168-176) */
 } ogcp_solver_config;
 
 /* A CP model bound to caller-owned device buffers.  factors[k] is a row-major
@@ -273,6 +275,27 @@ int ogcp_solve_static(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_conf
                       const ogcp_loss* loss, int64_t seed_key, const ogcp_model* m, double* weights,
                       ogcp_adam_state* adam, int32_t max_epochs, int32_t iters, double tol,
                       ogcp_trace* trace);
+
+/* ------------------------------------------------ Gaussian special cases */
+/* solve_weights_least_squares (solvers.py:271-288): (hadamard_k Gram_k + mu I) s
+ * = Z' vec(X) over the stored entries; s_out host [rank].  An exactly singular
+ * system is OGCP_E_DATA. */
+int ogcp_solve_weights_ls(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m, double reg_weights,
+                          double* s_out);
+
+/* gaussian_sum_sq_residual (kernels.py:135-146): sum over every cell of (x - m)^2
+ * = ||X||^2 - 2 <X, M> + ||M||^2.  weights host [rank]. */
+int ogcp_gaussian_residual(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m, const double* weights,
+                           double* out);
+
+/* dense_gaussian_factor_gradients (solvers.py:145-156) into grads_dev (nullable,
+ * device, model layout) and _dense_gaussian_weight_gradient (solvers.py:182-185)
+ * into weight_grad (nullable, host [rank]). */
+int ogcp_dense_gaussian_gradients(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m,
+                                  float* const* old_factors, const double* weights, const double* window_s,
+                                  const int64_t* window_ids, int32_t H, double hist_weight, double hist_decay,
+                                  int64_t t, double reg_factors, double reg_weights, float* const* grads_dev,
+                                  double* weight_grad);
 
 /* local_loss (metrics.py:36-70): mode 0 exact (every cell, <= max_elements),
  * mode 1 sampled on rng_at(seed, *key) with (p, q) (p < 0: all nonzeros).

@@ -44,7 +44,8 @@ class SolverC(C.Structure):
                 ("hist_decay", C.c_double), ("warm_start_weights", C.c_int32),
                 ("rate_weights", C.c_double), ("rate_factors", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("adam_eps", C.c_double), ("rate_decay", C.c_double),
-                ("lower_bound", C.c_double), ("samples", SamplerC)]
+                ("lower_bound", C.c_double), ("samples", SamplerC), ("gradient_mode", C.c_int32),
+                ("temporal_solver", C.c_int32)]
 
 
 class ModelC(C.Structure):
@@ -120,6 +121,11 @@ _SIGS = {
     "ogcp_solve_static": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(SolverC), C.POINTER(LossC), C.c_int64,
                                     C.POINTER(ModelC), c_f64p, C.POINTER(AdamC), C.c_int32, C.c_int32, C.c_double,
                                     C.POINTER(TraceC)]),
+    "ogcp_solve_weights_ls": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(ModelC), C.c_double, c_f64p]),
+    "ogcp_gaussian_residual": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(ModelC), c_f64p, c_f64p]),
+    "ogcp_dense_gaussian_gradients": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(ModelC), C.POINTER(C.c_void_p),
+                                                c_f64p, c_f64p, c_i64p, C.c_int32, C.c_double, C.c_double,
+                                                C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_void_p), c_f64p]),
     "ogcp_local_loss": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(ModelC), c_f64p, C.POINTER(LossC), C.c_int32,
                                   C.c_int64, C.c_int64, C.c_uint64, c_i64p, C.c_int32, C.c_int64, C.c_int64, c_f64p,
                                   C.POINTER(C.c_int32)]),

@@ -157,6 +157,9 @@ struct Ctx {
   DevBuf grad_ord, grad_zero;   // gradient sample set
   DevBuf obj_ord, obj_zero;     // objective sample set
   DevBuf window;                // window matrix / vectors
+  DevBuf iota;                  // 0..iota_n-1 ordinals: "every stored nonzero once" sample sets
+  int64_t iota_n = 0;
+  DevBuf dense;                 // dense-Gaussian terms: b[ldr], s[ldr] (double)
   DevBuf pinned_dummy;
   double* host_scalars = nullptr;  // pinned host mirror
   DevFlags* host_flags = nullptr;  // pinned

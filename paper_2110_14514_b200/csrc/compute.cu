@@ -55,7 +55,9 @@ __device__ __forceinline__ float dloss(int kind, float x, float m, float eps) {
   return 1.0f / (m + 1.0f) - x / (m + eps);
 }
 // f (losses.py:58-67) in fp64.
+// IDENTITY gives the cross term x*m of the exact Gaussian residual (kernels.py:143).
 __device__ __forceinline__ double floss(int kind, double x, double m, double eps) {
+  if (kind == OGCP_IDENTITY) return x * m;
   if (kind == OGCP_GAUSSIAN) return (x - m) * (x - m);
   if (kind == OGCP_POISSON) return m - x * log(m + eps);
   return log(m + 1.0) - x * log(m + eps);
@@ -751,22 +753,47 @@ __global__ void k_gram_finalize(const double* __restrict__ partials, int nblk, i
 }
 
 // ------------------------------------------------------------------ history coefficients
+// Mk = Gamma_k o (w S + extra s s'), Nk = Gamma^_k o (w S): the history term
+// (solvers.py:159-179) plus, for the dense-Gaussian gradient, its model term
+// 2 A_k (Gamma_k o s s') (kernels.py:117-132).  C / S / s may be null.
 __global__ void k_hist_coeffs(int ndim, int rank, const double* __restrict__ P, const double* __restrict__ C,
-                              const double* __restrict__ S, double w, float* __restrict__ Mk,
-                              float* __restrict__ Nk) {
+                              const double* __restrict__ S, double w, const double* __restrict__ s, double extra,
+                              float* __restrict__ Mk, float* __restrict__ Nk) {
   const int RR = rank * rank;
   for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+    const double se = S ? w * S[e] : 0.0;
+    const double me = se + (s ? extra * s[e / rank] * s[e % rank] : 0.0);
     for (int k = 0; k < ndim; ++k) {
       double gp = 1.0, gc = 1.0;
       for (int m = 0; m < ndim; ++m) {
         if (m == k) continue;
         gp *= P[(int64_t)m * RR + e];
-        gc *= C[(int64_t)m * RR + e];
+        if (C) gc *= C[(int64_t)m * RR + e];
       }
-      Mk[(int64_t)k * RR + e] = (float)(w * gp * S[e]);
-      Nk[(int64_t)k * RR + e] = (float)(w * gc * S[e]);
+      Mk[(int64_t)k * RR + e] = (float)(gp * me);
+      Nk[(int64_t)k * RR + e] = C ? (float)(gc * se) : 0.f;
     }
   }
+}
+
+// Dense-Gaussian weight gradient without the mu term (solvers.py:182-185):
+// out[r] = 2 ((hadamard_m P_m) s - b)[r]; weight_step adds mu s.
+__global__ void k_dense_wgrad(int ndim, int rank, int ldr, const double* __restrict__ P,
+                              const double* __restrict__ b, const double* __restrict__ s, double* __restrict__ out) {
+  const int r = threadIdx.x;
+  if (r >= ldr) return;
+  if (r >= rank) {
+    out[r] = 0.0;
+    return;
+  }
+  const int RR = rank * rank;
+  double acc = 0.0;
+  for (int j = 0; j < rank; ++j) {
+    double g = 1.0;
+    for (int m = 0; m < ndim; ++m) g *= P[(int64_t)m * RR + r * rank + j];
+    acc += g * s[j];
+  }
+  out[r] = 2.0 * (acc - b[r]);
 }
 
 // ------------------------------------------------------------------ K5
@@ -799,6 +826,7 @@ __global__ void __launch_bounds__(kThreads) k_factor_update(int64_t rows, int ra
                                                             float lower, DevFlags* flags, long long code) {
   constexpr int RPI = 2;
   const bool hist = Mk != nullptr;
+  const bool has_old = hist && Aold != nullptr;  // dense-Gaussian model term without history
   const int lane = threadIdx.x & 31;
   const int c = lane & (GR - 1);
   const bool col_on = c < rank;
@@ -822,7 +850,7 @@ __global__ void __launch_bounds__(kThreads) k_factor_update(int64_t rows, int ra
       ok[q] = i < rows && col_on;
       const int64_t at = i * ldr + c;
       a[q] = ok[q] ? A[at] : 0.f;
-      ao[q] = (ok[q] && hist) ? __ldg(Aold + at) : 0.f;
+      ao[q] = (ok[q] && has_old) ? __ldg(Aold + at) : 0.f;
       gv[q] = ok[q] ? __ldg(G + at) : 0.f;
     }
     if (hist) {
@@ -863,6 +891,7 @@ __global__ void __launch_bounds__(kThreads) k_factor_update_wide(int64_t rows, i
                                                                  long long code, int stage) {
   extern __shared__ float sm[];
   const bool hist = Mk != nullptr;
+  const bool has_old = hist && Aold != nullptr;
   const int RR = rank * rank;
   if (hist && stage) {  // Mk / Nk staged in shared memory when they fit, else read through L1/L2
     for (int i = threadIdx.x; i < RR; i += blockDim.x) {
@@ -885,7 +914,7 @@ __global__ void __launch_bounds__(kThreads) k_factor_update_wide(int64_t rows, i
     for (int j = 0; j < CPL; ++j) {
       const int cc = lane + j * 32;
       a[j] = (cc < rank && valid) ? A[i * ldr + cc] : 0.f;
-      ao[j] = (hist && cc < rank && valid) ? Aold[i * ldr + cc] : 0.f;
+      ao[j] = (has_old && cc < rank && valid) ? Aold[i * ldr + cc] : 0.f;
     }
     float h[CPL];
 #pragma unroll
@@ -1214,8 +1243,15 @@ void gram_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int ra
 }
 
 void hist_coeffs_enqueue(Ctx* ctx, int ndim, int rank, const double* P, const double* C, const double* S,
-                         double w, float* Mk, float* Nk) {
-  k_hist_coeffs<<<1, 256, 0, ctx->stream>>>(ndim, rank, P, C, S, w, Mk, Nk);
+                         double w, float* Mk, float* Nk, const double* s, double extra) {
+  k_hist_coeffs<<<1, 256, 0, ctx->stream>>>(ndim, rank, P, C, S, w, s, extra, Mk, Nk);
+  ctx->count();
+  check_launch();
+}
+
+void dense_wgrad_enqueue(Ctx* ctx, int ndim, int rank, int ldr, const double* P, const double* b, const double* s,
+                         double* out) {
+  k_dense_wgrad<<<1, ldr, 0, ctx->stream>>>(ndim, rank, ldr, P, b, s, out);
   ctx->count();
   check_launch();
 }

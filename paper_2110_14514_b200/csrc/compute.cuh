@@ -59,8 +59,12 @@ void gram_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int ra
 void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* outP,
                    double* outC, DevBuf& scratch);
 // History coefficients: Mk = w*(hadamard_{m!=k} P_m) o S, Nk = w*(hadamard_{m!=k} C_m) o S  (float [d][R][R]).
+// Dense-Gaussian model term: Mk += extra * Gamma_k o s s' (s: device double [R], nullable); C / S nullable.
 void hist_coeffs_enqueue(Ctx* ctx, int ndim, int rank, const double* P, const double* C, const double* S,
-                         double w, float* Mk, float* Nk);
+                         double w, float* Mk, float* Nk, const double* s = nullptr, double extra = 0.0);
+// Dense-Gaussian weight gradient 2((hadamard_m P_m) s - b) into out[ldr] (one block).
+void dense_wgrad_enqueue(Ctx* ctx, int ndim, int rank, int ldr, const double* P, const double* b, const double* s,
+                         double* out);
 // K5: g = G + lambda*A + (A Mk - Aold Nk) ; Adam ; clamp ; isfinite  (one mode).
 void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, const float* Aold,
                            const float* G, float* u, float* v, const float* Mk, const float* Nk,

@@ -29,6 +29,7 @@ int64_t gradient_tensor_impl(Ctx* ctx, const SamplesP& S, const ModelP& M, const
 void segment_layout_impl(Ctx* ctx, const int32_t* coords, int64_t n, int ndim, int mode, int64_t dim, int32_t* perm,
                          int64_t* offsets);
 void slice_contains_impl(Ctx* ctx, const Slice* s, const int64_t* subs, int64_t n, uint8_t* hit);
+void iota_enqueue(Ctx* ctx, int32_t* p, int64_t n);
 
 static thread_local std::string g_last_error;
 
@@ -172,6 +173,43 @@ static SamplesP sharded(const Ctx* ctx, SamplesP S) {
   return S;
 }
 
+// Ordinals 0..n-1 on the device (grown lazily, kept on the context).
+static const int32_t* iota_of(Ctx* ctx, int64_t n) {
+  if (n > ctx->iota_n) {
+    ctx->iota.ensure((size_t)std::max<int64_t>(n, 1) * 4);
+    iota_enqueue(ctx, ctx->iota.as<int32_t>(), n);
+    ctx->iota_n = n;
+  }
+  return ctx->iota.as<int32_t>();
+}
+
+// Every stored nonzero once with value weight `scale` (exact / dense-Gaussian terms),
+// sharded across the context's ranks.
+static SamplesP all_nonzeros(Ctx* ctx, const Slice* X, double scale) {
+  SamplesP S = samples_of(X, X->nnz ? iota_of(ctx, X->nnz) : nullptr, X->nnz, nullptr, 0);
+  S.nz_scale = scale;
+  return sharded(ctx, S);
+}
+
+// gradient_mode (solvers.py:110-124): "dense-gaussian" only with the Gaussian loss.
+static bool dense_mode(const ogcp_solver_config* cfg, int loss_kind) {
+  if (cfg->gradient_mode == 0) return false;
+  if (cfg->gradient_mode != 1) throw Error(OGCP_E_USAGE, "unknown gradient mode");
+  if (loss_kind != OGCP_GAUSSIAN) throw Error(OGCP_E_DATA, "gradient_mode 'dense-gaussian' requires gaussian loss");
+  return true;
+}
+
+// ctx->dense = [b (ldr) | s (ldr)] doubles; returns the device s after uploading w.
+static double* dense_upload_s(Ctx* ctx, const double* w, int rank, int ldr) {
+  ctx->dense.ensure((size_t)2 * ldr * 8);
+  std::vector<double> h(ldr, 0.0);
+  for (int r = 0; r < rank; ++r) h[r] = w[r];
+  double* s = ctx->dense.as<double>() + ldr;
+  OGCP_CUDA(cudaMemcpyAsync(s, h.data(), ldr * 8, cudaMemcpyHostToDevice, ctx->stream));
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return s;
+}
+
 static void upload_weights(Ctx* ctx, const double* w, int rank, int ldr, float* s_f) {
   std::vector<float> h(ldr, 0.0f);
   for (int r = 0; r < rank; ++r) h[r] = (float)w[r];
@@ -294,6 +332,45 @@ struct ObjectiveParts {
 
 static long long code_of(long long ev, int sub) { return ev * 4 + sub; }
 
+static const LossP kIdentityLoss = {OGCP_IDENTITY, 1e-10f, 1e-10};
+
+// sum over (i, j) of s_i s_j prod_m P_m[i][j]: ||M||^2 of the model (kernels.py:143-145).
+static double model_sq_host(const std::vector<double>& P, int ndim, int R, const double* s) {
+  const size_t RR = (size_t)R * R;
+  double acc = 0.0;
+  for (int i = 0; i < R; ++i) {
+    double row = 0.0;
+    for (int j = 0; j < R; ++j) {
+      double g = 1.0;
+      for (int m = 0; m < ndim; ++m) g *= P[m * RR + (size_t)i * R + j];
+      row += g * s[j];
+    }
+    acc += s[i] * row;
+  }
+  return acc;
+}
+
+struct FactorWork {
+  DevBuf grads;
+  HistBufs hb;
+  SampleBufs obj, grad;
+};
+
+static FactorWork& factor_work() {
+  static thread_local FactorWork w;
+  return w;
+}
+
+static void hist_alloc(HistBufs& hb, int ndim, int R) {
+  const size_t RR = (size_t)R * R;
+  hb.P.ensure(ndim * RR * 8);
+  hb.C.ensure(ndim * RR * 8);
+  hb.Poo.ensure(ndim * RR * 8);
+  hb.S.ensure(RR * 8);
+  hb.Mk.ensure(ndim * RR * 4);
+  hb.Nk.ensure(ndim * RR * 4);
+}
+
 // ============================================================= solve_weights
 static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config* cfg, const ogcp_loss* loss,
                                int64_t t, const ogcp_model* mdl, const double* s_init, double* s_out,
@@ -323,15 +400,20 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   int64_t po, qo, p, q;
   resolve_counts(cfg->samples.obj_nonzeros, cfg->samples.obj_zeros, X, &po, &qo);
   resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
-  if (po > 0 || p > 0) x_domain_check(X, L.kind);
   static thread_local SampleBufs obj, grad;
-  const bool semi = cfg->samples.semi_stratified != 0;
-  draw_sync(ctx, X, keyed(seed, {t, 2}), po, qo, cfg->samples.max_rejects, obj, semi);
-  SamplesP So = sharded(ctx, obj.sample_set(X));
-  precheck_draw(X, p, semi ? 0 : q);
-  grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
-  grad.semi = semi;
-  const int64_t budget = budget_of(q, cfg->samples.max_rejects);
+  const bool dense = dense_mode(cfg, L.kind);
+  SamplesP So{};
+  int64_t budget = 0;
+  if (!dense) {
+    if (po > 0 || p > 0) x_domain_check(X, L.kind);
+    const bool semi = cfg->samples.semi_stratified != 0;
+    draw_sync(ctx, X, keyed(seed, {t, 2}), po, qo, cfg->samples.max_rejects, obj, semi);
+    So = sharded(ctx, obj.sample_set(X));
+    precheck_draw(X, p, semi ? 0 : q);
+    grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+    grad.semi = semi;
+    budget = budget_of(q, cfg->samples.max_rejects);
+  }
   ctx->partials.ensure((size_t)kNumSMs * 8 * ldr * 8 + 64);
   double* part = ctx->partials.as<double>();
   ctx->scalars.ensure(64 * 8 + ldr * 8);
@@ -339,8 +421,41 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   double* gsum = dsc + 64;  // multi-GPU: the R-vector gradient summed across ranks
   double* hsc = ctx->host_scalars;
 
+  // dense-Gaussian (solvers.py:182-185, 220-224): with the factors fixed the
+  // Grams and b = Z' vec(X) are constant, so each step is an R-vector update
+  // and the objective ||X||^2 - 2 s'b + s'(hadamard P)s + (mu/2)||s||^2.
+  std::vector<double> Ph, bh(R, 0.0);
+  double* bdev = nullptr;
+  HistBufs* hb = nullptr;
+  if (dense) {
+    hb = &factor_work().hb;
+    hist_alloc(*hb, M.ndim, R);
+    grams_enqueue(ctx, M, nullptr, hb->P.as<double>(), *hb, true);
+    ctx->dense.ensure((size_t)2 * ldr * 8);
+    bdev = ctx->dense.as<double>();
+    const SamplesP Sx = all_nonzeros(ctx, X, 1.0);
+    const int nb = wgrad_enqueue(ctx, Sx, M, s_f, kIdentityLoss, part, code_of(0, 1));
+    sum_partials_enqueue(ctx, part, nb, ldr, bdev);
+    if (Sx.shard_world > 1) comm_allreduce_sum(ctx, bdev, (size_t)ldr);
+    Ph.resize((size_t)M.ndim * R * R);
+    OGCP_CUDA(cudaMemcpyAsync(Ph.data(), hb->P.ptr, Ph.size() * 8, cudaMemcpyDeviceToHost, st));
+    OGCP_CUDA(cudaMemcpyAsync(bh.data(), bdev, R * 8, cudaMemcpyDeviceToHost, st));
+    OGCP_CUDA(cudaStreamSynchronize(st));
+  }
+
   long long ev = 1;
   auto fest_fn = [&]() -> double {
+    if (dense) {
+      OGCP_CUDA(cudaMemcpyAsync(hsc + 8, ws, R * 8, cudaMemcpyDeviceToHost, st));
+      OGCP_CUDA(cudaStreamSynchronize(st));
+      const double* sv = hsc + 8;
+      double sb = 0.0, ss = 0.0;
+      for (int r = 0; r < R; ++r) {
+        sb += sv[r] * bh[r];
+        ss += sv[r] * sv[r];
+      }
+      return X->frob_sq - 2.0 * sb + model_sq_host(Ph, M.ndim, R, sv) + 0.5 * cfg->reg_weights * ss;
+    }
     reset_flags(ctx);
     const long long c = code_of(ev++, 1);
     int nb = objective_enqueue(ctx, So, M, s_f, L, part, c);
@@ -373,11 +488,17 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
       const long long ev0 = ev;
       for (int it = 0; it < cfg->iters_weights; ++it) {
         const long long e = ev++;
-        SamplesP Sg = sharded(ctx, grad.draw(ctx, X, keyed(seed, {t, 1, epoch, it}), budget, code_of(e, 0)));
-        int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1));
         const int64_t cnt = i + it + 1;
         const double rate_i = rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
                               (1.0 - std::pow(cfg->beta1, (double)cnt));
+        if (dense) {
+          dense_wgrad_enqueue(ctx, M.ndim, R, ldr, hb->P.as<double>(), bdev, ws, part);
+          weight_step_enqueue(ctx, part, 1, R, ldr, ws, s_f, cfg->reg_weights, rate_i, cfg->beta1, cfg->beta2,
+                              cfg->adam_eps, cfg->lower_bound, code_of(e, 2));
+          continue;
+        }
+        SamplesP Sg = sharded(ctx, grad.draw(ctx, X, keyed(seed, {t, 1, epoch, it}), budget, code_of(e, 0)));
+        int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1));
         const double* gparts = part;
         if (ctx->world > 1) {  // sum the shard gradients across ranks, then the replicated step
           sum_partials_enqueue(ctx, part, nb, ldr, gsum);
@@ -437,11 +558,6 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
 }
 
 // ============================================================= solve_factors
-struct FactorWork {
-  DevBuf grads;
-  HistBufs hb;
-  SampleBufs obj, grad;
-};
 
 static void window_upload(Ctx* ctx, HistBufs& hb, int R, const double* window_s, const int64_t* window_ids, int H,
                           double decay, int64_t t) {
@@ -472,24 +588,29 @@ __global__ void k_trace_sum(int ndim, int R, const double* __restrict__ P, doubl
   *out = t;
 }
 
-// F(factors) = data term on the fixed objective set + (w/2) history + (lambda/2) sum ||A||^2
+// F(factors) = data term on the fixed objective set + (w/2) history + (lambda/2) sum ||A||^2.
+// dense_s (host weights) selects the exact Gaussian residual ||X||^2 - 2<X,M> + ||M||^2
+// (kernels.py:135-146) as the data term instead of the sampled estimate.
 static double factor_objective(Ctx* ctx, const Slice* X, const SamplesP& So, const ModelP& M, const float* s_f,
                                const LossP& L, float* const* old_factors, int H, const ogcp_solver_config* cfg,
                                HistBufs& hb, long long code, int64_t budget, int64_t t,
-                               const char* what = "factor solve") {
+                               const char* what = "factor solve", const double* dense_s = nullptr) {
   cudaStream_t st = ctx->stream;
   const int RR = M.rank * M.rank;
   double* part = ctx->partials.as<double>();
   double* dsc = ctx->scalars.as<double>();
   double* hsc = ctx->host_scalars;
+  const bool dense = dense_s != nullptr;
   reset_flags(ctx);
-  int nb = objective_enqueue(ctx, So, M, s_f, L, part, code);
+  const SamplesP S = dense ? all_nonzeros(ctx, X, 1.0) : So;
+  int nb = objective_enqueue(ctx, S, M, s_f, dense ? kIdentityLoss : L, part, code);
   sum_partials_enqueue(ctx, part, nb, 1, dsc);
-  const bool collective = So.shard_world > 1;
+  const bool collective = S.shard_world > 1;
   if (collective) comm_allreduce_sum(ctx, dsc, 1);  // the data term is per-shard; Grams are replicated
   const bool hist = cfg->hist_weight != 0.0 && H > 0;
   const bool reg = cfg->reg_factors != 0.0;
-  if (hist || reg) {
+  std::vector<double> Ph;
+  if (hist || reg || dense) {
     if (hist) grams_pc_enqueue(ctx, M, old_factors, hb);
     else grams_enqueue(ctx, M, nullptr, hb.P.as<double>(), hb, true);
     if (reg) {
@@ -500,14 +621,18 @@ static double factor_objective(Ctx* ctx, const Slice* X, const SamplesP& So, con
       hist_penalty_enqueue(ctx, M.ndim, M.rank, hb.Poo.as<double>(), hb.C.as<double>(), hb.P.as<double>(),
                            hb.Ws.as<double>(), hb.coef.as<double>(), H, dsc + 1);
     }
+    if (dense) {
+      Ph.resize((size_t)M.ndim * RR);
+      OGCP_CUDA(cudaMemcpyAsync(Ph.data(), hb.P.ptr, Ph.size() * 8, cudaMemcpyDeviceToHost, st));
+    }
   }
-  (void)RR;
   OGCP_CUDA(cudaMemcpyAsync(hsc, dsc, 3 * 8, cudaMemcpyDeviceToHost, st));
   if (collective) comm_sync_flags(ctx);
   fetch_flags(ctx);
   OGCP_CUDA(cudaStreamSynchronize(st));
   check_flags(ctx, X, L.kind, budget, what, t);
   double val = hsc[0];
+  if (dense) val = X->frob_sq - 2.0 * hsc[0] + model_sq_host(Ph, M.ndim, M.rank, dense_s);
   if (hist) val += 0.5 * cfg->hist_weight * hsc[1];
   if (reg) val += 0.5 * cfg->reg_factors * hsc[2];
   return val;
@@ -529,49 +654,46 @@ static void adam_epoch(Ctx* ctx, const ModelP& M, float* const* A, ogcp_adam_sta
 }
 
 // One factor iteration: draw -> K2/K3 -> (K4 Grams -> coefficients) -> K5 per mode.
+// dense_s (device double weights) selects the exact Gaussian gradient
+// 2 (A_k (Gamma_k o s s') - mttkrp(X, k) diag(s)) (kernels.py:117-132): the
+// scatter runs over every stored nonzero with y = -2 x and the model term
+// joins the history coefficients of K5.
 static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* const* A, const float* s_f,
                              const LossP& L, float* const* old_factors, bool hist, const ogcp_solver_config* cfg,
-                             ogcp_adam_state* ad, double rate_i, const Pcg64& g, int64_t p, int64_t q,
-                             int64_t budget, FactorWork& W, long long ev) {
+                             ogcp_adam_state* ad, double rate_i, const Pcg64& g, int64_t budget, FactorWork& W,
+                             long long ev, const double* dense_s = nullptr) {
   const int RR = M.rank * M.rank;
-  SamplesP Sg = sharded(ctx, W.grad.draw(ctx, X, g, budget, code_of(ev, 0)));
-  (void)p;
-  (void)q;
+  const bool dense = dense_s != nullptr;
   float* gp[kMaxModes];
   size_t off = 0;
   for (int k = 0; k < M.ndim; ++k) {
     gp[k] = W.grads.as<float>() + off;
     off += (size_t)M.dims[k] * M.ldr;
   }
-  sgrad_enqueue(ctx, Sg, M, s_f, L, gp, code_of(ev, 1));
+  if (dense) {
+    sgrad_enqueue(ctx, all_nonzeros(ctx, X, -2.0), M, s_f, kIdentityLoss, gp, code_of(ev, 1));
+  } else {
+    SamplesP Sg = sharded(ctx, W.grad.draw(ctx, X, g, budget, code_of(ev, 0)));
+    sgrad_enqueue(ctx, Sg, M, s_f, L, gp, code_of(ev, 1));
+  }
   comm_allreduce_sum(ctx, W.grads.as<float>(), off);  // multi-GPU: sum of the shard gradients
-  if (hist) {
-    grams_pc_enqueue(ctx, M, old_factors, W.hb);
-    hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), W.hb.C.as<double>(), W.hb.S.as<double>(),
-                        cfg->hist_weight, W.hb.Mk.as<float>(), W.hb.Nk.as<float>());
+  const bool coeffs = hist || dense;
+  if (coeffs) {
+    if (hist) grams_pc_enqueue(ctx, M, old_factors, W.hb);
+    else grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true);
+    hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), hist ? W.hb.C.as<double>() : nullptr,
+                        hist ? W.hb.S.as<double>() : nullptr, cfg->hist_weight, W.hb.Mk.as<float>(),
+                        W.hb.Nk.as<float>(), dense_s, 2.0);
   }
   for (int k = 0; k < M.ndim; ++k) {
     factor_update_enqueue(ctx, M.dims[k], M.rank, M.ldr, A[k], hist ? old_factors[k] : nullptr, gp[k], ad->u[k],
-                          ad->v[k], hist ? W.hb.Mk.as<float>() + (size_t)k * RR : nullptr,
-                          hist ? W.hb.Nk.as<float>() + (size_t)k * RR : nullptr, cfg->reg_factors, rate_i,
+                          ad->v[k], coeffs ? W.hb.Mk.as<float>() + (size_t)k * RR : nullptr,
+                          coeffs ? W.hb.Nk.as<float>() + (size_t)k * RR : nullptr, cfg->reg_factors, rate_i,
                           cfg->beta1, cfg->beta2, cfg->adam_eps, cfg->lower_bound, code_of(ev, 2));
   }
 }
 
-static FactorWork& factor_work() {
-  static thread_local FactorWork w;
-  return w;
-}
 
-static void hist_alloc(HistBufs& hb, int ndim, int R) {
-  const size_t RR = (size_t)R * R;
-  hb.P.ensure(ndim * RR * 8);
-  hb.C.ensure(ndim * RR * 8);
-  hb.Poo.ensure(ndim * RR * 8);
-  hb.S.ensure(RR * 8);
-  hb.Mk.ensure(ndim * RR * 4);
-  hb.Nk.ensure(ndim * RR * 4);
-}
 
 static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config* cfg, const ogcp_loss* loss,
                                int64_t t, const ogcp_model* mdl, float* const* old_factors, const double* weights,
@@ -593,6 +715,8 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   for (int k = 0; k < M.ndim; ++k) gtot += (size_t)M.dims[k] * M.ldr;
   W.grads.ensure(gtot * 4);
   hist_alloc(W.hb, M.ndim, M.rank);
+  const bool dense = dense_mode(cfg, L.kind);
+  const double* s_dev = dense ? dense_upload_s(ctx, weights, M.rank, M.ldr) : nullptr;
   const bool hist = cfg->hist_weight != 0.0 && H > 0;
   if (hist && !old_factors) throw Error(OGCP_E_DATA, "history terms require the previous-step factors");
   window_upload(ctx, W.hb, M.rank, window_s, window_ids, H, cfg->hist_decay, t);
@@ -610,17 +734,23 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   int64_t po, qo, p, q;
   resolve_counts(cfg->samples.obj_nonzeros, cfg->samples.obj_zeros, X, &po, &qo);
   resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
-  if (po > 0 || p > 0) x_domain_check(X, L.kind);
-  const bool semi = cfg->samples.semi_stratified != 0;
-  draw_sync(ctx, X, keyed(seed, {t, 4}), po, qo, cfg->samples.max_rejects, W.obj, semi);
-  SamplesP So = sharded(ctx, W.obj.sample_set(X));
-  precheck_draw(X, p, semi ? 0 : q);
-  W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
-  W.grad.semi = semi;
-  const int64_t budget = budget_of(q, cfg->samples.max_rejects);
+  SamplesP So{};
+  int64_t budget = 0;
+  if (!dense) {  // the dense-Gaussian solve draws nothing (solvers.py:310-329)
+    if (po > 0 || p > 0) x_domain_check(X, L.kind);
+    const bool semi = cfg->samples.semi_stratified != 0;
+    draw_sync(ctx, X, keyed(seed, {t, 4}), po, qo, cfg->samples.max_rejects, W.obj, semi);
+    So = sharded(ctx, W.obj.sample_set(X));
+    precheck_draw(X, p, semi ? 0 : q);
+    W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+    W.grad.semi = semi;
+    budget = budget_of(q, cfg->samples.max_rejects);
+  }
+  const double* dense_w = dense ? weights : nullptr;
 
   long long ev = 1;
-  double fest = factor_objective(ctx, X, So, M, s_f, L, old_factors, H, cfg, W.hb, code_of(ev++, 1), budget, t);
+  double fest = factor_objective(ctx, X, So, M, s_f, L, old_factors, H, cfg, W.hb, code_of(ev++, 1), budget, t,
+                                 "factor solve", dense_w);
   std::vector<double> objv{fest};
   int64_t iter = *iteration;
   int epochs = 0, rejections = 0;
@@ -635,7 +765,7 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
         const double rate_i = ad->rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
                               (1.0 - std::pow(cfg->beta1, (double)cnt));
         factor_iteration(ctx, X, M, A, s_f, L, old_factors, hist, cfg, ad, rate_i, keyed(seed, {t, 3, epoch, it}),
-                         p, q, budget, W, ev++);
+                         budget, W, ev++, dense ? s_dev : nullptr);
       }
       comm_sync_flags(ctx);
       fetch_flags(ctx);
@@ -649,7 +779,8 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
       if (attempt > 8) throw Error(OGCP_E_INTERNAL, "sampler could not provision enough candidates");
     }
     iter += cfg->iters_factors;
-    fest = factor_objective(ctx, X, So, M, s_f, L, old_factors, H, cfg, W.hb, code_of(ev++, 1), budget, t);
+    fest = factor_objective(ctx, X, So, M, s_f, L, old_factors, H, cfg, W.hb, code_of(ev++, 1), budget, t,
+                            "factor solve", dense_w);
     if (!std::isfinite(fest)) throw Error(OGCP_E_DIVERGENCE, "factor solve diverged at slice " + std::to_string(t));
     if (fest > fold) {
       adam_epoch(ctx, M, A, ad, false);
@@ -714,25 +845,37 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
   int64_t po, qo, p, q;
   resolve_counts(cfg->samples.obj_nonzeros, cfg->samples.obj_zeros, X, &po, &qo);
   resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
-  if (po > 0 || p > 0) x_domain_check(X, L.kind);
-  const bool semi = cfg->samples.semi_stratified != 0;
-  draw_sync(ctx, X, keyed(seed, {seed_key, 8}), po, qo, cfg->samples.max_rejects, W.obj, semi);
-  SamplesP So = sharded(ctx, W.obj.sample_set(X));
-  precheck_draw(X, p, semi ? 0 : q);
-  W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
-  W.grad.semi = semi;
-  const int64_t budget = budget_of(q, cfg->samples.max_rejects);
+  const bool dense = dense_mode(cfg, L.kind);
+  SamplesP So{};
+  int64_t budget = 0;
+  if (!dense) {
+    if (po > 0 || p > 0) x_domain_check(X, L.kind);
+    const bool semi = cfg->samples.semi_stratified != 0;
+    draw_sync(ctx, X, keyed(seed, {seed_key, 8}), po, qo, cfg->samples.max_rejects, W.obj, semi);
+    So = sharded(ctx, W.obj.sample_set(X));
+    precheck_draw(X, p, semi ? 0 : q);
+    W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+    W.grad.semi = semi;
+    budget = budget_of(q, cfg->samples.max_rejects);
+  }
   const char* what = "static solve";
+  double* bdev = nullptr;
+  if (dense) {
+    ctx->dense.ensure((size_t)2 * ldr * 8);
+    bdev = ctx->dense.as<double>();
+  }
 
   long long ev = 1;
+  std::vector<double> cur_w(R);
   auto fest_fn = [&]() -> double {
+    OGCP_CUDA(cudaMemcpyAsync(hsc + 8, ws, R * 8, cudaMemcpyDeviceToHost, st));
+    OGCP_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < R; ++r) cur_w[r] = hsc[8 + r];
     double v = factor_objective(ctx, X, So, M, s_f, L, nullptr, 0, cfg, W.hb, code_of(ev++, 1), budget, seed_key,
-                                what);
+                                what, dense ? cur_w.data() : nullptr);
     if (cfg->reg_weights) {
-      OGCP_CUDA(cudaMemcpyAsync(hsc + 8, ws, R * 8, cudaMemcpyDeviceToHost, st));
-      OGCP_CUDA(cudaStreamSynchronize(st));
       double ss = 0.0;
-      for (int r = 0; r < R; ++r) ss += hsc[8 + r] * hsc[8 + r];
+      for (int r = 0; r < R; ++r) ss += cur_w[r] * cur_w[r];
       v += 0.5 * cfg->reg_weights * ss;
     }
     return v;
@@ -768,6 +911,28 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
         const int64_t cnt = iter + it + 1;
         const double rate_i = ad->rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
                               (1.0 - std::pow(cfg->beta1, (double)cnt));
+        if (dense) {
+          // exact Gaussian gradients (solvers.py:473-478) at the current iterate
+          grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true);
+          const SamplesP Sx = all_nonzeros(ctx, X, 1.0);
+          const int nbx = wgrad_enqueue(ctx, Sx, M, s_f, kIdentityLoss, part, code_of(e, 1));
+          sum_partials_enqueue(ctx, part, nbx, ldr, bdev);
+          if (Sx.shard_world > 1) comm_allreduce_sum(ctx, bdev, (size_t)ldr);
+          hist_coeffs_enqueue(ctx, M.ndim, R, W.hb.P.as<double>(), nullptr, nullptr, 0.0, W.hb.Mk.as<float>(),
+                              W.hb.Nk.as<float>(), ws, 2.0);
+          sgrad_enqueue(ctx, all_nonzeros(ctx, X, -2.0), M, s_f, kIdentityLoss, gp, code_of(e, 1));
+          comm_allreduce_sum(ctx, W.grads.as<float>(), gtot);
+          dense_wgrad_enqueue(ctx, M.ndim, R, ldr, W.hb.P.as<double>(), bdev, ws, part);
+          weight_step_enqueue(ctx, part, 1, R, ldr, ws, s_f, cfg->reg_weights, rate_i, cfg->beta1, cfg->beta2,
+                              cfg->adam_eps, cfg->lower_bound, code_of(e, 2));
+          const int RR = R * R;
+          for (int k = 0; k < M.ndim; ++k)
+            factor_update_enqueue(ctx, M.dims[k], R, ldr, A[k], nullptr, gp[k], ad->u[k], ad->v[k],
+                                  W.hb.Mk.as<float>() + (size_t)k * RR, W.hb.Nk.as<float>() + (size_t)k * RR,
+                                  cfg->reg_factors, rate_i, cfg->beta1, cfg->beta2, cfg->adam_eps, cfg->lower_bound,
+                                  code_of(e, 2));
+          continue;
+        }
         SamplesP Sg = sharded(ctx, W.grad.draw(ctx, X, keyed(seed, {seed_key, 7, epoch, it}), budget, code_of(e, 0)));
         // both gradients at the current iterate, before either update
         sgrad_enqueue(ctx, Sg, M, s_f, L, gp, code_of(e, 1));
@@ -826,6 +991,45 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
     trace->epochs = epochs;
     trace->rejections = rejections;
   }
+}
+
+// G += lambda A + (A Mk - Aold Nk): the K5 kernel on scratch moments with beta1 = 0
+// and rate 0, so its first moment u' = g is the assembled gradient.
+static void assemble_grads(Ctx* ctx, const ModelP& M, float* const* old_factors, float* const* grads, const float* Mk,
+                           const float* Nk, double reg_factors, HistBufs& hb) {
+  const int RR = M.rank * M.rank;
+  for (int k = 0; k < M.ndim; ++k) {
+    const size_t n = (size_t)M.dims[k] * M.ldr;
+    hb.tmp.ensure(n * 3 * 4);
+    float* u = hb.tmp.as<float>();
+    float* v = u + n;
+    float* a = v + n;
+    OGCP_CUDA(cudaMemsetAsync(u, 0, n * 4, ctx->stream));
+    OGCP_CUDA(cudaMemsetAsync(v, 0, n * 4, ctx->stream));
+    OGCP_CUDA(cudaMemcpyAsync(a, M.A[k], n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    factor_update_enqueue(ctx, M.dims[k], M.rank, M.ldr, a, old_factors ? old_factors[k] : nullptr, grads[k], u, v,
+                          Mk ? Mk + (size_t)k * RR : nullptr, Nk ? Nk + (size_t)k * RR : nullptr, reg_factors, 0.0,
+                          0.0, 0.0, 1.0, -INFINITY, code_of(1, 2));
+    OGCP_CUDA(cudaMemcpyAsync(grads[k], u, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+}
+
+// Per-mode Grams (host [ndim][R][R]) and b = Z' vec(X) (host [R]) at the model.
+static void dense_gamma_b(Ctx* ctx, const Slice* X, const ModelP& M, const float* s_f, HistBufs& hb,
+                          std::vector<double>& Ph, std::vector<double>& bh) {
+  grams_enqueue(ctx, M, nullptr, hb.P.as<double>(), hb, true);
+  ctx->dense.ensure((size_t)2 * M.ldr * 8);
+  double* bdev = ctx->dense.as<double>();
+  double* part = ctx->partials.as<double>();
+  const SamplesP Sx = all_nonzeros(ctx, X, 1.0);
+  const int nb = wgrad_enqueue(ctx, Sx, M, s_f, kIdentityLoss, part, code_of(1, 1));
+  sum_partials_enqueue(ctx, part, nb, M.ldr, bdev);
+  if (Sx.shard_world > 1) comm_allreduce_sum(ctx, bdev, (size_t)M.ldr);
+  Ph.resize((size_t)M.ndim * M.rank * M.rank);
+  bh.resize(M.rank);
+  OGCP_CUDA(cudaMemcpyAsync(Ph.data(), hb.P.ptr, Ph.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  OGCP_CUDA(cudaMemcpyAsync(bh.data(), bdev, M.rank * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 }  // namespace ogcp
@@ -1133,27 +1337,137 @@ int ogcp_factor_gradients(ogcp_ctx* ctx, const ogcp_slice* s, const int32_t* ord
     hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), W.hb.C.as<double>(), W.hb.S.as<double>(),
                         hist_weight, W.hb.Mk.as<float>(), W.hb.Nk.as<float>());
   }
-  // G += lambda A + history: run the K5 kernel on scratch moments with
-  // beta1 = 0 and rate 0, so its first moment u' = g is the assembled gradient.
-  for (int k = 0; k < M.ndim; ++k) {
-    DevBuf& tmp = W.hb.tmp;
-    const size_t n = (size_t)M.dims[k] * M.ldr;
-    tmp.ensure(n * 3 * 4);
-    float* u = tmp.as<float>();
-    float* v = u + n;
-    float* a = v + n;
-    OGCP_CUDA(cudaMemsetAsync(u, 0, n * 4, ctx->stream));
-    OGCP_CUDA(cudaMemsetAsync(v, 0, n * 4, ctx->stream));
-    OGCP_CUDA(cudaMemcpyAsync(a, M.A[k], n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
-    factor_update_enqueue(ctx, M.dims[k], M.rank, M.ldr, a, hist ? old_factors[k] : nullptr, grads_dev[k], u, v,
-                          hist ? W.hb.Mk.as<float>() + (size_t)k * RR : nullptr,
-                          hist ? W.hb.Nk.as<float>() + (size_t)k * RR : nullptr, reg_factors, 0.0, 0.0, 0.0, 1.0,
-                          -INFINITY, code_of(1, 2));
-    OGCP_CUDA(cudaMemcpyAsync(grads_dev[k], u, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
-  }
+  assemble_grads(ctx, M, hist ? old_factors : nullptr, grads_dev, hist ? W.hb.Mk.as<float>() : nullptr,
+                 hist ? W.hb.Nk.as<float>() : nullptr, reg_factors, W.hb);
   fetch_flags(ctx);
   OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
   check_flags(ctx, s, L.kind, 0, "gradient", t);
+  OGCP_API_END
+}
+
+int ogcp_dense_gaussian_gradients(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m,
+                                  float* const* old_factors, const double* weights, const double* window_s,
+                                  const int64_t* window_ids, int32_t H, double hist_weight, double hist_decay,
+                                  int64_t t, double reg_factors, double reg_weights, float* const* grads_dev,
+                                  double* weight_grad) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  check_model_slice(M, s);
+  const int R = M.rank, ldr = M.ldr;
+  ctx->wsolve.ensure((size_t)ldr * (6 * 8 + 4));
+  float* s_f = reinterpret_cast<float*>(ctx->wsolve.as<double>() + 6 * ldr);
+  upload_weights(ctx, weights, R, ldr, s_f);
+  const double* s_dev = dense_upload_s(ctx, weights, R, ldr);
+  ctx->partials.ensure((size_t)kNumSMs * 8 * ldr * 8 + 64);
+  FactorWork& W = factor_work();
+  hist_alloc(W.hb, M.ndim, R);
+  const bool hist = hist_weight != 0.0 && H > 0;
+  if (hist && !old_factors) throw Error(OGCP_E_DATA, "history terms require the previous-step factors");
+  reset_flags(ctx);
+  if (grads_dev) {
+    sgrad_enqueue(ctx, all_nonzeros(ctx, s, -2.0), M, s_f, kIdentityLoss, grads_dev, code_of(1, 1));
+    window_upload(ctx, W.hb, R, window_s, window_ids, H, hist_decay, t);
+    if (hist) {
+      k_window_matrix<<<1, 256, 0, ctx->stream>>>(R, H, W.hb.Ws.as<double>(), W.hb.coef.as<double>(),
+                                                  W.hb.S.as<double>());
+      ctx->count();
+      grams_pc_enqueue(ctx, M, old_factors, W.hb);
+    } else {
+      grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true);
+    }
+    hist_coeffs_enqueue(ctx, M.ndim, R, W.hb.P.as<double>(), hist ? W.hb.C.as<double>() : nullptr,
+                        hist ? W.hb.S.as<double>() : nullptr, hist_weight, W.hb.Mk.as<float>(), W.hb.Nk.as<float>(),
+                        s_dev, 2.0);
+    assemble_grads(ctx, M, hist ? old_factors : nullptr, grads_dev, W.hb.Mk.as<float>(), W.hb.Nk.as<float>(),
+                   reg_factors, W.hb);
+  }
+  if (weight_grad) {
+    std::vector<double> Ph, bh;
+    dense_gamma_b(ctx, s, M, s_f, W.hb, Ph, bh);
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
+      for (int j = 0; j < R; ++j) {
+        double g = 1.0;
+        for (int k = 0; k < M.ndim; ++k) g *= Ph[(size_t)k * R * R + (size_t)r * R + j];
+        acc += g * weights[j];
+      }
+      weight_grad[r] = 2.0 * (acc - bh[r]) + reg_weights * weights[r];
+    }
+  }
+  fetch_flags(ctx);
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+  check_flags(ctx, s, OGCP_GAUSSIAN, 0, "gradient", t);
+  OGCP_API_END
+}
+
+int ogcp_gaussian_residual(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m, const double* weights,
+                           double* out) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  check_model_slice(M, s);
+  ctx->wsolve.ensure((size_t)M.ldr * (6 * 8 + 4));
+  float* s_f = reinterpret_cast<float*>(ctx->wsolve.as<double>() + 6 * M.ldr);
+  upload_weights(ctx, weights, M.rank, M.ldr, s_f);
+  ctx->partials.ensure((size_t)kNumSMs * 8 * M.ldr * 8 + 64);
+  ctx->scalars.ensure(64 * 8);
+  FactorWork& W = factor_work();
+  hist_alloc(W.hb, M.ndim, M.rank);
+  ogcp_solver_config cfg{};
+  *out = factor_objective(ctx, s, SamplesP{}, M, s_f, kIdentityLoss, nullptr, 0, &cfg, W.hb, code_of(1, 1), 0, 0,
+                          "gaussian residual", weights);
+  OGCP_API_END
+}
+
+int ogcp_solve_weights_ls(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m, double reg_weights,
+                          double* s_out) {
+  OGCP_API_BEGIN
+  ModelP M = model_of(m);
+  check_model_slice(M, s);
+  const int R = M.rank;
+  ctx->wsolve.ensure((size_t)M.ldr * (6 * 8 + 4));
+  float* s_f = reinterpret_cast<float*>(ctx->wsolve.as<double>() + 6 * M.ldr);
+  std::vector<double> zeros(R, 0.0);
+  upload_weights(ctx, zeros.data(), R, M.ldr, s_f);
+  ctx->partials.ensure((size_t)kNumSMs * 8 * M.ldr * 8 + 64);
+  FactorWork& W = factor_work();
+  hist_alloc(W.hb, M.ndim, R);
+  reset_flags(ctx);
+  std::vector<double> Ph, bh;
+  dense_gamma_b(ctx, s, M, s_f, W.hb, Ph, bh);
+  // (hadamard_k Gram_k + mu I) s = b by LU with partial pivoting (LAPACK gesv);
+  // an exactly zero pivot is the singular system numpy.linalg.solve rejects.
+  std::vector<double> a((size_t)R * R);
+  for (int i = 0; i < R; ++i)
+    for (int j = 0; j < R; ++j) {
+      double g = 1.0;
+      for (int k = 0; k < M.ndim; ++k) g *= Ph[(size_t)k * R * R + (size_t)i * R + j];
+      a[(size_t)i * R + j] = g + (i == j ? reg_weights : 0.0);
+    }
+  std::vector<double> x = bh;
+  for (int c = 0; c < R; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < R; ++r)
+      if (std::fabs(a[(size_t)r * R + c]) > std::fabs(a[(size_t)piv * R + c])) piv = r;
+    if (a[(size_t)piv * R + c] == 0.0)
+      throw Error(OGCP_E_DATA,
+                  "temporal least-squares system is singular; set a positive weight regularization (mu)");
+    if (piv != c) {
+      for (int j = 0; j < R; ++j) std::swap(a[(size_t)c * R + j], a[(size_t)piv * R + j]);
+      std::swap(x[c], x[piv]);
+    }
+    for (int r = c + 1; r < R; ++r) {
+      const double f = a[(size_t)r * R + c] / a[(size_t)c * R + c];
+      if (f == 0.0) continue;
+      for (int j = c; j < R; ++j) a[(size_t)r * R + j] -= f * a[(size_t)c * R + j];
+      x[r] -= f * x[c];
+    }
+  }
+  for (int r = R - 1; r >= 0; --r) {
+    double acc = x[r];
+    for (int j = r + 1; j < R; ++j) acc -= a[(size_t)r * R + j] * x[j];
+    x[r] = acc / a[(size_t)r * R + r];
+  }
+  for (int r = 0; r < R; ++r) s_out[r] = x[r];
   OGCP_API_END
 }
 
@@ -1293,13 +1607,7 @@ int ogcp_local_loss(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m, con
     sum_partials_enqueue(ctx, part, nb, 1, dsc);
     SamplesP S = samples_of(s, nullptr, 0, nullptr, 0);
     if (s->nnz > 0) {
-      // every stored entry once: ordinals 0..nnz-1
-      static thread_local DevBuf iota;
-      iota.ensure((size_t)s->nnz * 4);
-      std::vector<int32_t> h(s->nnz);
-      for (int64_t i = 0; i < s->nnz; ++i) h[i] = (int32_t)i;
-      OGCP_CUDA(cudaMemcpyAsync(iota.ptr, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-      S = samples_of(s, iota.as<int32_t>(), s->nnz, nullptr, 0);
+      S = samples_of(s, iota_of(ctx, s->nnz), s->nnz, nullptr, 0);  // every stored entry once
       int nb2 = exact_nz_enqueue(ctx, S, M, s_f, L, part + nb, code_of(1, 1));
       sum_partials_enqueue(ctx, part + nb, nb2, 1, dsc + 1);
     } else {

@@ -105,6 +105,12 @@ __global__ void k_row_offsets(const int32_t* __restrict__ sorted_rows, int64_t n
 
 static int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kNumSMs * 8)); }
 
+void iota_enqueue(Ctx* ctx, int32_t* p, int64_t n) {
+  k_iota32<<<grid_for(n), 256, 0, ctx->stream>>>(p, n);
+  ctx->count();
+  check_launch();
+}
+
 struct YScratch {
   DevBuf keys, keys_s, idx, idx_s, coords, y, head, pos, cub, bad, cols, cols_s;
 };

@@ -87,3 +87,23 @@ def history_penalty(M_old: KTensor, M_new: KTensor) -> float:
     """||M_old - M_new||_F^2 clamped at 0 (kernels.py:109-114)."""
     val = ktensor_inner(M_old, M_old) - 2.0 * ktensor_inner(M_old, M_new) + ktensor_inner(M_new, M_new)
     return max(val, 0.0)
+
+
+def gaussian_sum_sq_residual(X: SparseTensor, factors: Sequence[np.ndarray], weights: np.ndarray) -> float:
+    """Exact sum over all cells of (x - m)^2 = ||X||^2 - 2 <X, M> + ||M||^2 (kernels.py:135-146)."""
+    _check_factor_shapes(X, factors)
+    model = factors if isinstance(factors, DeviceModel) else DeviceModel.from_numpy(factors)
+    w, wp = _lib.f64arr(weights)
+    out = C.c_double()
+    _lib.check(_lib.lib().ogcp_gaussian_residual(_lib.ctx(), X._handle, C.byref(model.c()), wp, C.byref(out)))
+    return float(out.value)
+
+
+def dense_gaussian_mttkrp_gradient(X: SparseTensor, factors: Sequence[np.ndarray], weights: np.ndarray,
+                                   mode: int) -> np.ndarray:
+    """Exact Gaussian gradient dF/dA(mode) = 2 (A diag(s) Gram diag(s) - mttkrp(X) diag(s)) (kernels.py:117-132)."""
+    from .solvers import dense_gaussian_factor_gradients
+    _check_factor_shapes(X, factors)
+    if not 0 <= mode < X.ndim:
+        raise IndexError(f"mode {mode} out of range for {X.ndim}-way tensor")
+    return dense_gaussian_factor_gradients(X, factors, weights)[mode]

@@ -84,3 +84,39 @@ def global_loss(slices: Sequence, factors: Sequence[np.ndarray], weights_log: Se
     for t, X_t in enumerate(slices, start=1):
         total += local_loss(X_t, KTensor(weights_log[t - 1], factors), loss, mode="exact").value
     return total / len(slices)
+
+
+def congruence_score(M1, M2) -> float:
+    """Component-matched similarity of two K-tensors in [-1, 1] (metrics.py:95-148).
+
+    Per-mode cosines come from the GPU Gram kernel (cross Gram over the column
+    norms from the self Grams); the norms and signs are absorbed into the
+    weights and components are paired greedily by descending signed cosine
+    product, as in the reference."""
+    from .kernels import gram
+    if M1.dims != M2.dims:
+        raise DataError(f"dims differ: {M1.dims} vs {M2.dims}")
+    R1, R2 = M1.rank, M2.rank
+    Rm = max(R1, R2)
+    pad = lambda a: np.hstack([a, np.zeros((a.shape[0], Rm - a.shape[1]))])
+    lam1, lam2 = np.array(M1.weights, dtype=np.float64), np.array(M2.weights, dtype=np.float64)
+    cos = np.ones((R1, R2))
+    for a, b in zip(M1.factors, M2.factors):
+        A, B = pad(a), pad(b)
+        n1 = np.sqrt(np.maximum(np.diag(gram([A])), 0.0))[:R1]
+        n2 = np.sqrt(np.maximum(np.diag(gram([B])), 0.0))[:R2]
+        cross = gram([B], other_factors=[A])[:R1, :R2]
+        cos *= cross / np.outer(np.where(n1 > 0, n1, 1.0), np.where(n2 > 0, n2, 1.0))
+        lam1, lam2 = lam1 * n1, lam2 * n2
+    cos *= np.where(lam1 < 0, -1.0, 1.0)[:, None] * np.where(lam2 < 0, -1.0, 1.0)[None, :]
+    lam1, lam2 = np.abs(lam1), np.abs(lam2)
+    n_pairs = min(R1, R2)
+    masked, total = cos.copy(), 0.0
+    for _ in range(n_pairs):
+        i, j = np.unravel_index(np.argmax(masked), masked.shape)
+        top = max(lam1[i], lam2[j])
+        if top > 0:
+            total += (1.0 - abs(lam1[i] - lam2[j]) / top) * cos[i, j]
+        masked[i, :] = -np.inf
+        masked[:, j] = -np.inf
+    return total / n_pairs

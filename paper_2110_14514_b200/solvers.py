@@ -73,13 +73,12 @@ class SolverConfig:
         return Adam(rate, self.beta1, self.beta2, self.adam_eps, self.bound_for(loss), self.rate_decay)
 
     def _c(self, loss: LossFunction):
-        if self.gradient_mode != "sampled":
-            raise DataError("gradient_mode 'dense-gaussian' is not implemented by the GPU engine yet")
         return _lib.SolverC(self.tol_weights, self.tol_factors, self.max_epochs_weights, self.max_epochs_factors,
                             self.iters_weights, self.iters_factors, self.reg_factors, self.reg_weights,
                             self.hist_weight, self.hist_decay, int(bool(self.warm_start_weights)),
                             self.rate_weights, self.rate_factors, self.beta1, self.beta2, self.adam_eps,
-                            self.rate_decay, float(self.bound_for(loss)), self.samples._c())
+                            self.rate_decay, float(self.bound_for(loss)), self.samples._c(),
+                            GRADIENT_MODES.index(self.gradient_mode), TEMPORAL_SOLVERS.index(self.temporal_solver))
 
 
 @dataclass
@@ -250,7 +249,9 @@ def solve_static(X: SparseTensor, rank: int, loss: LossFunction, cfg: SolverConf
         cands = [solve_static(X, rank, loss, cfg, max_epochs=max_epochs, iters_per_epoch=iters_per_epoch,
                               rate=rate, tol=tol, seed_key=seed_key + r) for r in range(restarts)]
         if cfg.gradient_mode == "dense-gaussian":
-            raise DataError("gradient_mode 'dense-gaussian' is not implemented by the GPU engine yet")
+            from .kernels import gaussian_sum_sq_residual
+            scores = [gaussian_sum_sq_residual(X, c.model.factors, c.model.weights) for c in cands]
+            return cands[int(np.argmin(scores))]
         p_eval, q_eval = cfg.samples.objective_counts(X)
         ev = draw_samples(X, p_eval, q_eval, rng_at(cfg.samples.seed, seed_key, PHASE_RESTART_EVAL),
                           cfg.samples.max_rejects)
@@ -274,3 +275,59 @@ def solve_static(X: SparseTensor, rank: int, loss: LossFunction, cfg: SolverConf
     w, trace = solve_static_device(X, model, weights, loss, cfg, max_epochs=max_epochs, iters=iters, rate=rate,
                                    tol=tol, seed_key=seed_key)
     return StaticSolve(KTensor(w, model.to_numpy()), trace)
+
+
+def solve_weights_least_squares_device(X: SparseTensor, model: DeviceModel, reg_weights: float = 0.0) -> np.ndarray:
+    """Gaussian least-squares temporal row on device-resident factors (engine entry)."""
+    out = np.zeros(model.rank)
+    _lib.check(_lib.lib().ogcp_solve_weights_ls(_lib.ctx(), X._handle, C.byref(model.c()), float(reg_weights),
+                                                 out.ctypes.data_as(_lib.c_f64p)))
+    return out
+
+
+def solve_weights_least_squares(X: SparseTensor, factors: Sequence[np.ndarray], reg_weights: float = 0.0) -> np.ndarray:
+    """Single Gaussian least-squares solve for the temporal weights (solvers.py:271-288):
+    (hadamard_k Gram_k + mu I) s = Z' vec(X), implicit zeros as zero residuals."""
+    model = factors if isinstance(factors, DeviceModel) else DeviceModel.from_numpy(factors)
+    return solve_weights_least_squares_device(X, model, reg_weights)
+
+
+def _dense_gradients(X, factors, weights, want_factors, want_weights, old_factors=None, window=(),
+                     hist_weight=0.0, hist_decay=1.0, t=0, reg_factors=0.0, reg_weights=0.0):
+    model = factors if isinstance(factors, DeviceModel) else DeviceModel.from_numpy(factors)
+    if len(model.dims) != X.ndim or tuple(model.dims) != tuple(X.dims):
+        raise DataError("factor shapes do not match the tensor")
+    old = None
+    if old_factors is not None:
+        old = old_factors if isinstance(old_factors, DeviceModel) else DeviceModel.from_numpy(old_factors)
+    if hist_weight and len(window) and old is None:
+        raise DataError("history terms require the previous-step factors")
+    w, wp = _lib.f64arr(weights)
+    ids, ws = _window_arrays(window, model.rank)
+    grads = DeviceModel.zeros_like(model) if want_factors else None
+    gw = np.zeros(model.rank) if want_weights else None
+    op = old.ptrs() if old is not None else None
+    gp = grads.ptrs() if grads is not None else None
+    _lib.check(_lib.lib().ogcp_dense_gaussian_gradients(
+        _lib.ctx(), X._handle, C.byref(model.c()), C.cast(op, C.POINTER(C.c_void_p)) if op is not None else None,
+        wp, ws.ctypes.data_as(_lib.c_f64p), ids.ctypes.data_as(_lib.c_i64p), len(window), float(hist_weight),
+        float(hist_decay), int(t), float(reg_factors), float(reg_weights),
+        C.cast(gp, C.POINTER(C.c_void_p)) if gp is not None else None,
+        gw.ctypes.data_as(_lib.c_f64p) if gw is not None else None))
+    return (grads.to_numpy() if grads is not None else None), gw
+
+
+def dense_gaussian_factor_gradients(X: SparseTensor, factors: Sequence[np.ndarray], weights: np.ndarray, *,
+                                    old_factors=None, window: Sequence = (), hist_weight: float = 0.0,
+                                    hist_decay: float = 1.0, t: int = 0, reg_factors: float = 0.0) -> list:
+    """Exact Gaussian factor gradients plus regularization/history terms (solvers.py:145-156)."""
+    g, _ = _dense_gradients(X, factors, weights, True, False, old_factors, window, hist_weight, hist_decay, t,
+                            reg_factors)
+    return g
+
+
+def dense_gaussian_weight_gradient(X: SparseTensor, factors: Sequence[np.ndarray], weights: np.ndarray,
+                                   reg_weights: float = 0.0) -> np.ndarray:
+    """2 (Gamma s - Z' vec(X)) + mu s (solvers.py:182-185)."""
+    _, gw = _dense_gradients(X, factors, weights, False, True, reg_weights=reg_weights)
+    return gw

@@ -184,6 +184,7 @@ def main():
     streams["names"] = np.array(json.dumps([c[0] for c in scases]))
     np.savez_compressed(os.path.join(OUT, "streams.npz"), **streams)
     make_static()
+    make_gaussian()
     print("golden fixtures written to", os.path.abspath(OUT))
 
 
@@ -237,8 +238,97 @@ def make_static():
     np.savez_compressed(os.path.join(OUT, "static.npz"), **static)
 
 
+def make_gaussian():
+    """Gaussian special cases (kernels.py:117-146, solvers.py:145-185, 271-288) and
+    congruence (metrics.py:95-148)."""
+    sys.path.insert(0, REF)
+    import ogcp
+    from ogcp import kernels, metrics, sampling, solvers, streaming
+
+    rng = np.random.default_rng(77)
+    out = {}
+    X, _ = ogcp.gen_gaussian(ogcp.SyntheticSpec("gaussian", dims=(7, 6, 5, 6), rank=3, noise=0.1, seed=13))
+    out.update(subs0=X.subs0, vals=X.vals, dims=np.array(X.dims))
+    R = 3
+    init = [rng.uniform(0.2, 1.0, (d, R)) for d in X.dims[:-1]]
+    for k, a in enumerate(init):
+        out[f"init{k}"] = a
+    warm = rng.uniform(0.5, 1.5, (2, R))
+    out["warm_weights"] = warm
+    # direct calls on slice 1
+    X1 = X.slice_view(1)
+    out["resid"] = np.array(kernels.gaussian_sum_sq_residual(X1, init, warm[0]))
+    out["ls_mu0"] = solvers.solve_weights_least_squares(X1, init, 0.0)
+    out["ls_mu"] = solvers.solve_weights_least_squares(X1, init, 0.3)
+    out["dense_wgrad"] = solvers._dense_gaussian_weight_gradient(X1, init, warm[0], 0.2)
+    for k, g in enumerate(solvers.dense_gaussian_factor_gradients(X1, init, warm[0], reg_factors=0.1)):
+        out[f"dense_fgrad{k}"] = g
+    cases = {
+        "dense": dict(gradient_mode="dense-gaussian", max_epochs_weights=3, max_epochs_factors=2, iters_weights=20,
+                      iters_factors=20, rate_weights=0.2, rate_factors=1e-2, hist_weight=1.0, hist_decay=0.9,
+                      reg_factors=0.01, reg_weights=0.05, samples=sampling.SamplerConfig(100, 0, 200, 0, seed=4)),
+        "ls": dict(temporal_solver="least-squares", max_epochs_factors=2, iters_factors=15, rate_factors=1e-2,
+                   hist_weight=2.0, reg_weights=0.1, samples=sampling.SamplerConfig(150, 0, 200, 0, seed=4)),
+    }
+    loss = ogcp.make_loss("gaussian")
+    for name, kw in cases.items():
+        cfg = solvers.SolverConfig(**kw)
+        state = streaming.fresh_state(X.dims[:-1], R, loss, cfg, factors=init)
+        state.window = streaming.HistoryWindow(capacity=2)
+        for h in (1, 2):
+            state.weights_log.append(warm[h - 1])
+            state.window.observe(h, warm[h - 1], sampling.rng_at(cfg.samples.seed, h, sampling.PHASE_WINDOW))
+        state.t = 2
+        loc = []
+        for t in range(3, X.dims[-1] + 1):
+            m = streaming.process_slice(state, X.slice_view(t), loss, cfg, exact_loss=True)
+            loc.append(m.local_loss_exact)
+        out[f"{name}_cfg"] = np.array(json.dumps({k: v for k, v in kw.items() if k != "samples"}))
+        out[f"{name}_weights_log"] = np.vstack(state.weights_log)
+        out[f"{name}_local_exact"] = np.array(loc)
+        out[f"{name}_iteration"] = np.array(state.iteration)
+        out[f"{name}_ftrace"] = np.array(json.dumps([tr[2] for tr in state.trace_log]))
+        out[f"{name}_wtrace"] = np.array(json.dumps([tr[1] for tr in state.trace_log]))
+        for k, a in enumerate(state.factors):
+            out[f"{name}_final{k}"] = a
+    # static, dense-gaussian, two restarts
+    cfg = solvers.SolverConfig(gradient_mode="dense-gaussian", max_epochs_factors=3, iters_factors=10,
+                               rate_factors=2e-2, reg_factors=0.01, reg_weights=0.02,
+                               samples=sampling.SamplerConfig(100, 0, 200, 0, seed=4))
+    st = solvers.solve_static(X, R, loss, cfg, restarts=2, seed_key=3)
+    out["static_weights"] = st.model.weights
+    for k, a in enumerate(st.model.factors):
+        out[f"static_A{k}"] = a
+    out["static_trace"] = np.array(st.trace.objective)
+    # congruence pairs
+    pairs = []
+    for i in range(4):
+        R1, R2 = (3, 3) if i < 2 else (3, 4 + i - 2)
+        dims = (5, 4, 6)
+        w1 = rng.uniform(0.5, 2.0, R1)
+        f1 = [rng.standard_normal((d, R1)) for d in dims]
+        if i == 1:
+            w2 = w1[::-1] * 1.3
+            f2 = [a[:, ::-1] * (-1.0 if k == 0 else 1.0) for k, a in enumerate(f1)]
+            w2 = w2 * -1.0
+        else:
+            w2 = rng.uniform(-1.0, 2.0, R2)
+            f2 = [rng.standard_normal((d, R2)) for d in dims]
+            if i == 3:
+                f2[1][:, 0] = 0.0
+        sc = metrics.congruence_score(ogcp.KTensor(w1, f1), ogcp.KTensor(w2, f2))
+        out[f"cong{i}_w1"], out[f"cong{i}_w2"] = w1, np.array(w2)
+        for k in range(3):
+            out[f"cong{i}_f1_{k}"], out[f"cong{i}_f2_{k}"] = f1[k], np.array(f2[k])
+        pairs.append(sc)
+    out["cong_scores"] = np.array(pairs)
+    np.savez_compressed(os.path.join(OUT, "gaussian.npz"), **out)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["static"]:
         make_static()
+    elif sys.argv[1:] == ["gaussian"]:
+        make_gaussian()
     else:
         main()

@@ -23,7 +23,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.lib()
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.ogcp_abi_version() == 1
+    assert lib.ogcp_abi_version() == 2
 
 
 @pytest.mark.parametrize("seed,key,highs,n", [

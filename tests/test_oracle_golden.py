@@ -147,3 +147,76 @@ def test_static_and_warm_start_match_reference(golden_dir, name):
     np.testing.assert_allclose(np.vstack(st.weights_log), c("warm_weights_log"), rtol=1e-9, atol=1e-12)
     assert [h for h, _ in st.window] == c("warm_window_ids").tolist()
     assert st.t == int(c("warm_t"))
+
+
+def gaussian_fixture(golden_dir):
+    g = load(golden_dir, "gaussian.npz")
+    dims = tuple(int(d) for d in g["dims"])
+    full = O.Slice(dims, g["subs0"], g["vals"])
+    init = [g[f"init{k}"] for k in range(len(dims) - 1)]
+
+    def slice_at(t):
+        mask = full.subs0[:, -1] == t - 1
+        return O.Slice(dims[:-1], full.subs0[mask, :-1], full.vals[mask])
+    return g, dims, full, init, slice_at
+
+
+def gaussian_cfg(kw, seed=0):
+    return O.Cfg(kappa_w=kw.get("max_epochs_weights", 20), kappa_f=kw["max_epochs_factors"],
+                 tau_w=kw.get("iters_weights", 100), tau_f=kw["iters_factors"],
+                 rate_w=kw.get("rate_weights", 0.1), rate_f=kw["rate_factors"],
+                 hist_weight=kw.get("hist_weight", 0.0), hist_decay=kw.get("hist_decay", 1.0),
+                 reg_factors=kw.get("reg_factors", 0.0), reg_weights=kw.get("reg_weights", 0.0),
+                 p=100 if kw.get("gradient_mode") else 150, q=0, p_obj=200, q_obj=0, seed=4,
+                 dense=kw.get("gradient_mode") == "dense-gaussian",
+                 least_squares=kw.get("temporal_solver") == "least-squares")
+
+
+def test_gaussian_direct_match_reference(golden_dir):
+    g, dims, full, init, slice_at = gaussian_fixture(golden_dir)
+    X1, w0 = slice_at(1), g["warm_weights"][0]
+    assert O.gaussian_residual(X1, init, w0) == pytest.approx(float(g["resid"]), rel=1e-12)
+    np.testing.assert_allclose(O.least_squares_weights(X1, init, 0.0), g["ls_mu0"], rtol=1e-10)
+    np.testing.assert_allclose(O.least_squares_weights(X1, init, 0.3), g["ls_mu"], rtol=1e-10)
+    np.testing.assert_allclose(O.dense_weight_grad(X1, init, w0, 0.2), g["dense_wgrad"], rtol=1e-10)
+    for k, gk in enumerate(O.dense_factor_grads(X1, init, w0, None, (), 0.0, 1.0, 0, 0.1)):
+        np.testing.assert_allclose(gk, g[f"dense_fgrad{k}"], rtol=1e-10, atol=1e-12)
+    for i, want in enumerate(g["cong_scores"]):
+        got = O.congruence(g[f"cong{i}_w1"], [g[f"cong{i}_f1_{k}"] for k in range(3)],
+                           g[f"cong{i}_w2"], [g[f"cong{i}_f2_{k}"] for k in range(3)])
+        assert got == pytest.approx(float(want), rel=1e-12, abs=1e-14)
+
+
+@pytest.mark.parametrize("name", ["dense", "ls"])
+def test_gaussian_streams_match_reference(golden_dir, name):
+    g, dims, full, init, slice_at = gaussian_fixture(golden_dir)
+    cfg = gaussian_cfg(json.loads(str(g[f"{name}_cfg"])))
+    st = O.new_stream(init, "gaussian", cfg, capacity=2)
+    for h in (1, 2):
+        st.weights_log.append(g["warm_weights"][h - 1])
+        O.window_observe(st, h, g["warm_weights"][h - 1], cfg.seed)
+    st.t = 2
+    loc = []
+    for t in range(3, dims[-1] + 1):
+        s_t = O.slice_step(st, slice_at(t), "gaussian", cfg)
+        loc.append(O.exact_local_loss(slice_at(t), st.factors, s_t, "gaussian"))
+    np.testing.assert_allclose(np.vstack(st.weights_log), g[f"{name}_weights_log"], rtol=1e-8, atol=1e-12)
+    for k, a in enumerate(st.factors):
+        np.testing.assert_allclose(a, g[f"{name}_final{k}"], rtol=1e-8, atol=1e-12)
+    np.testing.assert_allclose(loc, g[f"{name}_local_exact"], rtol=1e-8)
+    assert st.iteration == int(g[f"{name}_iteration"])
+    for (_, w, f), wr, fr in zip(st.traces, json.loads(str(g[f"{name}_wtrace"])),
+                                 json.loads(str(g[f"{name}_ftrace"]))):
+        np.testing.assert_allclose(w, wr, rtol=1e-8)
+        np.testing.assert_allclose(f, fr, rtol=1e-8)
+
+
+def test_gaussian_static_restarts_match_reference(golden_dir):
+    g, dims, full, init, slice_at = gaussian_fixture(golden_dir)
+    cfg = O.Cfg(kappa_f=3, tau_f=10, rate_f=2e-2, reg_factors=0.01, reg_weights=0.02, p=100, q=0, p_obj=200,
+                q_obj=0, seed=4, dense=True)
+    w, fs, trace, *_ = O.static_fit(full, 3, "gaussian", cfg, restarts=2, seed_key=3)
+    np.testing.assert_allclose(w, g["static_weights"], rtol=1e-8)
+    for k, a in enumerate(fs):
+        np.testing.assert_allclose(a, g[f"static_A{k}"], rtol=1e-8, atol=1e-12)
+    np.testing.assert_allclose(trace, g["static_trace"], rtol=1e-8)
