@@ -226,8 +226,10 @@ def main():
         # the shard gradients / objective with NCCL (paper_2110_14514_b200/distributed.py)
         import paper_2110_14514_b200.distributed as PD
         PD.init_sharded_solves()
-    if os.environ.get("OGCP_SPLIT") == "0":  # A/B knob for the two-pass scatter
-        _lib.set_split_scatter(False)
+    if os.environ.get("OGCP_SPLIT") == "1":  # A/B knob for the two-pass scatter
+        _lib.set_split_scatter(True)
+    if os.environ.get("OGCP_BUCKETS") == "0":  # A/B knob for the bucketed merged walk
+        _lib.set_buckets(False)
     if os.environ.get("OGCP_MERGE") == "0":  # A/B knob for the merged draws
         _lib.set_merge_draws(False)
     loss = P.make_loss("poisson")

@@ -145,9 +145,13 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * nonzero draws (p >= eta/8) into distinct ordinals with multiplicities before
  * evaluation -- the same merge sampled_gradient_tensor performs
  * (sampling.py:233-237); 0 evaluates every draw separately. */
-/* OGCP_OPT_SPLIT_SCATTER (default 1): for merged sets, scatter the largest
- * random-access mode in a second pass from stored per-sample values. */
-enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2 };
+/* OGCP_OPT_SPLIT_SCATTER (default 0): for merged sets, scatter the largest
+ * random-access mode in a second pass from stored per-sample values.
+ * OGCP_OPT_BUCKETS (default 1): walk merged sets of slices with a large
+ * random-access mode in row-bucket order (Slice bucketed copy, built once per
+ * slice) so the bucket's factor/gradient rows stay L2-resident; a value k > 1
+ * forces k buckets on every merged solve (tests). */
+enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 3 };
 int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value);
 
 /* Multi-GPU (the reference is single-process): the

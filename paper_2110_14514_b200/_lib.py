@@ -234,6 +234,11 @@ def set_merge_draws(on: bool):
     check(lib().ogcp_ctx_set_option(ctx(), 1, int(bool(on))))
 
 
+def set_buckets(value):
+    """Engine option OGCP_OPT_BUCKETS: False/0 off, True/1 auto, k > 1 force k buckets."""
+    check(lib().ogcp_ctx_set_option(ctx(), 3, int(value)))
+
+
 def set_split_scatter(on: bool):
     """Engine option OGCP_OPT_SPLIT_SCATTER for the current device's context."""
     check(lib().ogcp_ctx_set_option(ctx(), 2, int(bool(on))))

@@ -87,6 +87,13 @@ struct Slice {
   DevBuf hash;              // table_size uint64 linear keys, ~0 = empty
   uint64_t table_mask = 0;
   uint64_t strides[kMaxModes] = {0};
+  // Bucketed copy for merged (count-form) sample sets: positions ordered by
+  // (row bucket of bucket_mode, ordinal), perm[pos] = ordinal, rec_b[pos] =
+  // records[perm[pos]].  A merged set walked in position order touches one
+  // 1/nbuckets slice of the bucket mode's factor and gradient rows at a time,
+  // which then stay L2-resident; within a bucket mode-0 order is kept.
+  int bucket_mode = -1, nbuckets = 0;
+  DevBuf perm, rec_b;
 };
 
 // Per-kernel-class CUDA-event timing on the context stream (bench evidence).
@@ -140,6 +147,8 @@ struct Ctx {
   // c4 it measured 19.2 ms vs 10.2 ms for the fused pass (profiles/), the second
   // pass repeating the gather latency chain without saving enough traffic.
   bool split_scatter = false;
+  bool buckets = true;          // bucketed layout for merged sets of large slices (OGCP_OPT_BUCKETS)
+  int buckets_force = 0;        // > 1: always bucket, with this many buckets (tests)
   DevBuf ybuf;                  // per-sample y of the split scatter
   // multi-GPU: NCCL communicator over the ranks that share one stream of slices
   void* comm = nullptr;         // ncclComm_t

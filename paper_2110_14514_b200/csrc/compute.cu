@@ -29,7 +29,7 @@ constexpr int kThreads = 256;
 #define OGCP_SGRAD_MINB 1
 #endif
 #ifndef OGCP_WGRAD_MINB
-#define OGCP_WGRAD_MINB 1
+#define OGCP_WGRAD_MINB 2
 #endif
 
 template <int D>
@@ -99,7 +99,7 @@ struct SampleStream {
   static constexpr int RI = (D > 0 && D <= 3) ? 4 : 8;
   SamplesP S;
   const ModelP* M;
-  int64_t p, total, stride, b, end;
+  int64_t p, total, b, end;
   int lane, gl, nd;
   int skip = -1;  // mode whose rows are not gathered (split scatter, pass 2)
   int oB[U];
@@ -143,9 +143,22 @@ struct SampleStream {
     }
   }
 
-  // contiguous = true: warp w walks its own contiguous range of samples (keeps
-  // the ordinal order of a merged sample set, so consecutive samples of a group
-  // share mode-0 rows); false: grid-stride batches.
+  // Walk order.  contiguous = true: warp w walks its own contiguous range of
+  // samples (keeps the ordinal order of a merged sample set, so consecutive
+  // samples of a group share mode-0 rows).  Otherwise warps take chunks of
+  // 2^S.chunk_shift batches round-robin (shift 0: plain grid-stride batches), so
+  // the warps in flight stay inside a narrow window of the set -- one row bucket
+  // of a bucketed merged set, whose rows then stay in L2.
+  int64_t lo_, warp_, nwarps_, t_ = 0;
+  int64_t stride_ = 0, b1_ = 0, b2_ = 0;  // unchunked walks: fixed stride, next two batch bases
+  int cshift = 0;
+  bool contig = false;
+  __device__ __forceinline__ int64_t base_of(int64_t t) const {
+    const int64_t chunk = t >> cshift;
+    const int64_t within = t & ((1 << cshift) - 1);
+    return lo_ + (((warp_ + chunk * nwarps_) << cshift) + within) * SPB;
+  }
+
   __device__ __forceinline__ void init(const SamplesP& S_, const ModelP& M_, int lane_, int64_t warp,
                                        int64_t nwarps, bool contiguous = false) {
     S = S_;
@@ -160,15 +173,28 @@ struct SampleStream {
       lo = total * S.shard_rank / S.shard_world;
       hi = total * (S.shard_rank + 1) / S.shard_world;
     }
+    contig = contiguous;
+    warp_ = warp;
+    nwarps_ = nwarps;
     if (contiguous) {
       const int64_t per = ((hi - lo + nwarps - 1) / nwarps + SPB - 1) / SPB * SPB;
       b = lo + warp * per;
       end = min(hi, b + per);
-      stride = SPB;
+      stride_ = SPB;
     } else {
-      stride = nwarps * SPB;
-      b = lo + warp * SPB;
+      lo_ = lo;
+      cshift = S.chunk_shift;
       end = hi;
+      b = base_of(0);
+      stride_ = cshift ? 0 : nwarps * SPB;
+      if (cshift) {
+        b1_ = base_of(1);
+        b2_ = base_of(2);
+      }
+    }
+    if (stride_) {
+      b1_ = b + stride_;
+      b2_ = b + 2 * stride_;
     }
     int o0[U];
     float c0[U];
@@ -176,13 +202,11 @@ struct SampleStream {
     load_rec(b, o0, tC);
 #pragma unroll
     for (int u = 0; u < U; ++u) cC[u] = c0[u];
-    load_ord(b + stride, oB, cB);
+    load_ord(b1_, oB, cB);
   }
 
-  // Issue the row gathers of the current batch (and the next batches' earlier
-  // stages); returns false when the warp has no batch left.
-  __device__ __forceinline__ bool next(Sample<D, V> (&s)[U], bool (&valid)[U]) {
-    if (b >= end) return false;
+  // Fill the per-sample fields of the current batch except the factor rows.
+  __device__ __forceinline__ void meta(Sample<D, V> (&s)[U], bool (&valid)[U]) const {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t n = nidx(b, u);
@@ -200,8 +224,36 @@ struct SampleStream {
       s[u].x = s[u].nz ? x : 0.0f;
       s[u].n = n;
 #pragma unroll
+      for (int k = 0; k < NDm; ++k) s[u].idx[k] = tC[u][k < RI ? k : 0];
+    }
+  }
+
+  // Move the ordinal/record stages one batch forward.
+  __device__ __forceinline__ void advance() {
+    // stage 2 for the next batch, stage 1 for the one after
+    int tB[U][RI];
+    load_rec(b1_, oB, tB);
+#pragma unroll
+    for (int u = 0; u < U; ++u) cC[u] = cB[u];
+    load_ord(b2_, oB, cB);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < RI; ++k) tC[u][k] = tB[u][k];
+    b = b1_;
+    b1_ = b2_;
+    b2_ = stride_ ? b2_ + stride_ : base_of(++t_ + 2);
+  }
+
+  // Issue the row gathers of the current batch (and the next batches' earlier
+  // stages); returns false when the warp has no batch left.
+  __device__ __forceinline__ bool next(Sample<D, V> (&s)[U], bool (&valid)[U]) {
+    if (b >= end) return false;
+    meta(s, valid);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
       for (int k = 0; k < NDm; ++k) {
-        s[u].idx[k] = tC[u][k < RI ? k : 0];
         if (k < nd && k != skip) {
           const float4* row = reinterpret_cast<const float4*>(M->A[k] + (int64_t)s[u].idx[k] * M->ldr);
 #pragma unroll
@@ -213,17 +265,7 @@ struct SampleStream {
         }
       }
     }
-    // stage 2 for the next batch, stage 1 for the one after
-    int tB[U][RI];
-    load_rec(b + stride, oB, tB);
-#pragma unroll
-    for (int u = 0; u < U; ++u) cC[u] = cB[u];
-    load_ord(b + 2 * stride, oB, cB);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int k = 0; k < RI; ++k) tC[u][k] = tB[u][k];
-    b += stride;
+    advance();
     return true;
   }
 };
@@ -357,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, OGCP_SGRAD_MINB) k_sgrad(SamplesP S,
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
   SampleStream<D, G, V, U> stream;
-  stream.init(S, M, lane, warp, nwarps, SEG);
+  stream.init(S, M, lane, warp, nwarps, SEG && S.chunk_shift == 0);
   Sample<D, V> s[U];
   bool valid[U];
   const bool seg0 = SEG && priv_slot[0] < 0;
@@ -450,7 +492,7 @@ __global__ void __launch_bounds__(kThreads) k_sgrad_split(SamplesP S, ModelP M, 
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   SampleStream<D, G, V, U> stream;
   stream.skip = split;
-  stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr);
+  stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr && S.chunk_shift == 0);
   Sample<D, V> s[U];
   bool valid[U];
   while (stream.next(s, valid)) {
@@ -489,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, OGCP_WGRAD_MINB) k_wgrad(SamplesP S,
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
   SampleStream<D, G, V, U> stream;
-  stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr);
+  stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr && S.chunk_shift == 0);
   Sample<D, V> s[U];
   bool valid[U];
   while (stream.next(s, valid)) {
@@ -565,7 +607,7 @@ __global__ void __launch_bounds__(kThreads) k_objective(SamplesP S, ModelP M, co
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned bits = 0;
   SampleStream<D, G, V, U> stream;
-  stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr);
+  stream.init(S, M, lane, warp, nwarps, S.cnt != nullptr && S.chunk_shift == 0);
   Sample<D, V> s[U];
   bool valid[U];
   while (stream.next(s, valid)) {

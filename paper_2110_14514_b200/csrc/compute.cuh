@@ -22,6 +22,7 @@ struct SamplesP {
   const long long* q_dev;   // nullable: lazy zero layout, rows [0, *q_dev) with -1-flagged rows skipped
   int shard_rank, shard_world;  // multi-GPU: this rank evaluates its contiguous 1/world of the samples
   int semi;                 // semi-stratified estimator: nonzero draws use g(x,m) - g(0,m); zero_scale = omega/q
+  int chunk_shift;          // bucketed merged set: warps walk chunks of 2^chunk_shift batches round-robin
 };
 
 struct GradPtrs {

@@ -30,6 +30,7 @@ void segment_layout_impl(Ctx* ctx, const int32_t* coords, int64_t n, int ndim, i
                          int64_t* offsets);
 void slice_contains_impl(Ctx* ctx, const Slice* s, const int64_t* subs, int64_t n, uint8_t* hit);
 void iota_enqueue(Ctx* ctx, int32_t* p, int64_t n);
+void slice_bucket_layout(Ctx* ctx, Slice* X, int mode, int nb);
 
 static thread_local std::string g_last_error;
 
@@ -154,6 +155,7 @@ static SamplesP samples_of(const Slice* X, const int32_t* ord, int64_t p, const 
   S.shard_rank = 0;
   S.shard_world = 1;
   S.semi = 0;
+  S.chunk_shift = 0;
   return S;
 }
 
@@ -242,6 +244,7 @@ struct SampleBufs {
   }
   // Enqueue the draw of this buffer set and return its device sample set.
   SamplesP draw(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t budget, long long code) {
+    md.perm = (merged && ctx->buckets && X->bucket_mode >= 0) ? X->perm.as<int32_t>() : nullptr;
     const DrawOut o = draw_enqueue(ctx, X, g, p, q, budget, merged ? nullptr : ord.as<int32_t>(),
                                    zero.as<int32_t>(), code, scr, merged ? &md : nullptr, /*lazy=*/true, semi);
     zsub = o.zsub;
@@ -259,6 +262,10 @@ SamplesP SampleBufs::sample_set(const Slice* X) const {
   }
   SamplesP S = semi_of(X, samples_of(X, md.ord.as<int32_t>(), p, zsub, q), semi);
   S.q_dev = q_dev;
+  if (md.perm) {  // positions into the bucketed copy, walked in round-robin chunks
+    S.rec = X->rec_b.as<int>();
+    S.chunk_shift = 3;  // 8 batches per chunk (measured flat for shifts 2..6 on c4)
+  }
   S.p = std::min<int64_t>(p, X->nnz);  // upper bound of the distinct count
   S.p_dev = md.count;
   S.cnt = md.cnt.as<uint8_t>();
@@ -271,6 +278,33 @@ static bool use_merged(const Ctx* ctx, const Slice* X, int64_t p) {
   // 4-bit counters: with p <= 1.25 eta a counter reaches 16 with probability
   // ~5e-13 per ordinal; the count-sum check catches it and the epoch is redone.
   return ctx->merge_draws && X->nnz >= 65536 && p >= X->nnz / 8 && p <= X->nnz + X->nnz / 4;
+}
+
+// Bucketed layout for merged sets (Slice::perm): the largest mode k >= 1 whose
+// factor + gradient rows (2 dims[k] ldr 4 B) exceed 48 MB is cut into
+// power-of-two row buckets of <= 32 MB, so each bucket's rows stay L2-resident
+// while the set's positions inside it are walked.  Built once per slice.
+static void prepare_buckets(Ctx* ctx, const Slice* Xc, int ldr) {
+  Slice* X = const_cast<Slice*>(Xc);
+  if (!ctx->buckets || X->ndim < 2) return;
+  int mode = -1;
+  double ws = 0.0;
+  for (int k = 1; k < X->ndim; ++k) {
+    const double w = 2.0 * (double)X->dims[k] * ldr * 4.0;
+    if (w > ws) {
+      ws = w;
+      mode = k;
+    }
+  }
+  int nb = 2;
+  if (ctx->buckets_force > 1) {
+    nb = ctx->buckets_force;
+  } else {
+    if (ws <= 48e6) return;
+    while (nb < 256 && ws / nb > 32e6) nb <<= 1;
+  }
+  if (X->bucket_mode == mode && X->nbuckets == nb) return;
+  slice_bucket_layout(ctx, X, mode, nb);
 }
 
 // Synchronous draw with shortfall retry (used for objective sets).
@@ -411,6 +445,7 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     So = sharded(ctx, obj.sample_set(X));
     precheck_draw(X, p, semi ? 0 : q);
     grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+    if (grad.merged) prepare_buckets(ctx, X, M.ldr);
     grad.semi = semi;
     budget = budget_of(q, cfg->samples.max_rejects);
   }
@@ -743,6 +778,7 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     So = sharded(ctx, W.obj.sample_set(X));
     precheck_draw(X, p, semi ? 0 : q);
     W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+    if (W.grad.merged) prepare_buckets(ctx, X, M.ldr);
     W.grad.semi = semi;
     budget = budget_of(q, cfg->samples.max_rejects);
   }
@@ -855,6 +891,7 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
     So = sharded(ctx, W.obj.sample_set(X));
     precheck_draw(X, p, semi ? 0 : q);
     W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+    if (W.grad.merged) prepare_buckets(ctx, X, M.ldr);
     W.grad.semi = semi;
     budget = budget_of(q, cfg->samples.max_rejects);
   }
@@ -1200,6 +1237,10 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   OGCP_API_BEGIN
   if (option == OGCP_OPT_MERGE_DRAWS) ctx->merge_draws = value != 0;
   else if (option == OGCP_OPT_SPLIT_SCATTER) ctx->split_scatter = value != 0;
+  else if (option == OGCP_OPT_BUCKETS) {
+    ctx->buckets = value != 0;
+    ctx->buckets_force = value > 1 ? (int)std::min<int64_t>(value, 256) : 0;
+  }
   else throw Error(OGCP_E_USAGE, "unknown option");
   OGCP_API_END
 }

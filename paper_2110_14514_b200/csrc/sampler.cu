@@ -729,6 +729,31 @@ __global__ void __launch_bounds__(kScanThreads) k_hist_write(const uint32_t* __r
   (void)eta;
 }
 
+// Gather the ordinal-indexed counters into position order (perm[pos] = ordinal):
+// one output word = 8 consecutive positions; the counter reads are random but
+// hit the L2-resident histogram.
+__global__ void k_hist_permute(const uint32_t* __restrict__ hist, const int32_t* __restrict__ perm, int64_t eta,
+                               int64_t nwords, uint32_t* __restrict__ pnib) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p0 = w * 8;
+    int32_t o[8];
+    if (p0 + 8 <= eta) {
+      const int4 a = __ldg(reinterpret_cast<const int4*>(perm + p0));
+      const int4 b = __ldg(reinterpret_cast<const int4*>(perm + p0) + 1);
+      o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+      o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = p0 + j < eta ? __ldg(perm + p0 + j) : -1;
+    }
+    uint32_t out = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (o[j] >= 0) out |= ((__ldg(hist + (o[j] >> 3)) >> (4 * (o[j] & 7))) & 0xfu) << (4 * j);
+    pnib[w] = out;
+  }
+}
+
 template <int NCOL>
 static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int64_t target, int64_t words,
                        int32_t* out, long long* end_word, long long* elems_total, DrawScratch& scr,
@@ -817,18 +842,26 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
         merged->cnt.ensure((size_t)std::min(p, eta));
         OGCP_CUDA(cudaMemsetAsync(merged->hist.ptr, 0, (size_t)nwords * 4, s));
         run_stream<1>(ctx, sp, nullptr, p, words, nullptr, nz_end, nz_avail, scr, merged->hist.as<uint32_t>());
+        const uint32_t* counters = merged->hist.as<uint32_t>();
+        if (merged->perm) {  // emit in the slice's bucketed position order
+          merged->pnib.ensure((size_t)nwords * 4);
+          k_hist_permute<<<std::min<int64_t>((nwords + 255) / 256, kNumSMs * 16), 256, 0, s>>>(
+              counters, merged->perm, eta, nwords, merged->pnib.as<uint32_t>());
+          ctx->count();
+          counters = merged->pnib.as<uint32_t>();
+        }
         const int64_t hblocks = (nwords + (int64_t)kHistWordsPerThread * kScanThreads - 1) /
                                 ((int64_t)kHistWordsPerThread * kScanThreads);
         merged->bcount.ensure((size_t)hblocks * 4);
         merged->boff.ensure((size_t)hblocks * 8);
         unsigned long long* cnt_sum = reinterpret_cast<unsigned long long*>(sc + 7);
-        k_hist_count<<<(unsigned)hblocks, kScanThreads, 0, s>>>(merged->hist.as<uint32_t>(), nwords,
-                                                                merged->bcount.as<uint32_t>(), cnt_sum);
+        k_hist_count<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, merged->bcount.as<uint32_t>(),
+                                                                cnt_sum);
         k_hist_verify<<<1, 32, 0, s>>>(cnt_sum, (long long)p, ctx->flags.as<DevFlags>());
         ctx->count();
         k_zero_scan<<<1, 1024, 0, s>>>(merged->bcount.as<uint32_t>(), hblocks, merged->boff.as<long long>(),
                                        sc + 5);
-        k_hist_write<<<(unsigned)hblocks, kScanThreads, 0, s>>>(merged->hist.as<uint32_t>(), nwords, eta,
+        k_hist_write<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, eta,
                                                                 merged->boff.as<long long>(),
                                                                 merged->ord.as<int32_t>(), merged->cnt.as<uint8_t>());
         ctx->count(3);

@@ -11,9 +11,12 @@ struct DrawScratch {
 // order with their multiplicities (uint8; callers keep p <= 8*eta so a count
 // cannot reach 256 with any realistic probability) and the distinct count on
 // the device.
+// perm (nullable): the slice's bucketed order (Slice::perm); the set is then
+// emitted in position order -- ord holds positions into Slice::rec_b.
 struct MergedDraw {
-  DevBuf hist, ord, cnt, bcount, boff;
+  DevBuf hist, ord, cnt, bcount, boff, pnib;
   long long* count = nullptr;
+  const int32_t* perm = nullptr;
 };
 
 void init_jump_table();

@@ -111,6 +111,53 @@ void iota_enqueue(Ctx* ctx, int32_t* p, int64_t n) {
   check_launch();
 }
 
+// ---------------------------------------------------------- bucketed layout
+__global__ void k_bucket_keys(const int* __restrict__ rec, int rec_ints, int mode, long long dim, int nb, int64_t n,
+                              uint8_t* __restrict__ keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = (uint8_t)(((long long)rec[i * rec_ints + mode] * nb) / dim);
+}
+
+__global__ void k_gather_records(const int4* __restrict__ rec, int vec_per_rec, const int32_t* __restrict__ perm,
+                                 int64_t n, int4* __restrict__ out) {
+  const int64_t total = n * vec_per_rec;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / vec_per_rec;
+    const int v = (int)(e - i * vec_per_rec);
+    out[e] = __ldg(rec + (int64_t)__ldg(perm + i) * vec_per_rec + v);
+  }
+}
+
+void slice_bucket_layout(Ctx* ctx, Slice* X, int mode, int nb) {
+  const int64_t n = X->nnz;
+  cudaStream_t s = ctx->stream;
+  int bits = 0;
+  while ((1 << bits) < nb) ++bits;
+  DevBuf keys, keys_s, iota, cub_tmp;
+  keys.ensure(n);
+  keys_s.ensure(n);
+  iota.ensure(n * 4);
+  X->perm.ensure(n * 4);
+  X->rec_b.ensure((size_t)n * X->rec_ints * 4);
+  k_bucket_keys<<<grid_for(n), 256, 0, s>>>(X->records.as<int>(), X->rec_ints, mode, (long long)X->dims[mode], nb, n,
+                                            keys.as<uint8_t>());
+  k_iota32<<<grid_for(n), 256, 0, s>>>(iota.as<int32_t>(), n);
+  size_t tb = 0;
+  OGCP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint8_t>(), keys_s.as<uint8_t>(),
+                                            iota.as<int32_t>(), X->perm.as<int32_t>(), (int)n, 0, bits, s));
+  cub_tmp.ensure(tb);
+  OGCP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp.ptr, tb, keys.as<uint8_t>(), keys_s.as<uint8_t>(),
+                                            iota.as<int32_t>(), X->perm.as<int32_t>(), (int)n, 0, bits, s));
+  const int vpr = X->rec_ints / 4;
+  k_gather_records<<<grid_for(n * vpr), 256, 0, s>>>(reinterpret_cast<const int4*>(X->records.ptr), vpr,
+                                                     X->perm.as<int32_t>(), n, reinterpret_cast<int4*>(X->rec_b.ptr));
+  ctx->count(4);
+  check_launch();
+  OGCP_CUDA(cudaStreamSynchronize(s));  // scratch buffers are released on return
+  X->bucket_mode = mode;
+  X->nbuckets = nb;
+}
+
 struct YScratch {
   DevBuf keys, keys_s, idx, idx_s, coords, y, head, pos, cub, bad, cols, cols_s;
 };
