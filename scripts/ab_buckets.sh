@@ -1,8 +1,6 @@
-# A/B of the bucketed merged walk on the c4 bench (per-kernel ms per launch)
-python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-for cfg in "OGCP_BUCKETS=1" "OGCP_BUCKETS=0"; do
-  env $cfg python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab.json 2> gpurun_out/ab.err
+for lib in libogcp_b200 libogcp_b200_s1 libogcp_b200_s2; do
+  OGCP_LIB=paper_2110_14514_b200/$lib.so python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab.json 2> gpurun_out/ab.err
   python -c "
 import json; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); k=d['kernel_ms']; n=d['kernel_launch_brackets']
-print('$cfg', round(d['value']/1e9,3), {c: round(k[c]/max(n[c],1),3) for c in k})"
+print('$lib', round(d['value']/1e9,3), {c: round(k[c]/max(n[c],1),3) for c in k})"
 done
