@@ -1091,7 +1091,7 @@ static void dispatch_layout(Layout kind, int ndim, int ldr, F&& f) {
         case 4: f(Dc, IC<1>(), IC<1>(), IC<2>()); break;
         case 8: f(Dc, IC<2>(), IC<1>(), IC<2>()); break;
         case 16: f(Dc, IC<4>(), IC<1>(), IC<2>()); break;
-        case 32: f(Dc, IC<4>(), IC<2>(), IC<2>()); break;
+        case 32: f(Dc, IC<4>(), IC<2>(), IC<2>()); break;  // measured best of (4,2,1) (2,4,1) (8,1,2) on c4
         case 64: f(Dc, IC<8>(), IC<2>(), IC<2>()); break;
         case 128: f(Dc, IC<16>(), IC<2>(), IC<2>()); break;
         case 256: f(Dc, IC<32>(), IC<2>(), IC<1>()); break;

@@ -1,3 +1,4 @@
+#include <chrono>
 // Native runtime of the engine: context, slices, the per-slice solvers and
 // the extern "C" boundary declared in include/ogcp_b200.h.
 //
@@ -33,6 +34,35 @@ void iota_enqueue(Ctx* ctx, int32_t* p, int64_t n);
 void slice_bucket_layout(Ctx* ctx, Slice* X, int mode, int nb);
 
 static thread_local std::string g_last_error;
+
+cudaStream_t alloc_stream() {
+  static thread_local cudaStream_t st = [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    return s;
+  }();
+  return st;
+}
+
+// OGCP_DEBUG_TIMING=1: host wall time of the named scope on stderr (diagnostics only)
+struct DbgTimer {
+  const char* name;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit DbgTimer(const char* n) : name(n) {}
+  ~DbgTimer() {
+    static const bool on = getenv("OGCP_DEBUG_TIMING") != nullptr;
+    if (on)
+      fprintf(stderr, "[timing] %s %.1f ms\n", name,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
 
 static const char* kind_name(int k) {
   return k == OGCP_GAUSSIAN ? "gaussian" : (k == OGCP_POISSON ? "poisson" : "bernoulli");
@@ -304,12 +334,17 @@ static void prepare_buckets(Ctx* ctx, const Slice* Xc, int ldr) {
     while (nb < 256 && ws / nb > 32e6) nb <<= 1;
   }
   if (X->bucket_mode == mode && X->nbuckets == nb) return;
+  const auto t0 = std::chrono::steady_clock::now();
   slice_bucket_layout(ctx, X, mode, nb);
+  if (getenv("OGCP_DEBUG_TIMING"))
+    fprintf(stderr, "bucket layout %.1f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
 }
 
 // Synchronous draw with shortfall retry (used for objective sets).
 static void draw_sync(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t max_rejects,
                       SampleBufs& b, bool semi = false) {
+  DbgTimer dt("draw_sync");
   precheck_draw(X, p, semi ? 0 : q);
   b.size(p, q, X->ndim);
   b.semi = semi;
@@ -1599,6 +1634,7 @@ int ogcp_adam_update(ogcp_ctx* ctx, const ogcp_model* m, ogcp_adam_state* st, in
 int ogcp_solve_weights(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_config* cfg, const ogcp_loss* loss,
                        int64_t t, const ogcp_model* m, const double* s_init, double* s_out, ogcp_trace* trace) {
   OGCP_API_BEGIN
+  DbgTimer dt("solve_weights");
   solve_weights_impl(ctx, s, cfg, loss, t, m, s_init, s_out, trace);
   OGCP_API_END
 }
@@ -1608,6 +1644,7 @@ int ogcp_solve_factors(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_con
                        const double* window_s, const int64_t* window_ids, int32_t H, ogcp_adam_state* adam,
                        int64_t* iteration, ogcp_trace* trace) {
   OGCP_API_BEGIN
+  DbgTimer dt("solve_factors");
   solve_factors_impl(ctx, s, cfg, loss, t, m, old_factors, weights, window_s, window_ids, H, adam, iteration, trace);
   OGCP_API_END
 }
@@ -1625,6 +1662,7 @@ int ogcp_local_loss(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_model* m, con
                     const ogcp_loss* loss, int32_t mode, int64_t p, int64_t q, uint64_t seed, const int64_t* key,
                     int32_t nkey, int64_t max_rejects, int64_t max_elements, double* out, int32_t* normalized) {
   OGCP_API_BEGIN
+  DbgTimer dt("local_loss");
   ModelP M = model_of(m);
   if (M.ndim != s->ndim) throw Error(OGCP_E_DATA, "dims differ");
   for (int k = 0; k < M.ndim; ++k)

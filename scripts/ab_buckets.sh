@@ -1,4 +1,4 @@
-for lib in libogcp_b200 libogcp_b200_s1 libogcp_b200_s2; do
+for lib in libogcp_b200 libogcp_b200_r1 libogcp_b200_r2 libogcp_b200_r3 libogcp_b200_r1m3; do
   OGCP_LIB=paper_2110_14514_b200/$lib.so python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab.json 2> gpurun_out/ab.err
   python -c "
 import json; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); k=d['kernel_ms']; n=d['kernel_launch_brackets']
