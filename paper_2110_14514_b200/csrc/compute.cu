@@ -683,6 +683,16 @@ __global__ void k_sum_partials_vec(const double* __restrict__ p, int nblk, int l
 // (gram, 4x4 sub-block); a thread accumulates its sub-blocks over a row group
 // in fp32 per 32-row tile and in fp64 across tiles; row groups are reduced in
 // fixed order in shared memory, blocks by the finalize kernel.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 constexpr int kGramTile = 32;
 constexpr int kGramIPT = 2;
 __global__ void __launch_bounds__(kThreads) k_gram2(const float* __restrict__ A, const float* __restrict__ B,
@@ -690,7 +700,6 @@ __global__ void __launch_bounds__(kThreads) k_gram2(const float* __restrict__ A,
                                                     int64_t rows_per_block, double* __restrict__ partials) {
   extern __shared__ __align__(16) unsigned char gsm[];
   float* sa = reinterpret_cast<float*>(gsm);
-  float* sb = sa + kGramTile * ldr;
   const int nsb = ldr / 4;
   const int nsub = nsb * nsb;
   const int nitems = ngram * nsub;
@@ -721,25 +730,39 @@ __global__ void __launch_bounds__(kThreads) k_gram2(const float* __restrict__ A,
   const int64_t r0 = blockIdx.x * rows_per_block;
   const int64_t r1 = min(rows, r0 + rows_per_block);
   const bool has_b = ngram > 1;
-  for (int64_t rb = r0; rb < r1; rb += kGramTile) {
+  // double-buffered tiles: the cp.async copy of tile k+1 overlaps the FMAs on tile k
+  const int tile_f = kGramTile * ldr;
+  auto stage = [&](int64_t rb, int buf) {
     const int nr = (int)min((int64_t)kGramTile, r1 - rb);
-    __syncthreads();
     const int nv = nr * ldr / 4;
+    float4* da = reinterpret_cast<float4*>(sa + buf * 2 * tile_f);
+    float4* db = reinterpret_cast<float4*>(sa + buf * 2 * tile_f + tile_f);
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-      reinterpret_cast<float4*>(sa)[i] = __ldg(reinterpret_cast<const float4*>(A + rb * ldr) + i);
-      if (has_b) reinterpret_cast<float4*>(sb)[i] = __ldg(reinterpret_cast<const float4*>(B + rb * ldr) + i);
+      cp_async16(da + i, reinterpret_cast<const float4*>(A + rb * ldr) + i);
+      if (has_b) cp_async16(db + i, reinterpret_cast<const float4*>(B + rb * ldr) + i);
     }
+  };
+  if (r0 < r1) stage(r0, 0);
+  cp_async_commit();
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += kGramTile, buf ^= 1) {
+    const int nr = (int)min((int64_t)kGramTile, r1 - rb);
+    if (rb + kGramTile < r1) stage(rb + kGramTile, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
+    const float* ta = sa + buf * 2 * tile_f;
+    const float* tb = ta + tile_f;
 #pragma unroll
     for (int t = 0; t < kGramIPT; ++t) {
       if (!on[t]) continue;
       float acc[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-      const float* lhs = gi[t] == 0 ? sa : sb;
+      const float* lhs = gi[t] == 0 ? ta : tb;
       for (int r = rg; r < nr; r += nrg) {
         const float4 l = reinterpret_cast<const float4*>(lhs + r * ldr)[bi[t]];
-        const float4 a = reinterpret_cast<const float4*>(sa + r * ldr)[bj[t]];
+        const float4 a = reinterpret_cast<const float4*>(ta + r * ldr)[bj[t]];
         const float lv[4] = {l.x, l.y, l.z, l.w};
         const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
@@ -750,6 +773,7 @@ __global__ void __launch_bounds__(kThreads) k_gram2(const float* __restrict__ A,
 #pragma unroll
       for (int e = 0; e < 16; ++e) dacc[t][e] += (double)acc[e];
     }
+    __syncthreads();  // this buffer is refilled by the next iteration's stage
   }
   // reduce row groups in fixed order through shared memory
   __syncthreads();
@@ -1288,7 +1312,7 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
   const int64_t rpb = (rows + nblk - 1) / nblk;
   nblk = (int)std::max<int64_t>(1, (rows + rpb - 1) / rpb);
   scratch.ensure((size_t)nblk * ngram * ldr * ldr * 8);
-  size_t smem = (size_t)2 * kGramTile * ldr * 4;
+  size_t smem = (size_t)4 * kGramTile * ldr * 4;  // two buffers x (A tile, B tile)
   smem = std::max(smem, (size_t)kThreads * 16 * 8);
   if (smem > 48 * 1024)
     OGCP_CUDA(cudaFuncSetAttribute(k_gram2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

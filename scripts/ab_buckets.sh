@@ -1,5 +1,5 @@
 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
-for lib in libogcp_b200 libogcp_b200_u8 libogcp_b200_r2m4 libogcp_b200_r8m2 libogcp_b200_u8m4; do
+for lib in libogcp_b200; do
   OGCP_LIB=paper_2110_14514_b200/$lib.so python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab.json 2> gpurun_out/ab.err
   python -c "
 import json; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); k=d['kernel_ms']; n=d['kernel_launch_brackets']
