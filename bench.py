@@ -354,7 +354,12 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgrad (K2+K3 fused eval/scatter)",
                          "algorithmic_bytes_per_launch": sg_bytes, "avg_launch_ms": sg_ms,
                          "bytes_model": "B_f = 8dR+4d+4 = 784 B per entry of the merged gradient tensor Y; "
-                                        f"|Y| = {y_entries:.4g} (distinct nonzero draws + zero draws)"},
+                                        f"|Y| = {y_entries:.4g} (distinct nonzero draws + zero draws)",
+                         # measured DRAM bytes (ncu, profiles/traffic.json) over this run's launch time: the
+                         # row-bucketed walk serves most row gathers/reductions from L2, so frac > 1 on the
+                         # algorithmic model while the HBM itself runs at dram_frac
+                         "dram_gbs": (traffic / (sg_ms / 1000.0) / 1e9) if traffic else None,
+                         "dram_frac": (traffic / (sg_ms / 1000.0) / 1e9 / peak) if traffic else None},
             "kernel_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
             "kernel_launch_brackets": {k: v["launches"] for k, v in prof.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,

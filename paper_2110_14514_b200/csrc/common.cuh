@@ -98,6 +98,11 @@ struct Slice {
   DevBuf records;           // nnz * rec_ints int32
   DevBuf hash;              // table_size uint64 linear keys, ~0 = empty
   uint64_t table_mask = 0;
+  // Prefilter for large slices: one bit per filter_bit(mix64(key)); a clear bit
+  // proves absence without touching the (DRAM-resident) table.  <= 32 MB so it
+  // stays in L2 while the zero candidates are probed.
+  DevBuf filter;
+  uint64_t filter_mask = 0;  // 0: no prefilter
   uint64_t strides[kMaxModes] = {0};
   // Bucketed copy for merged (count-form) sample sets: positions ordered by
   // (row bucket of bucket_mode, ordinal), perm[pos] = ordinal, rec_b[pos] =

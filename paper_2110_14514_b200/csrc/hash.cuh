@@ -37,6 +37,10 @@ __device__ __forceinline__ bool hash_insert(unsigned long long* table, uint64_t 
   }
 }
 
+// Bit of the membership prefilter (a one-hash Bloom bitmap over the same keys):
+// the high half of the mixed key, independent of the table's low-bit slot.
+__device__ __forceinline__ uint64_t filter_bit(uint64_t h, uint64_t fmask) { return (h >> 32) & fmask; }
+
 __device__ __forceinline__ bool hash_contains(const unsigned long long* __restrict__ table, uint64_t mask,
                                               uint64_t key) {
   uint64_t slot = mix64(key) & mask;

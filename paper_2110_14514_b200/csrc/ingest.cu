@@ -67,13 +67,17 @@ __global__ void k_ingest(int ndim, int64_t nnz, const CT* __restrict__ subs, con
 
 __global__ void k_hash_insert(int ndim, int64_t nnz, const int* __restrict__ rec, int rec_ints,
                               Strides st, unsigned long long* __restrict__ table, uint64_t mask,
-                              IngestOut* out) {
+                              IngestOut* out, unsigned int* __restrict__ filter, uint64_t fmask) {
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < nnz;
        n += (int64_t)gridDim.x * blockDim.x) {
     const int* r = rec + n * rec_ints;
     uint64_t key = 0;
     for (int k = 0; k < ndim; ++k) key += (uint64_t)(uint32_t)r[k] * st.s[k];
     if (!hash_insert(table, mask, key)) atomicMin(&out->dup_key, (unsigned long long)key);
+    if (filter) {
+      const uint64_t b = filter_bit(mix64(key), fmask);
+      atomicOr(filter + (b >> 5), 1u << (b & 31));
+    }
   }
 }
 
@@ -178,9 +182,21 @@ Slice* slice_create_impl(Ctx* ctx, int ndim, const int64_t* dims, int64_t nnz, c
     s->x_negative = res.negative != 0;
     s->x_nonbinary = res.nonbinary != 0;
     if (nnz > 0) {
+      s->filter_mask = 0;
+      // prefilter: >= 4 bits per key, at most 2^28 bits (32 MB; c4: 1e8 keys -> 31% of the
+      // absent candidates still reach the table, draw 1.77 -> 1.60 ms)
+      if (nnz >= (int64_t)1 << 20) {
+        uint64_t fbits = 1 << 20;
+        while (fbits < 4 * (uint64_t)nnz && fbits < ((uint64_t)1 << 28)) fbits <<= 1;
+        s->filter.ensure(fbits / 8);
+        OGCP_CUDA(cudaMemsetAsync(s->filter.ptr, 0, fbits / 8, str));
+        s->filter_mask = fbits - 1;
+      }
       k_hash_insert<<<blocks, threads, 0, str>>>(ndim, nnz, s->records.as<int>(), s->rec_ints, ss,
                                                  s->hash.as<unsigned long long>(), s->table_mask,
-                                                 scratch.as<IngestOut>());
+                                                 scratch.as<IngestOut>(),
+                                                 s->filter_mask ? s->filter.as<unsigned int>() : nullptr,
+                                                 s->filter_mask);
       ctx->count();
       check_launch();
       OGCP_CUDA(cudaMemcpyAsync(&res, scratch.ptr, sizeof(res), cudaMemcpyDeviceToHost, str));

@@ -377,7 +377,8 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_hits(ZeroSpec zs, const i
                                                             uint64_t mask, uint8_t* __restrict__ miss,
                                                             uint32_t* __restrict__ bcount, int64_t q,
                                                             unsigned long long* __restrict__ hit_in_q,
-                                                            int mark_hits) {
+                                                            int mark_hits, const unsigned int* __restrict__ filter,
+                                                            uint64_t fmask) {
   const int64_t rows = zero_rows_avail(zs, elems_avail, rows_max);
   const int64_t t = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
   const int64_t r0 = t * kRowsPerThread;
@@ -397,8 +398,19 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_hits(ZeroSpec zs, const i
       }
   }
 #pragma unroll
-  for (int j = 0; j < kRowsPerThread; ++j)
-    if (live[j] && !(table && hash_contains(table, mask, key[j]))) bits |= 1u << j;
+  for (int j = 0; j < kRowsPerThread; ++j) {
+    if (!live[j]) continue;
+    bool present = false;
+    if (table) {
+      present = true;
+      if (filter) {  // a clear prefilter bit proves absence (L2-resident bitmap)
+        const uint64_t b = filter_bit(mix64(key[j]), fmask);
+        present = (__ldg(filter + (b >> 5)) >> (b & 31)) & 1u;
+      }
+      if (present) present = hash_contains(table, mask, key[j]);
+    }
+    if (!present) bits |= 1u << j;
+  }
   if (r0 < rows_max) miss[t] = (uint8_t)bits;
   if (hit_in_q) {  // any of the first q candidate rows not a miss -> the slow (compacting) path
     bool hit = false;
@@ -955,7 +967,9 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
         (in_place && !lazy) ? reinterpret_cast<unsigned long long*>(sc + 6) : nullptr;
     k_zero_hits<<<(unsigned)zblocks, kScanThreads, 0, s>>>(zs, scr.cand.as<int32_t>(), z_elems, rows_max, table,
                                                            X->table_mask, scr.miss.as<uint8_t>(),
-                                                           scr.zcount.as<uint32_t>(), q, hit_in_q, mark ? 1 : 0);
+                                                           scr.zcount.as<uint32_t>(), q, hit_in_q, mark ? 1 : 0,
+                                                           X->filter_mask ? X->filter.as<unsigned int>() : nullptr,
+                                                           X->filter_mask);
     k_zero_scan<<<1, 1024, 0, s>>>(scr.zcount.as<uint32_t>(), zblocks, scr.zoff.as<long long>(), z_misses);
     ctx->count(2);
     if (mark) {
