@@ -270,73 +270,6 @@ struct SampleStream {
   }
 };
 
-// (unpipelined variant kept for reference-shaped small launches)
-template <int D, int G, int V, int U>
-__device__ __forceinline__ void gather_batch(int64_t base, int64_t total, const SamplesP& S, const ModelP& M,
-                                             int lane, Sample<D, V> (&s)[U], bool (&valid)[U]) {
-  constexpr int NDm = ND<D>::v;
-  constexpr int SPW = 32 / G;
-  const int nd = D > 0 ? D : M.ndim;
-  const int gl = lane & (G - 1);
-  int64_t n[U];
-  int o[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    n[u] = base + u * SPW + lane / G;
-    valid[u] = n[u] < total;
-    s[u].nz = valid[u] && n[u] < S.p;
-    o[u] = s[u].nz ? __ldg(S.ord + n[u]) : 0;
-  }
-  int t[U][8];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t[u][k] = 0;
-    s[u].x = 0.0f;
-    s[u].scale = 0.0f;
-    if (s[u].nz) {
-      const int4* r = reinterpret_cast<const int4*>(S.rec + (int64_t)o[u] * S.rec_ints);
-      int4 v0 = __ldg(r);
-      t[u][0] = v0.x; t[u][1] = v0.y; t[u][2] = v0.z; t[u][3] = v0.w;
-      if (D == 0 || D > 3) {
-        if (S.rec_ints == 8) {
-          int4 v1 = __ldg(r + 1);
-          t[u][4] = v1.x; t[u][5] = v1.y; t[u][6] = v1.z; t[u][7] = v1.w;
-        }
-      }
-      if (D > 0) s[u].x = __int_as_float(t[u][D]);
-      else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (k == nd) s[u].x = __int_as_float(t[u][k]);
-      }
-      s[u].scale = (float)S.nz_scale;
-    } else if (valid[u]) {
-      const int32_t* z = S.zsub + (n[u] - S.p) * nd;
-#pragma unroll
-      for (int k = 0; k < NDm; ++k)
-        if (k < nd) t[u][k] = __ldg(z + k);
-      s[u].scale = (float)S.zero_scale;
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-#pragma unroll
-    for (int k = 0; k < NDm; ++k) {
-      s[u].idx[k] = t[u][k];
-      if (k < nd) {
-        const float4* row = reinterpret_cast<const float4*>(M.A[k] + (int64_t)t[u][k] * M.ldr);
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-          s[u].a[k][v] = valid[u] ? __ldg(row + v * G + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
-#pragma unroll
-        for (int v = 0; v < V; ++v) s[u].a[k][v] = make_float4(1.f, 1.f, 1.f, 1.f);
-      }
-    }
-  }
-}
-
 template <int D, int G, int V>
 __device__ __forceinline__ float model_value(const Sample<D, V>& s, const float4* s4) {
   constexpr int NDm = ND<D>::v;
