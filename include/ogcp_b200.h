@@ -151,7 +151,11 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * random-access mode in row-bucket order (Slice bucketed copy, built once per
  * slice) so the bucket's factor/gradient rows stay L2-resident; a value k > 1
  * forces k buckets on every merged solve (tests). */
-enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 3 };
+/* OGCP_OPT_SHARD_SIM: value = rank | world << 16 on a context without a
+ * communicator -- the solves then run rank `rank`'s share of a world-`world`
+ * multi-GPU solve with the collectives skipped (single-process tests of the
+ * shard partition); world 1 (or 0) restores the single-GPU context. */
+enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 3, OGCP_OPT_SHARD_SIM = 4 };
 int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value);
 
 /* Multi-GPU (the reference is single-process): the
@@ -300,6 +304,14 @@ int ogcp_dense_gaussian_gradients(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp
                                   const int64_t* window_ids, int32_t H, double hist_weight, double hist_decay,
                                   int64_t t, double reg_factors, double reg_weights, float* const* grads_dev,
                                   double* weight_grad);
+
+/* Diagnostics: the gradient sample set a solve iteration would evaluate on
+ * this context (merged/bucketed form and multi-GPU share included), keyed
+ * rng_at(seed, *key): this rank's nonzero ordinals with multiplicities and its
+ * accepted zero rows.  Used by the tests of the shard partition. */
+int ogcp_debug_solve_draw(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const int64_t* key, int32_t nkey,
+                          int64_t p, int64_t q, int64_t max_rejects, int32_t ldr, int64_t cap_nz, int32_t* ord_out,
+                          uint8_t* cnt_out, int64_t* n_nz, int64_t cap_zero, int32_t* zero_out, int64_t* n_zero);
 
 /* local_loss (metrics.py:36-70): mode 0 exact (every cell, <= max_elements),
  * mode 1 sampled on rng_at(seed, *key) with (p, q) (p < 0: all nonzeros).

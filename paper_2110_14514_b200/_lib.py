@@ -126,6 +126,9 @@ _SIGS = {
     "ogcp_dense_gaussian_gradients": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(ModelC), C.POINTER(C.c_void_p),
                                                 c_f64p, c_f64p, c_i64p, C.c_int32, C.c_double, C.c_double,
                                                 C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_void_p), c_f64p]),
+    "ogcp_debug_solve_draw": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, c_i64p, C.c_int32, C.c_int64, C.c_int64,
+                                        C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, c_i64p, C.c_int64,
+                                        C.c_void_p, c_i64p]),
     "ogcp_local_loss": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(ModelC), c_f64p, C.POINTER(LossC), C.c_int32,
                                   C.c_int64, C.c_int64, C.c_uint64, c_i64p, C.c_int32, C.c_int64, C.c_int64, c_f64p,
                                   C.POINTER(C.c_int32)]),
@@ -237,6 +240,27 @@ def set_merge_draws(on: bool):
 def set_buckets(value):
     """Engine option OGCP_OPT_BUCKETS: False/0 off, True/1 auto, k > 1 force k buckets."""
     check(lib().ogcp_ctx_set_option(ctx(), 3, int(value)))
+
+
+def set_shard_sim(rank: int, world: int):
+    """OGCP_OPT_SHARD_SIM: run this context as rank `rank` of `world` without a communicator (tests)."""
+    check(lib().ogcp_ctx_set_option(ctx(), 4, int(rank) | (int(world) << 16)))
+
+
+def debug_solve_draw(X, seed: int, key, p, q: int, ldr: int, max_rejects=None):
+    """(ordinals, multiplicities, zero rows) of the gradient sample set a solve iteration evaluates here."""
+    p = -1 if p is None else int(p)
+    cap_nz = max(X.nnz, 1)
+    ords = np.zeros(cap_nz, np.int32)
+    cnts = np.zeros(cap_nz, np.uint8)
+    zeros = np.zeros((max(q, 1), X.ndim), np.int32)
+    nn, nz = C.c_int64(), C.c_int64()
+    k = np.ascontiguousarray(np.asarray(key, np.int64))
+    check(lib().ogcp_debug_solve_draw(ctx(), X._handle, int(seed), k.ctypes.data_as(c_i64p), len(k), p, int(q),
+                                      -1 if max_rejects is None else int(max_rejects), int(ldr), cap_nz,
+                                      ords.ctypes.data, cnts.ctypes.data, C.byref(nn), max(q, 1), zeros.ctypes.data,
+                                      C.byref(nz)))
+    return ords[:nn.value].astype(np.int64), cnts[:nn.value].astype(np.int64), zeros[:nz.value].astype(np.int64)
 
 
 def set_split_scatter(on: bool):

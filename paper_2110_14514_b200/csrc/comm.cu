@@ -73,18 +73,19 @@ __global__ void k_flags_unpack(DevFlags* f, const long long* pk) {
 
 }  // namespace
 
+// (no communicator with world > 1: single-process shard simulation, sums are the caller's)
 void comm_allreduce_sum(Ctx* ctx, float* p, size_t n) {
-  if (ctx->world <= 1 || n == 0) return;
+  if (ctx->world <= 1 || n == 0 || !ctx->comm) return;
   nccl_check(api().AllReduce(p, p, n, ncclFloat32, ncclSum, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");
 }
 
 void comm_allreduce_sum(Ctx* ctx, double* p, size_t n) {
-  if (ctx->world <= 1 || n == 0) return;
+  if (ctx->world <= 1 || n == 0 || !ctx->comm) return;
   nccl_check(api().AllReduce(p, p, n, ncclFloat64, ncclSum, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");
 }
 
 void comm_sync_flags(Ctx* ctx) {
-  if (ctx->world <= 1) return;
+  if (ctx->world <= 1 || !ctx->comm) return;
   long long* pk = static_cast<long long*>(ctx->flagpack.ensure(8 * sizeof(long long)));
   k_flags_pack<<<1, 1, 0, ctx->stream>>>(ctx->flags.as<DevFlags>(), pk);
   nccl_check(api().AllReduce(pk, pk, 4, ncclInt64, ncclMin, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");

@@ -110,6 +110,7 @@ struct Slice {
   // 1/nbuckets slice of the bucket mode's factor and gradient rows at a time,
   // which then stay L2-resident; within a bucket mode-0 order is kept.
   int bucket_mode = -1, nbuckets = 0;
+  int64_t bucket_olo = 0, bucket_ohi = 0;  // ordinal range covered (a rank's share in a multi-GPU solve)
   DevBuf perm, rec_b;
 };
 
@@ -158,6 +159,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   Profiler prof;
+  bool shard_sim = false;       // rank/world set without a communicator (single-process tests of the shard logic)
   double slack = 1.0;           // sampler over-provisioning multiplier (grows on shortfall)
   bool merge_draws = true;      // merged (count) form of dense nonzero draws in the solves
   // Two-pass scatter for merged sets with a large random-access mode.  Off: on

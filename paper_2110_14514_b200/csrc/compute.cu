@@ -100,6 +100,7 @@ struct SampleStream {
   SamplesP S;
   const ModelP* M;
   int64_t p, total, b, end;
+  int64_t zoff;  // walk index m >= p maps to sample p + zoff + (m - p) (zero-row share of a rank)
   int lane, gl, nd;
   int skip = -1;  // mode whose rows are not gathered (split scatter, pass 2)
   int oB[U];
@@ -135,7 +136,7 @@ struct SampleStream {
           t[u][RI > 4 ? 6 : 2] = v1.z; t[u][RI > 4 ? 7 : 3] = v1.w;
         }
       } else {
-        const int32_t* z = S.zsub + (n - p) * nd;
+        const int32_t* z = S.zsub + (n + zoff - p) * nd;
 #pragma unroll
         for (int k = 0; k < NDm; ++k)
           if (k < nd) t[u][k] = __ldg(z + k);
@@ -169,7 +170,13 @@ struct SampleStream {
     gl = lane & (G - 1);
     nd = D > 0 ? D : M_.ndim;
     int64_t lo = 0, hi = total;
-    if (S.shard_world > 1) {  // sample-sharded multi-GPU solve: this rank's contiguous share
+    zoff = 0;
+    if (S.shard_world > 1 && S.zshard) {  // rank-owned merged nonzeros + a contiguous share of the zero rows
+      const int64_t zrows = total - p;
+      const int64_t zlo = zrows * S.shard_rank / S.shard_world, zhi = zrows * (S.shard_rank + 1) / S.shard_world;
+      hi = p + (zhi - zlo);
+      zoff = zlo;
+    } else if (S.shard_world > 1) {  // sample-sharded multi-GPU solve: this rank's contiguous share
       lo = total * S.shard_rank / S.shard_world;
       hi = total * (S.shard_rank + 1) / S.shard_world;
     }
@@ -222,7 +229,7 @@ struct SampleStream {
           if (k == nd) x = __int_as_float(tC[u][k]);
       }
       s[u].x = s[u].nz ? x : 0.0f;
-      s[u].n = n;
+      s[u].n = s[u].nz ? n : n + zoff;
 #pragma unroll
       for (int k = 0; k < NDm; ++k) s[u].idx[k] = tC[u][k < RI ? k : 0];
     }

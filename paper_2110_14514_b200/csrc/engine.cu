@@ -31,7 +31,7 @@ void segment_layout_impl(Ctx* ctx, const int32_t* coords, int64_t n, int ndim, i
                          int64_t* offsets);
 void slice_contains_impl(Ctx* ctx, const Slice* s, const int64_t* subs, int64_t n, uint8_t* hit);
 void iota_enqueue(Ctx* ctx, int32_t* p, int64_t n);
-void slice_bucket_layout(Ctx* ctx, Slice* X, int mode, int nb);
+void slice_bucket_layout(Ctx* ctx, Slice* X, int mode, int nb, int64_t olo, int64_t ohi);
 
 static thread_local std::string g_last_error;
 
@@ -186,6 +186,7 @@ static SamplesP samples_of(const Slice* X, const int32_t* ord, int64_t p, const 
   S.shard_world = 1;
   S.semi = 0;
   S.chunk_shift = 0;
+  S.zshard = 0;
   return S;
 }
 
@@ -196,6 +197,13 @@ static SamplesP semi_of(const Slice* X, SamplesP S, bool semi) {
   S.zero_scale = S.q ? X->omega_d / (double)S.q : 0.0;
   if (X->omega_fits && S.q) S.zero_scale = (double)X->omega / (double)S.q;
   return S;
+}
+
+// Multi-GPU merged draws: rank r owns the nonzero ordinals [eta r / N, eta (r+1) / N)
+// and evaluates every merged sample there, plus a contiguous 1/N of the zero rows.
+static void owned_range(const Ctx* ctx, const Slice* X, int64_t* olo, int64_t* ohi) {
+  *olo = X->nnz * ctx->rank / ctx->world;
+  *ohi = X->nnz * (ctx->rank + 1) / ctx->world;
 }
 
 // Solve-time sample sets are evaluated sharded across the context's ranks.
@@ -261,6 +269,7 @@ struct SampleBufs {
   DrawScratch scr;
   MergedDraw md;
   bool merged = false;
+  bool owned = false;  // multi-GPU: the merged nonzero part is this rank's own ordinal range
   bool semi = false;  // semi-stratified extension
   const int32_t* zsub = nullptr;   // where the last draw left the zero coordinates
   const long long* q_dev = nullptr;  // lazy zero layout row count (device)
@@ -274,7 +283,14 @@ struct SampleBufs {
   }
   // Enqueue the draw of this buffer set and return its device sample set.
   SamplesP draw(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t budget, long long code) {
-    md.perm = (merged && ctx->buckets && X->bucket_mode >= 0) ? X->perm.as<int32_t>() : nullptr;
+    int64_t olo = 0, ohi = X->nnz;
+    owned_range(ctx, X, &olo, &ohi);
+    md.perm = (merged && ctx->buckets && X->bucket_mode >= 0 && X->bucket_olo == olo && X->bucket_ohi == ohi)
+                  ? X->perm.as<int32_t>()
+                  : nullptr;
+    md.olo = ctx->world > 1 ? (uint32_t)olo : 0u;
+    md.ohi = ctx->world > 1 ? (uint32_t)ohi : 0u;
+    owned = merged && ctx->world > 1;
     const DrawOut o = draw_enqueue(ctx, X, g, p, q, budget, merged ? nullptr : ord.as<int32_t>(),
                                    zero.as<int32_t>(), code, scr, merged ? &md : nullptr, /*lazy=*/true, semi);
     zsub = o.zsub;
@@ -292,6 +308,7 @@ SamplesP SampleBufs::sample_set(const Slice* X) const {
   }
   SamplesP S = semi_of(X, samples_of(X, md.ord.as<int32_t>(), p, zsub, q), semi);
   S.q_dev = q_dev;
+  S.zshard = owned ? 1 : 0;
   if (md.perm) {  // positions into the bucketed copy, walked in round-robin chunks
     S.rec = X->rec_b.as<int>();
     S.chunk_shift = 3;  // 8 batches per chunk (measured flat for shifts 2..6 on c4)
@@ -333,9 +350,11 @@ static void prepare_buckets(Ctx* ctx, const Slice* Xc, int ldr) {
     if (ws <= 48e6) return;
     while (nb < 256 && ws / nb > 32e6) nb <<= 1;
   }
-  if (X->bucket_mode == mode && X->nbuckets == nb) return;
+  int64_t olo = 0, ohi = X->nnz;
+  owned_range(ctx, X, &olo, &ohi);
+  if (X->bucket_mode == mode && X->nbuckets == nb && X->bucket_olo == olo && X->bucket_ohi == ohi) return;
   const auto t0 = std::chrono::steady_clock::now();
-  slice_bucket_layout(ctx, X, mode, nb);
+  slice_bucket_layout(ctx, X, mode, nb, olo, ohi);
   if (getenv("OGCP_DEBUG_TIMING"))
     fprintf(stderr, "bucket layout %.1f ms\n",
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
@@ -1272,7 +1291,19 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   OGCP_API_BEGIN
   if (option == OGCP_OPT_MERGE_DRAWS) ctx->merge_draws = value != 0;
   else if (option == OGCP_OPT_SPLIT_SCATTER) ctx->split_scatter = value != 0;
-  else if (option == OGCP_OPT_BUCKETS) {
+  else if (option == OGCP_OPT_SHARD_SIM) {
+    if (ctx->comm) throw Error(OGCP_E_USAGE, "shard simulation needs a context without a communicator");
+    const int r = (int)(value & 0xffff), w = (int)(value >> 16);
+    if (w < 1 || r >= w) {
+      ctx->rank = 0;
+      ctx->world = 1;
+      ctx->shard_sim = false;
+    } else {
+      ctx->rank = r;
+      ctx->world = w;
+      ctx->shard_sim = w > 1;
+    }
+  } else if (option == OGCP_OPT_BUCKETS) {
     ctx->buckets = value != 0;
     ctx->buckets_force = value > 1 ? (int)std::min<int64_t>(value, 256) : 0;
   }
@@ -1655,6 +1686,74 @@ int ogcp_solve_static(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_conf
   OGCP_API_BEGIN
   if (max_epochs < 0 || iters < 1) throw Error(OGCP_E_USAGE, "epoch and iteration counts must be >= 1");
   solve_static_impl(ctx, s, cfg, loss, seed_key, m, weights, adam, max_epochs, iters, tol, trace);
+  OGCP_API_END
+}
+
+int ogcp_debug_solve_draw(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const int64_t* key, int32_t nkey,
+                          int64_t p, int64_t q, int64_t max_rejects, int32_t ldr, int64_t cap_nz, int32_t* ord_out,
+                          uint8_t* cnt_out, int64_t* n_nz, int64_t cap_zero, int32_t* zero_out, int64_t* n_zero) {
+  OGCP_API_BEGIN
+  const Slice* X = s;
+  if (p < 0) p = X->nnz;
+  if (X->nnz == 0) p = 0;
+  static thread_local SampleBufs b;
+  precheck_draw(X, p, q);
+  b.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
+  b.semi = false;
+  if (b.merged) prepare_buckets(ctx, X, ldr);
+  const int64_t budget = budget_of(q, max_rejects);
+  if (nkey > 8) throw Error(OGCP_E_USAGE, "at most 8 key words");
+  uint64_t k[8];
+  for (int i = 0; i < nkey; ++i) k[i] = (uint64_t)key[i];
+  reset_flags(ctx);
+  const SamplesP S = sharded(ctx, b.draw(ctx, X, seedseq_pcg64(seed, k, nkey), budget, code_of(1, 0)));
+  fetch_flags(ctx);
+  OGCP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (check_flags(ctx, X, OGCP_GAUSSIAN, budget, "draw", 0) != 0)
+    throw Error(OGCP_E_INTERNAL, "draw shortfall or counter overflow (retry with more slack)");
+  // the samples this rank's SampleStream walks (compute.cu SampleStream::init)
+  int64_t pn = S.p;
+  if (S.p_dev) OGCP_CUDA(cudaMemcpy(&pn, S.p_dev, 8, cudaMemcpyDeviceToHost));
+  int64_t zrows = S.q;
+  if (S.q_dev) OGCP_CUDA(cudaMemcpy(&zrows, S.q_dev, 8, cudaMemcpyDeviceToHost));
+  const int64_t total = pn + zrows;
+  int64_t nlo = 0, nhi = pn, zlo = 0, zhi = zrows;
+  if (S.shard_world > 1 && S.zshard) {
+    zlo = zrows * S.shard_rank / S.shard_world;
+    zhi = zrows * (S.shard_rank + 1) / S.shard_world;
+  } else if (S.shard_world > 1) {
+    const int64_t lo = total * S.shard_rank / S.shard_world, hi = total * (S.shard_rank + 1) / S.shard_world;
+    nlo = std::min(lo, pn);
+    nhi = std::min(hi, pn);
+    zlo = std::max<int64_t>(lo - pn, 0);
+    zhi = std::max<int64_t>(hi - pn, 0);
+  }
+  std::vector<int32_t> ord(std::max<int64_t>(nhi - nlo, 0));
+  std::vector<uint8_t> cnt(ord.size(), 1);
+  if (!ord.empty()) {
+    OGCP_CUDA(cudaMemcpy(ord.data(), S.ord + nlo, ord.size() * 4, cudaMemcpyDeviceToHost));
+    if (S.cnt) OGCP_CUDA(cudaMemcpy(cnt.data(), S.cnt + nlo, ord.size(), cudaMemcpyDeviceToHost));
+  }
+  if (b.merged && b.md.perm) {  // positions of the bucketed copy -> ordinals
+    std::vector<int32_t> perm(X->bucket_ohi - X->bucket_olo);
+    OGCP_CUDA(cudaMemcpy(perm.data(), b.md.perm, perm.size() * 4, cudaMemcpyDeviceToHost));
+    for (auto& o : ord) o = perm[o];
+  }
+  if ((int64_t)ord.size() > cap_nz) throw Error(OGCP_E_USAGE, "nonzero output capacity too small");
+  std::copy(ord.begin(), ord.end(), ord_out);
+  std::copy(cnt.begin(), cnt.end(), cnt_out);
+  *n_nz = (int64_t)ord.size();
+  const int d = X->ndim;
+  std::vector<int32_t> z((size_t)std::max<int64_t>(zhi - zlo, 0) * d);
+  if (!z.empty()) OGCP_CUDA(cudaMemcpy(z.data(), S.zsub + zlo * d, z.size() * 4, cudaMemcpyDeviceToHost));
+  int64_t nz = 0;
+  for (int64_t r = 0; r < zhi - zlo; ++r) {
+    if (z[r * d] < 0) continue;  // rejected candidate of the lazy layout
+    if (nz >= cap_zero) throw Error(OGCP_E_USAGE, "zero output capacity too small");
+    std::copy(z.begin() + r * d, z.begin() + (r + 1) * d, zero_out + nz * d);
+    ++nz;
+  }
+  *n_zero = nz;
   OGCP_API_END
 }
 

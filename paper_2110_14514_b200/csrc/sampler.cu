@@ -311,8 +311,11 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
                                                              const long long* __restrict__ bstart,
                                                              int64_t target, int32_t* __restrict__ out,
                                                              long long* __restrict__ end_word,
-                                                             uint32_t* __restrict__ hist, DevFlags* flags) {
+                                                             uint32_t* __restrict__ hist, DevFlags* flags,
+                                                             uint32_t olo, uint32_t ohi,
+                                                             unsigned long long* __restrict__ owned) {
   __shared__ int32_t stage[kBlockWords];
+  uint32_t mine = 0;  // merged form: accepted draws landing in this rank's ordinal range [olo, ohi)
   const int64_t chunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
   WordGen g = block_wordgen(sp, w0p);
   Map<NCOL> m = identity_map<NCOL>();
@@ -340,8 +343,12 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
       const uint64_t prod = (uint64_t)word * n;
       if ((uint32_t)prod >= thr) {
         const uint32_t val = (uint32_t)(prod >> 32);
-        if (hist) {  // merged form: byte counters (a wrap is caught by the count-sum check)
-          atomicAdd(hist + (val >> 3), 1u << ((val & 7u) << 2));
+        if (hist) {  // merged form: 4-bit counters (a wrap is caught by the count-sum check)
+          if (val >= olo && val < ohi) {
+            const uint32_t o = val - olo;
+            atomicAdd(hist + (o >> 3), 1u << ((o & 7u) << 2));
+            ++mine;
+          }
         } else {
           stage[rel++] = (int32_t)val;
         }
@@ -351,7 +358,12 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
       }
     }
   }
-  if (hist) return;
+  if (hist) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(owned, (unsigned long long)mine);
+    return;
+  }
   __syncthreads();
   const long long lim = min((long long)nblk, (long long)target - eb);
   for (long long i = threadIdx.x; i < lim; i += kScanThreads) out[eb + i] = stage[i];
@@ -686,14 +698,16 @@ __global__ void __launch_bounds__(kScanThreads) k_hist_count(const uint32_t* __r
   }
 }
 
-__global__ void k_hist_verify(const unsigned long long* __restrict__ cnt_sum, long long p, DevFlags* flags) {
-  if (threadIdx.x == 0 && blockIdx.x == 0 && *cnt_sum != (unsigned long long)p)
-    atomicOr(&flags->data_bits, kMergeOverflowBit);
+// Σ counters must equal the draws that landed in this rank's range (all p on one GPU).
+__global__ void k_hist_verify(const unsigned long long* __restrict__ cnt_sum,
+                              const unsigned long long* __restrict__ owned, DevFlags* flags) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && *cnt_sum != *owned) atomicOr(&flags->data_bits, kMergeOverflowBit);
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_hist_write(const uint32_t* __restrict__ hist, int64_t nwords,
                                                              int64_t eta, const long long* __restrict__ boff,
-                                                             int32_t* __restrict__ ord, uint8_t* __restrict__ cnt) {
+                                                             int32_t* __restrict__ ord, uint8_t* __restrict__ cnt,
+                                                             int32_t obase) {
   const int64_t w0 = (blockIdx.x * (int64_t)kScanThreads + threadIdx.x) * kHistWordsPerThread;
   uint32_t w[kHistWordsPerThread];
   int c = 0;
@@ -727,7 +741,7 @@ __global__ void __launch_bounds__(kScanThreads) k_hist_write(const uint32_t* __r
     for (int b = 0; b < 8; ++b) {
       const uint32_t v = (w[j] >> (4 * b)) & 0xfu;
       if (v) {
-        s_ord[rel] = (int32_t)((w0 + j) * 8 + b);
+        s_ord[rel] = obase + (int32_t)((w0 + j) * 8 + b);
         s_cnt[rel] = (uint8_t)v;
         ++rel;
       }
@@ -745,18 +759,18 @@ __global__ void __launch_bounds__(kScanThreads) k_hist_write(const uint32_t* __r
 // one output word = 8 consecutive positions; the counter reads are random but
 // hit the L2-resident histogram.
 __global__ void k_hist_permute(const uint32_t* __restrict__ hist, const int32_t* __restrict__ perm, int64_t eta,
-                               int64_t nwords, uint32_t* __restrict__ pnib) {
+                               int64_t nwords, uint32_t* __restrict__ pnib, int32_t olo) {
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p0 = w * 8;
     int32_t o[8];
     if (p0 + 8 <= eta) {
       const int4 a = __ldg(reinterpret_cast<const int4*>(perm + p0));
       const int4 b = __ldg(reinterpret_cast<const int4*>(perm + p0) + 1);
-      o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
-      o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+      o[0] = a.x - olo; o[1] = a.y - olo; o[2] = a.z - olo; o[3] = a.w - olo;
+      o[4] = b.x - olo; o[5] = b.y - olo; o[6] = b.z - olo; o[7] = b.w - olo;
     } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = p0 + j < eta ? __ldg(perm + p0 + j) : -1;
+      for (int j = 0; j < 8; ++j) o[j] = p0 + j < eta ? __ldg(perm + p0 + j) - olo : -1;
     }
     uint32_t out = 0;
 #pragma unroll
@@ -769,7 +783,8 @@ __global__ void k_hist_permute(const uint32_t* __restrict__ hist, const int32_t*
 template <int NCOL>
 static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int64_t target, int64_t words,
                        int32_t* out, long long* end_word, long long* elems_total, DrawScratch& scr,
-                       uint32_t* hist = nullptr) {
+                       uint32_t* hist = nullptr, uint32_t olo = 0, uint32_t ohi = 0,
+                       unsigned long long* owned = nullptr) {
   const int64_t nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
   const int64_t nblocks = (nchunks + kScanThreads - 1) / kScanThreads;
   scr.tmaps.ensure((size_t)nblocks * kScanThreads * NCOL);
@@ -782,7 +797,7 @@ static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int6
                                                       elems_total);
   k_draw_write<NCOL><<<(unsigned)nblocks, kScanThreads, 0, s>>>(sp, w0, nchunks, scr.tmaps.as<uint8_t>(),
                                                                scr.bstart.as<long long>(), target, out, end_word,
-                                                               hist, ctx->flags.as<DevFlags>());
+                                                               hist, ctx->flags.as<DevFlags>(), olo, ohi, owned);
   ctx->count(3);
   check_launch();
 }
@@ -848,34 +863,41 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
       const double sd = std::sqrt((double)p * r) / (1.0 - r);
       const int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
       if (merged) {
-        const int64_t nwords = (eta + 7) / 8;
-        merged->hist.ensure((size_t)nwords * 4);
-        merged->ord.ensure((size_t)std::min(p, eta) * 4);
-        merged->cnt.ensure((size_t)std::min(p, eta));
-        OGCP_CUDA(cudaMemsetAsync(merged->hist.ptr, 0, (size_t)nwords * 4, s));
-        run_stream<1>(ctx, sp, nullptr, p, words, nullptr, nz_end, nz_avail, scr, merged->hist.as<uint32_t>());
+        // counters for this rank's ordinal range [olo, ohi) (the whole slice on one GPU)
+        const uint32_t olo = merged->ohi ? merged->olo : 0u;
+        const uint32_t ohi = merged->ohi ? merged->ohi : (uint32_t)eta;
+        const int64_t own = (int64_t)ohi - olo;
+        const int64_t nwords = (own + 7) / 8;
+        merged->hist.ensure((size_t)std::max<int64_t>(nwords, 1) * 4);
+        merged->ord.ensure((size_t)std::max<int64_t>(std::min(p, own), 1) * 4);
+        merged->cnt.ensure((size_t)std::max<int64_t>(std::min(p, own), 1));
+        OGCP_CUDA(cudaMemsetAsync(merged->hist.ptr, 0, (size_t)std::max<int64_t>(nwords, 1) * 4, s));
+        unsigned long long* owned = reinterpret_cast<unsigned long long*>(sc + 9);
+        run_stream<1>(ctx, sp, nullptr, p, words, nullptr, nz_end, nz_avail, scr, merged->hist.as<uint32_t>(), olo,
+                      ohi, owned);
         const uint32_t* counters = merged->hist.as<uint32_t>();
         if (merged->perm) {  // emit in the slice's bucketed position order
-          merged->pnib.ensure((size_t)nwords * 4);
-          k_hist_permute<<<std::min<int64_t>((nwords + 255) / 256, kNumSMs * 16), 256, 0, s>>>(
-              counters, merged->perm, eta, nwords, merged->pnib.as<uint32_t>());
+          merged->pnib.ensure((size_t)std::max<int64_t>(nwords, 1) * 4);
+          k_hist_permute<<<std::max<int64_t>(1, std::min<int64_t>((nwords + 255) / 256, kNumSMs * 16)), 256, 0, s>>>(
+              counters, merged->perm, own, nwords, merged->pnib.as<uint32_t>(), (int32_t)olo);
           ctx->count();
           counters = merged->pnib.as<uint32_t>();
         }
-        const int64_t hblocks = (nwords + (int64_t)kHistWordsPerThread * kScanThreads - 1) /
-                                ((int64_t)kHistWordsPerThread * kScanThreads);
+        const int64_t hblocks = std::max<int64_t>(1, (nwords + (int64_t)kHistWordsPerThread * kScanThreads - 1) /
+                                                         ((int64_t)kHistWordsPerThread * kScanThreads));
         merged->bcount.ensure((size_t)hblocks * 4);
         merged->boff.ensure((size_t)hblocks * 8);
         unsigned long long* cnt_sum = reinterpret_cast<unsigned long long*>(sc + 7);
         k_hist_count<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, merged->bcount.as<uint32_t>(),
                                                                 cnt_sum);
-        k_hist_verify<<<1, 32, 0, s>>>(cnt_sum, (long long)p, ctx->flags.as<DevFlags>());
+        k_hist_verify<<<1, 32, 0, s>>>(cnt_sum, owned, ctx->flags.as<DevFlags>());
         ctx->count();
         k_zero_scan<<<1, 1024, 0, s>>>(merged->bcount.as<uint32_t>(), hblocks, merged->boff.as<long long>(),
                                        sc + 5);
-        k_hist_write<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, eta,
-                                                                merged->boff.as<long long>(),
-                                                                merged->ord.as<int32_t>(), merged->cnt.as<uint8_t>());
+        // positions (bucketed copy) are local; unbucketed ordinals are global
+        k_hist_write<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, own, merged->boff.as<long long>(),
+                                                                merged->ord.as<int32_t>(), merged->cnt.as<uint8_t>(),
+                                                                merged->perm ? 0 : (int32_t)olo);
         ctx->count(3);
         merged->count = sc + 5;
       } else {

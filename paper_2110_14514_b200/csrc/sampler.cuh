@@ -13,10 +13,14 @@ struct DrawScratch {
 // the device.
 // perm (nullable): the slice's bucketed order (Slice::perm); the set is then
 // emitted in position order -- ord holds positions into Slice::rec_b.
+// [olo, ohi) (ohi = 0: the whole slice): the ordinal range this rank owns in a
+// multi-GPU solve; only draws landing there are counted (the RNG words are
+// still generated in full, so the counts are exactly the reference's).
 struct MergedDraw {
   DevBuf hist, ord, cnt, bcount, boff, pnib;
   long long* count = nullptr;
   const int32_t* perm = nullptr;
+  uint32_t olo = 0, ohi = 0;
 };
 
 void init_jump_table();

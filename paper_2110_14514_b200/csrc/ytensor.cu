@@ -118,6 +118,11 @@ __global__ void k_bucket_keys(const int* __restrict__ rec, int rec_ints, int mod
     keys[i] = (uint8_t)(((long long)rec[i * rec_ints + mode] * nb) / dim);
 }
 
+__global__ void k_add32(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] += v;
+}
+
 __global__ void k_gather_records(const int4* __restrict__ rec, int vec_per_rec, const int32_t* __restrict__ perm,
                                  int64_t n, int4* __restrict__ out) {
   const int64_t total = n * vec_per_rec;
@@ -128,8 +133,8 @@ __global__ void k_gather_records(const int4* __restrict__ rec, int vec_per_rec, 
   }
 }
 
-void slice_bucket_layout(Ctx* ctx, Slice* X, int mode, int nb) {
-  const int64_t n = X->nnz;
+void slice_bucket_layout(Ctx* ctx, Slice* X, int mode, int nb, int64_t olo, int64_t ohi) {
+  const int64_t n = ohi - olo;  // the ordinals [olo, ohi) this rank owns (the whole slice on one GPU)
   cudaStream_t s = ctx->stream;
   int bits = 0;
   while ((1 << bits) < nb) ++bits;
@@ -139,9 +144,10 @@ void slice_bucket_layout(Ctx* ctx, Slice* X, int mode, int nb) {
   iota.ensure(n * 4);
   X->perm.ensure(n * 4);
   X->rec_b.ensure((size_t)n * X->rec_ints * 4);
-  k_bucket_keys<<<grid_for(n), 256, 0, s>>>(X->records.as<int>(), X->rec_ints, mode, (long long)X->dims[mode], nb, n,
-                                            keys.as<uint8_t>());
+  k_bucket_keys<<<grid_for(n), 256, 0, s>>>(X->records.as<int>() + olo * X->rec_ints, X->rec_ints, mode,
+                                            (long long)X->dims[mode], nb, n, keys.as<uint8_t>());
   k_iota32<<<grid_for(n), 256, 0, s>>>(iota.as<int32_t>(), n);
+  if (olo) k_add32<<<grid_for(n), 256, 0, s>>>(iota.as<int32_t>(), n, (int32_t)olo);
   size_t tb = 0;
   OGCP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint8_t>(), keys_s.as<uint8_t>(),
                                             iota.as<int32_t>(), X->perm.as<int32_t>(), (int)n, 0, bits, s));
@@ -156,6 +162,8 @@ void slice_bucket_layout(Ctx* ctx, Slice* X, int mode, int nb) {
   OGCP_CUDA(cudaStreamSynchronize(s));  // scratch buffers are released on return
   X->bucket_mode = mode;
   X->nbuckets = nb;
+  X->bucket_olo = olo;
+  X->bucket_ohi = ohi;
 }
 
 struct YScratch {

@@ -1,6 +1,5 @@
-for lib in libogcp_b200 libogcp_b200_s3 libogcp_b200_w3 libogcp_b200_s3w3; do
-  OGCP_LIB=paper_2110_14514_b200/$lib.so python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab.json 2> gpurun_out/ab.err
-  python -c "
+python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab.json 2> gpurun_out/ab.err
+python -c "
 import json; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); k=d['kernel_ms']; n=d['kernel_launch_brackets']
-print('$lib', round(d['value']/1e9,3), {c: round(k[c]/max(n[c],1),3) for c in k})"
-done
+print(round(d['value']/1e9,3), {c: round(k[c]/max(n[c],1),3) for c in k})"

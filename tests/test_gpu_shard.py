@@ -1,0 +1,96 @@
+"""The multi-GPU shard partition, checked in one process: a context put in
+shard-simulation mode (OGCP_OPT_SHARD_SIM, no communicator) runs exactly the
+share of rank r of a world-N solve.  For merged (count-form) gradient draws --
+with and without the row-bucketed layout -- the ranks' nonzero shares (their
+own ordinal ranges) and zero-row shares must partition the single-GPU set
+exactly; for plain draws the contiguous split must too."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2110_14514_b200 as P
+from paper_2110_14514_b200 import _lib
+
+
+@pytest.fixture(scope="module")
+def slice_1e5():
+    rng = np.random.default_rng(21)
+    dims = (300, 200, 40)
+    lin = rng.choice(int(np.prod(dims)), size=100_000, replace=False)
+    subs0 = np.array(np.unravel_index(np.sort(lin), dims)).T
+    vals = rng.integers(1, 4, size=lin.size).astype(float)
+    return P.SparseTensor.from_zero_based(dims, subs0, vals)
+
+
+def _draw(X, p, q, world=1, rank=0):
+    _lib.set_shard_sim(rank, world)
+    try:
+        return _lib.debug_solve_draw(X, 5, (7, 3, 0, 1), p, q, ldr=8)
+    finally:
+        _lib.set_shard_sim(0, 1)
+
+
+@pytest.mark.parametrize("buckets", [1, 4])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_merged_draw_shards_partition(slice_1e5, buckets, world):
+    X = slice_1e5
+    _lib.set_buckets(buckets)
+    try:
+        o, c, z = _draw(X, None, 4000)  # p = all: merged form
+        assert c.sum() == X.nnz and len(z) == 4000
+        parts = [_draw(X, None, 4000, world, r) for r in range(world)]
+    finally:
+        _lib.set_buckets(1)
+    po = np.concatenate([q[0] for q in parts])
+    pc = np.concatenate([q[1] for q in parts])
+    a, b = np.argsort(o, kind="stable"), np.argsort(po, kind="stable")
+    np.testing.assert_array_equal(po[b], o[a])
+    np.testing.assert_array_equal(pc[b], c[a])
+    for r, (ro, _, _) in enumerate(parts):  # each rank holds its own ordinal range
+        lo, hi = X.nnz * r // world, X.nnz * (r + 1) // world
+        assert ro.size == 0 or (ro.min() >= lo and ro.max() < hi)
+    np.testing.assert_array_equal(np.concatenate([q[2] for q in parts]), z)
+
+
+def test_plain_draw_shards_partition(slice_1e5):
+    X = slice_1e5
+    o, c, z = _draw(X, 3000, 2000)  # p << eta: per-draw form, contiguous split of [nonzeros | zeros]
+    parts = [_draw(X, 3000, 2000, 3, r) for r in range(3)]
+    np.testing.assert_array_equal(np.concatenate([q[0] for q in parts]), o)
+    np.testing.assert_array_equal(np.concatenate([q[2] for q in parts]), z)
+
+
+def test_sharded_gradients_sum_to_single_gpu(slice_1e5):
+    """Shard-simulated factor solves of one iteration with rate ~0: every rank's
+    K3 output is its partial gradient, so the per-rank first Adam moments
+    (u = (1-b1) g) must sum to the single-GPU one."""
+    X = slice_1e5
+    R = 6
+    rng = np.random.default_rng(2)
+    init = [rng.uniform(0.2, 1.0, (d, R)) for d in X.dims]
+    w = np.full(R, 1.1)
+    cfg = P.SolverConfig(max_epochs_factors=1, iters_factors=1, rate_factors=1e-30,
+                         samples=P.SamplerConfig(None, 3000, 5000, 5000, seed=4))
+    loss = P.make_loss("poisson")
+
+    def u_of(world, rank):
+        _lib.set_shard_sim(rank, world)
+        try:
+            model = P.DeviceModel.from_numpy(init)
+            adam = cfg.make_adam(cfg.rate_factors, loss)
+            adam.init_device(model.dims, model.rank)
+            from paper_2110_14514_b200.solvers import solve_factors_device
+            solve_factors_device(X, model, w, None, [], cfg, loss, adam, 0, 1)
+            return [t[:, :R].double().cpu().numpy() for t in adam._buf["u"]]
+        finally:
+            _lib.set_shard_sim(0, 1)
+
+    full = u_of(1, 0)
+    for world in (2, 4):
+        parts = [u_of(world, r) for r in range(world)]
+        for k in range(3):
+            tot = sum(p_[k] for p_ in parts)
+            assert np.linalg.norm(tot - full[k]) <= 1e-5 * np.linalg.norm(full[k])
