@@ -182,25 +182,59 @@ def run_reference(args):
     adam = O.AdamOracle(1e-3, lower=0.0)
     adam.init(init)
     pq = CPU_SAMPLE_PQ
+    # All host cores, sample-sharded (SURVEY 8(d) multi-process bound): each of n forked
+    # workers draws and evaluates (p+q)/n samples of the step (sampled_gradient_tensor and
+    # the sampled MTTKRP of factor_gradients on its share, factors shared copy-on-write,
+    # one BLAS thread each); the state-sized terms -- history Grams (multithreaded BLAS)
+    # and the Adam step -- run once in the parent.  The cross-process sum of the partial
+    # gradients is not timed (best case for the CPU).
+    ncores = os.cpu_count() or 1
+    nproc = max(1, min(ncores, REF_MAX_PROCS))
+    _REF.update(X=Xo, init=init, w=w, window=window, pq=max(1, pq // nproc))
+    import multiprocessing as mp
+    pool = mp.get_context("fork").Pool(nproc) if nproc > 1 else None
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        _, ys, yv = O.sampled_y(Xo, init, w, "poisson", pq, pq, O.keyed_rng(7, H + 1, 3, 0, i))
-        grads = O.assemble_factor_grads(ys, yv, DIMS, init, w, init, window, 1.0, 1.0, H + 1, 0.0)
-        adam.step([a.copy() for a in init], grads, i + 1)
+        jobs = [(i, k) for k in range(nproc)]
+        list(pool.map(_ref_share, jobs)) if pool else [_ref_share(j) for j in jobs]
+        state = O.assemble_factor_grads(np.empty((0, 3), np.int64), np.empty(0), DIMS, init, w, init, window, 1.0,
+                                        1.0, H + 1, 0.0)
+        adam.step([a.copy() for a in init], state, i + 1)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
+    if pool:
+        pool.close()
     tot = sum(times)
-    value = args.steps * 2 * pq / tot
-    sample = f"one factor iteration per step at p=q=2^19 on the c4 slice (oracle numpy port, 1 process)"
+    value = args.steps * 2 * _REF["pq"] * nproc / tot
+    sample = (f"one factor iteration per step at p=q=2^19 on the c4 slice, sample-sharded over {nproc} forked "
+              f"processes (oracle numpy port; {ncores} host cores, at most {REF_MAX_PROCS} workers for memory)")
     line = {"metric": "sampled GCP gradient entries/s", "value": value, "unit": "entries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": WORKLOAD, "sample_per_step": sample},
-            "cpu_baseline": {"value": value, "unit": "entries/s", "cores": 1, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "entries/s", "cores": nproc, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+_REF = {}
+REF_MAX_PROCS = 32
+
+
+def _ref_share(job):
+    """One worker's share of a reference-arm step (see run_reference): its samples' draw,
+    merged gradient tensor and sampled MTTKRP (times s) for every mode."""
+    from oracle import ogcp_oracle as O
+    from threadpoolctl import threadpool_limits
+    step, k = job
+    R = _REF
+    with threadpool_limits(1):
+        _, ys, yv = O.sampled_y(R["X"], R["init"], R["w"], "poisson", R["pq"], R["pq"],
+                                O.keyed_rng(7, H + 1, 3, step, k))
+        g = [O.mttkrp(ys, yv, DIMS, R["init"], m) * R["w"][None, :] for m in range(len(DIMS))]
+    return float(g[0][0, 0])
 
 
 def main():
