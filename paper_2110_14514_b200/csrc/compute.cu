@@ -917,6 +917,91 @@ __global__ void __launch_bounds__(kThreads, 3) k_factor_update(int64_t rows, int
   if (bad) report(flags, kFlagDiverge, code, 0);
 }
 
+// 32 < rank <= 128 with history / model terms: the apply H = A Mk - Aold Nk is
+// an [rows x R] x [R x R] product, so it is register-tiled: a CTA stages Mk, Nk
+// (R x R) once and a 32-row tile of A / Aold per pass in shared memory; thread
+// (warp w, lane l) owns rows 4w..4w+3 and columns CPT*l..CPT*l+CPT-1 (CPT = LDR/32),
+// reading A / Aold rows as broadcasts and Mk / Nk rows as contiguous vectors,
+// then applies reg + Adam to its 4 x CPT elements (coalesced row segments).
+constexpr int kK5TileRows = 32;
+template <int LDR>
+__global__ void __launch_bounds__(kThreads) k_factor_update_tiled(int64_t rows, int rank, float* __restrict__ A,
+                                                                  const float* __restrict__ Aold,
+                                                                  const float* __restrict__ G, float* __restrict__ u,
+                                                                  float* __restrict__ v, const float* __restrict__ Mk,
+                                                                  const float* __restrict__ Nk, float reg,
+                                                                  float rate_i, float b1, float omb1, float b2,
+                                                                  float omb2, float eps, float lower, DevFlags* flags,
+                                                                  long long code) {
+  constexpr int CPT = LDR / 32;
+  constexpr int TR = kK5TileRows;
+  extern __shared__ __align__(16) float k5s[];
+  float* sm = k5s;                 // [LDR][LDR] Mk (zero padded)
+  float* sn = sm + LDR * LDR;      // [LDR][LDR] Nk
+  float* sa = sn + LDR * LDR;      // [TR][LDR] A tile
+  float* so = sa + TR * LDR;       // [TR][LDR] Aold tile
+  const bool has_old = Aold != nullptr;
+  for (int e = threadIdx.x; e < LDR * LDR; e += blockDim.x) {
+    const int r = e / LDR, c = e % LDR;
+    const bool in = r < rank && c < rank;
+    sm[e] = in ? Mk[r * rank + c] : 0.f;
+    sn[e] = (in && has_old) ? Nk[r * rank + c] : 0.f;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c0 = lane * CPT;
+  bool bad = false;
+  const int64_t ntiles = (rows + TR - 1) / TR;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * TR;
+    __syncthreads();  // previous tile consumed (and Mk / Nk staged on the first pass)
+    for (int e = threadIdx.x; e < TR * LDR / 4; e += blockDim.x) {
+      const int rr = e / (LDR / 4);
+      const bool ok = r0 + rr < rows;
+      const int64_t at = (r0 + rr) * LDR + (e % (LDR / 4)) * 4;
+      reinterpret_cast<float4*>(sa)[e] = ok ? *reinterpret_cast<const float4*>(A + at) : make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(so)[e] =
+          (ok && has_old) ? __ldg(reinterpret_cast<const float4*>(Aold + at)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    float h[4][CPT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) h[i][j] = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < LDR; ++k) {
+      float mr[CPT], nr[CPT];
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        mr[j] = sm[k * LDR + c0 + j];
+        nr[j] = sn[k * LDR + c0 + j];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float a = sa[(w * 4 + i) * LDR + k];
+        const float ao = so[(w * 4 + i) * LDR + k];
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) h[i][j] += a * mr[j] - ao * nr[j];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t row = r0 + w * 4 + i;
+      if (row >= rows) continue;
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const int c = c0 + j;
+        if (c >= rank) continue;
+        const int64_t at = row * LDR + c;
+        const float a = sa[(w * 4 + i) * LDR + c];
+        const float g = __ldg(G + at) + reg * a + h[i][j];
+        if (!adam_regs(A, u, v, at, a, g, u[at], v[at], b1, omb1, b2, omb2, rate_i, eps, lower)) bad = true;
+      }
+    }
+  }
+  if (bad) report(flags, kFlagDiverge, code, 0);
+}
+
 // rank > 32: one warp per row, CPL columns per lane, Mk / Nk in shared memory.
 template <int CPL>
 __global__ void __launch_bounds__(kThreads) k_factor_update_wide(int64_t rows, int rank, int ldr,
@@ -1325,6 +1410,21 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
       case 16: launch(k_factor_update<16>); break;
       default: launch(k_factor_update<32>); break;
     }
+  } else if (Mk && ldr <= 128) {
+    auto launch = [&](auto kern, int L) {
+      const size_t smem = ((size_t)2 * L * L + (size_t)2 * kK5TileRows * L) * 4;
+      if (smem > 48 * 1024)
+        OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      OGCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+      const int64_t tiles = (rows + kK5TileRows - 1) / kK5TileRows;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)kNumSMs * std::max(per_sm, 1)));
+      kern<<<grid, kThreads, smem, ctx->stream>>>(rows, rank, A, Aold, G, u, v, Mk, Nk, (float)reg, (float)rate_i,
+                                                  fb1, fomb1, fb2, fomb2, (float)eps, (float)lower,
+                                                  ctx->flags.as<DevFlags>(), code);
+    };
+    if (ldr <= 64) launch(k_factor_update_tiled<64>, 64);
+    else launch(k_factor_update_tiled<128>, 128);
   } else {
     const size_t need = Mk ? (size_t)2 * rank * rank * 4 : 0;
     const bool stage = need > 0 && need <= 200 * 1024;

@@ -1198,7 +1198,7 @@ int ogcp_ctx_create(int32_t device, void* cuda_stream, ogcp_ctx** out) {
   c->device = device;
   c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   c->flags.ensure(sizeof(DevFlags));
-  OGCP_CUDA(cudaMallocHost((void**)&c->host_scalars, 64 * 8));
+  OGCP_CUDA(cudaMallocHost((void**)&c->host_scalars, 1024 * 8));
   OGCP_CUDA(cudaMallocHost((void**)&c->host_flags, sizeof(DevFlags)));
   init_jump_table();
   *out = c.release();

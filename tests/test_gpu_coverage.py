@@ -212,3 +212,20 @@ def test_large_slice_prefiltered_zero_draws_bit_exact():
     ref = O.draw(O.Slice(dims, subs0, vals), 5000, 200_000, O.keyed_rng(3, 9))
     np.testing.assert_array_equal(s.nz_ordinals, ref.ordinals)
     np.testing.assert_array_equal(s.zero_subs0, ref.zero_subs0)
+
+
+@pytest.mark.parametrize("R", [64, 130])
+def test_weight_solve_vs_oracle_large_ranks(R):
+    """solve_weights at ranks whose temporal row no longer fits a 64-double host mirror."""
+    dims = (40, 30, 12)
+    subs0, vals = _slice(R + 5, dims, 900)
+    rng = np.random.default_rng(R + 1)
+    A = [rng.uniform(0.2, 1.0, (d, R)) / 3 for d in dims]
+    cfg = P.SolverConfig(max_epochs_weights=2, iters_weights=5, rate_weights=0.05, reg_weights=0.1,
+                         samples=P.SamplerConfig(500, 600, 1500, 1500, seed=4))
+    X = P.SparseTensor.from_zero_based(dims, subs0, vals)
+    res = P.solve_weights(X, A, P.make_loss("poisson"), cfg, t=3)
+    ocfg = O.Cfg(kappa_w=2, tau_w=5, rate_w=0.05, reg_weights=0.1, p=500, q=600, p_obj=1500, q_obj=1500, seed=4)
+    s, tr, _, _ = O.temporal_solve(O.Slice(dims, subs0, vals), A, "poisson", ocfg, 3)
+    assert rel_err(res.weights, s) < 1e-4
+    np.testing.assert_allclose(res.trace.objective, tr, rtol=1e-4)
