@@ -744,6 +744,125 @@ __global__ void __launch_bounds__(kThreads) k_gram2(const float* __restrict__ A,
   }
 }
 
+// ---- K4 on tensor cores for ldr 64 / 128 (the Grams are
+// [R x rows] x [rows x R] products with arithmetic intensity growing with R).
+// mma.sync m16n8k8 TF32 with the 3-term split x = hi + lo (hi = tf32(x),
+// lo = tf32(x - hi)): hi*hi + hi*lo + lo*hi keeps fp32-level accuracy.  Warp w
+// owns one 16-row block of the output (i) and JPW 8-column blocks (j); row tiles
+// of A (and B = A_old) are double-buffered in padded shared memory (stride
+// LDR + 8: conflict-free fragment loads).  fp32 accumulation over a CTA's rows,
+// fp64 across CTAs (k_gram_finalize, fixed order).
+__device__ __forceinline__ uint32_t tf32_of(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+constexpr int kGramTcRows = 32;
+template <int LDR>
+__global__ void __launch_bounds__(kThreads, 1) k_gram_tc(const float* __restrict__ A, const float* __restrict__ B,
+                                                         int64_t rows, int64_t rows_per_block, int ngram,
+                                                         double* __restrict__ partials) {
+  constexpr int LDP = LDR + 8;
+  constexpr int IB = LDR / 16, JB = LDR / 8;
+  constexpr int WPI = 8 / IB;        // warps per i-block
+  constexpr int JPW = JB / WPI;      // j-blocks per warp
+  constexpr int TILE = kGramTcRows * LDP;
+  extern __shared__ __align__(16) float gts[];  // [2 buffers][A tile, B tile]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int i0 = (w / WPI) * 16;
+  const int jb0 = (w % WPI) * JPW;
+  const bool has_b = ngram > 1;
+  float acc[2][JPW][4];
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+#pragma unroll
+    for (int j = 0; j < JPW; ++j) acc[g][j][0] = acc[g][j][1] = acc[g][j][2] = acc[g][j][3] = 0.f;
+  const int64_t r0 = blockIdx.x * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  auto stage = [&](int64_t rb, int buf) {
+    float* da = gts + buf * 2 * TILE;
+    float* db = da + TILE;
+    for (int e = threadIdx.x; e < kGramTcRows * (LDR / 4); e += blockDim.x) {
+      const int rr = e / (LDR / 4), c4 = e % (LDR / 4);
+      const int64_t row = rb + rr;
+      float* pa = da + rr * LDP + c4 * 4;
+      float* pb = db + rr * LDP + c4 * 4;
+      if (row < r1) {
+        cp_async16(pa, A + row * LDR + c4 * 4);
+        if (has_b) cp_async16(pb, B + row * LDR + c4 * 4);
+      } else {
+        *reinterpret_cast<float4*>(pa) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (has_b) *reinterpret_cast<float4*>(pb) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  };
+  if (r0 < r1) stage(r0, 0);
+  cp_async_commit();
+  int buf = 0;
+  for (int64_t rb = r0; rb < r1; rb += kGramTcRows, buf ^= 1) {
+    if (rb + kGramTcRows < r1) stage(rb + kGramTcRows, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const float* ta = gts + buf * 2 * TILE;
+    const float* tb = ta + TILE;
+#pragma unroll
+    for (int k0 = 0; k0 < kGramTcRows; k0 += 8) {
+      // operand "A" of the MMA: L^T (16 x 8) from L = A (P) or B (C); operand "B": A (8 x 8)
+      uint32_t ah[2][4], al[2][4];
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        if (g == 1 && !has_b) break;
+        const float* L = g == 0 ? ta : tb;
+        const float x[4] = {L[(k0 + tig) * LDP + i0 + gid], L[(k0 + tig) * LDP + i0 + gid + 8],
+                            L[(k0 + tig + 4) * LDP + i0 + gid], L[(k0 + tig + 4) * LDP + i0 + gid + 8]};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ah[g][q] = tf32_of(x[q]);
+          al[g][q] = tf32_of(x[q] - __uint_as_float(ah[g][q]));
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < JPW; ++jj) {
+        const int j0 = (jb0 + jj) * 8;
+        const float y0 = ta[(k0 + tig) * LDP + j0 + gid], y1 = ta[(k0 + tig + 4) * LDP + j0 + gid];
+        const uint32_t bh[2] = {tf32_of(y0), tf32_of(y1)};
+        const uint32_t bl[2] = {tf32_of(y0 - __uint_as_float(bh[0])), tf32_of(y1 - __uint_as_float(bh[1]))};
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          if (g == 1 && !has_b) break;
+          mma_tf32(acc[g][jj], al[g], bh);
+          mma_tf32(acc[g][jj], ah[g], bl);
+          mma_tf32(acc[g][jj], ah[g], bh);
+        }
+      }
+    }
+    __syncthreads();  // this buffer is refilled by the next iteration's stage
+  }
+  const int LL = LDR * LDR;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    if (g >= ngram) break;
+    double* out = partials + ((int64_t)blockIdx.x * ngram + g) * LL;
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj) {
+      const int j = (jb0 + jj) * 8 + 2 * tig;
+      out[(i0 + gid) * LDR + j] = acc[g][jj][0];
+      out[(i0 + gid) * LDR + j + 1] = acc[g][jj][1];
+      out[(i0 + gid + 8) * LDR + j] = acc[g][jj][2];
+      out[(i0 + gid + 8) * LDR + j + 1] = acc[g][jj][3];
+    }
+  }
+}
+
 // Sum block partials (fixed order) and extract the rank x rank blocks.
 __global__ void k_gram_finalize(const double* __restrict__ partials, int nblk, int ngram, int ldr, int rank,
                                 double* __restrict__ outP, double* __restrict__ outC) {
@@ -1330,6 +1449,26 @@ void sum_partials_enqueue(Ctx* ctx, const double* partials, int nblk, int len, d
 void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* outP,
                    double* outC, DevBuf& scratch) {
   const int ngram = B ? 2 : 1;
+  if (ldr == 64 || ldr == 128) {  // tensor-core path
+    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, kNumSMs));
+    const int64_t rpb = (rows + nblk - 1) / nblk;
+    scratch.ensure((size_t)nblk * ngram * ldr * ldr * 8);
+    const size_t smem = (size_t)2 * 2 * kGramTcRows * (ldr + 8) * 4;
+    auto go = [&](auto kern) {
+      if (smem > 48 * 1024)
+        OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ProfScope prof_scope(ctx, kProfGram);
+      kern<<<nblk, kThreads, smem, ctx->stream>>>(A, B ? B : A, rows, rpb, ngram, scratch.as<double>());
+      ctx->count();
+      k_gram_finalize<<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
+                        ctx->stream>>>(scratch.as<double>(), nblk, ngram, ldr, rank, outP, outC);
+      ctx->count();
+      check_launch();
+    };
+    if (ldr == 64) go(k_gram_tc<64>);
+    else go(k_gram_tc<128>);
+    return;
+  }
   const int nsub = (ldr / 4) * (ldr / 4);
   const int nitems = ngram * nsub;
   const int per_pass = kGramIPT * kThreads;

@@ -229,3 +229,19 @@ def test_weight_solve_vs_oracle_large_ranks(R):
     s, tr, _, _ = O.temporal_solve(O.Slice(dims, subs0, vals), A, "poisson", ocfg, 3)
     assert rel_err(res.weights, s) < 1e-4
     np.testing.assert_allclose(res.trace.objective, tr, rtol=1e-4)
+
+
+@pytest.mark.parametrize("R", [40, 64, 100, 128])
+def test_tensor_core_grams_vs_oracle(R):
+    """ldr 64 / 128 Grams run on tensor cores (split-TF32 mma): fp32-level accuracy,
+    checked norm-wise like the gradients (entries of a Hadamard of Grams of
+    random signs cancel, so elementwise relative error is meaningless near 0)."""
+    rng = np.random.default_rng(R)
+    dims = (3000, 257, 40)
+    A = [rng.uniform(-1, 1, (d, R)) for d in dims]
+    B = [a + 0.1 * rng.uniform(-1, 1, a.shape) for a in A]
+    for mode in (None, 1):
+        g, want = P.gram(A, mode), O.hadamard_gram(A, mode)
+        assert rel_err(g, want) < 1e-5
+        np.testing.assert_allclose(np.diag(g), np.diag(want), rtol=1e-5)
+        assert rel_err(P.gram(A, mode, other_factors=B), O.hadamard_gram(A, mode, B)) < 1e-5
