@@ -319,6 +319,50 @@ SamplesP SampleBufs::sample_set(const Slice* X) const {
   return S;                            // nz_scale stays eta / p (p draws)
 }
 
+// Two-deep draw pipeline.  A draw depends only on the slice and its key, never on
+// the iterate, so the draw of iteration it+1 is enqueued on a side stream before
+// iteration it's evaluation is enqueued on the context stream and overlaps it.
+// The side stream first waits for everything already enqueued on the context
+// stream (which includes the last reader of the buffer set it refills).
+struct DrawPipe {
+  SampleBufs buf[2];
+  SamplesP S[2];
+  cudaStream_t side = nullptr;
+  cudaEvent_t go = nullptr, done[2] = {nullptr, nullptr};
+  void init() {
+    if (side) return;
+    OGCP_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    OGCP_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
+    for (auto& e : done) OGCP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  void size(int64_t p, int64_t q, int ndim, bool merged, bool semi) {
+    for (auto& b : buf) {
+      b.size(p, q, ndim, merged);
+      b.semi = semi;
+    }
+  }
+  bool merged() const { return buf[0].merged; }
+  void issue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t budget, long long code, int slot) {
+    init();
+    const cudaStream_t main = ctx->stream;
+    OGCP_CUDA(cudaEventRecord(go, main));
+    OGCP_CUDA(cudaStreamWaitEvent(side, go, 0));
+    ctx->stream = side;
+    try {
+      S[slot] = buf[slot].draw(ctx, X, g, budget, code);
+    } catch (...) {
+      ctx->stream = main;
+      throw;
+    }
+    ctx->stream = main;
+    OGCP_CUDA(cudaEventRecord(done[slot], side));
+  }
+  SamplesP take(Ctx* ctx, int slot) {
+    OGCP_CUDA(cudaStreamWaitEvent(ctx->stream, done[slot], 0));
+    return S[slot];
+  }
+};
+
 // Merged (count) form pays off when the nonzero draws cover the slice densely
 // (p = "all" draws eta with replacement, sampling.py:71-77, 125).
 static bool use_merged(const Ctx* ctx, const Slice* X, int64_t p) {
@@ -441,7 +485,8 @@ static double model_sq_host(const std::vector<double>& P, int ndim, int R, const
 struct FactorWork {
   DevBuf grads;
   HistBufs hb;
-  SampleBufs obj, grad;
+  SampleBufs obj;
+  DrawPipe grad;
 };
 
 static FactorWork& factor_work() {
@@ -488,7 +533,8 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   int64_t po, qo, p, q;
   resolve_counts(cfg->samples.obj_nonzeros, cfg->samples.obj_zeros, X, &po, &qo);
   resolve_counts(cfg->samples.grad_nonzeros, cfg->samples.grad_zeros, X, &p, &q);
-  static thread_local SampleBufs obj, grad;
+  static thread_local SampleBufs obj;
+  static thread_local DrawPipe grad;
   const bool dense = dense_mode(cfg, L.kind);
   SamplesP So{};
   int64_t budget = 0;
@@ -498,9 +544,8 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     draw_sync(ctx, X, keyed(seed, {t, 2}), po, qo, cfg->samples.max_rejects, obj, semi);
     So = sharded(ctx, obj.sample_set(X));
     precheck_draw(X, p, semi ? 0 : q);
-    grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
-    if (grad.merged) prepare_buckets(ctx, X, M.ldr);
-    grad.semi = semi;
+    grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p), semi);
+    if (grad.merged()) prepare_buckets(ctx, X, M.ldr);
     budget = budget_of(q, cfg->samples.max_rejects);
   }
   ctx->partials.ensure((size_t)kNumSMs * 8 * ldr * 8 + 64);
@@ -575,6 +620,7 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     for (int attempt = 0;; ++attempt) {
       reset_flags(ctx);
       const long long ev0 = ev;
+      if (!dense) grad.issue(ctx, X, keyed(seed, {t, 1, epoch, 0}), budget, code_of(ev0, 0), 0);
       for (int it = 0; it < cfg->iters_weights; ++it) {
         const long long e = ev++;
         const int64_t cnt = i + it + 1;
@@ -586,7 +632,9 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
                               cfg->adam_eps, cfg->lower_bound, code_of(e, 2));
           continue;
         }
-        SamplesP Sg = sharded(ctx, grad.draw(ctx, X, keyed(seed, {t, 1, epoch, it}), budget, code_of(e, 0)));
+        if (it + 1 < cfg->iters_weights)
+          grad.issue(ctx, X, keyed(seed, {t, 1, epoch, it + 1}), budget, code_of(e + 1, 0), (it + 1) & 1);
+        SamplesP Sg = sharded(ctx, grad.take(ctx, it & 1));
         int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1));
         const double* gparts = part;
         if (ctx->world > 1) {  // sum the shard gradients across ranks, then the replicated step
@@ -605,7 +653,7 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
       if (r == 0) break;
       // shortfall: restore the epoch-start snapshot and redo with more candidates
       // (r == 2: a merged-draw counter wrapped; redo with per-draw evaluation)
-      if (r == 2) grad.size(p, q, X->ndim, false);
+      if (r == 2) grad.size(p, q, X->ndim, false, cfg->samples.semi_stratified != 0);
       else ctx->slack *= 4.0;
       OGCP_CUDA(cudaMemcpyAsync(ws, ws + 3 * ldr, 3 * ldr * 8, cudaMemcpyDeviceToDevice, st));
       OGCP_CUDA(cudaMemcpyAsync(hsc, ws, ldr * 8, cudaMemcpyDeviceToHost, st));
@@ -749,7 +797,7 @@ static void adam_epoch(Ctx* ctx, const ModelP& M, float* const* A, ogcp_adam_sta
 // joins the history coefficients of K5.
 static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* const* A, const float* s_f,
                              const LossP& L, float* const* old_factors, bool hist, const ogcp_solver_config* cfg,
-                             ogcp_adam_state* ad, double rate_i, const Pcg64& g, int64_t budget, FactorWork& W,
+                             ogcp_adam_state* ad, double rate_i, const SamplesP* Sdrawn, FactorWork& W,
                              long long ev, const double* dense_s = nullptr) {
   const int RR = M.rank * M.rank;
   const bool dense = dense_s != nullptr;
@@ -762,8 +810,7 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
   if (dense) {
     sgrad_enqueue(ctx, all_nonzeros(ctx, X, -2.0), M, s_f, kIdentityLoss, gp, code_of(ev, 1));
   } else {
-    SamplesP Sg = sharded(ctx, W.grad.draw(ctx, X, g, budget, code_of(ev, 0)));
-    sgrad_enqueue(ctx, Sg, M, s_f, L, gp, code_of(ev, 1));
+    sgrad_enqueue(ctx, *Sdrawn, M, s_f, L, gp, code_of(ev, 1));
   }
   comm_allreduce_sum(ctx, W.grads.as<float>(), off);  // multi-GPU: sum of the shard gradients
   const bool coeffs = hist || dense;
@@ -831,9 +878,8 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     draw_sync(ctx, X, keyed(seed, {t, 4}), po, qo, cfg->samples.max_rejects, W.obj, semi);
     So = sharded(ctx, W.obj.sample_set(X));
     precheck_draw(X, p, semi ? 0 : q);
-    W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
-    if (W.grad.merged) prepare_buckets(ctx, X, M.ldr);
-    W.grad.semi = semi;
+    W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p), semi);
+    if (W.grad.merged()) prepare_buckets(ctx, X, M.ldr);
     budget = budget_of(q, cfg->samples.max_rejects);
   }
   const double* dense_w = dense ? weights : nullptr;
@@ -850,19 +896,26 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     for (int attempt = 0;; ++attempt) {
       reset_flags(ctx);
       const long long ev0 = ev;
+      if (!dense) W.grad.issue(ctx, X, keyed(seed, {t, 3, epoch, 0}), budget, code_of(ev0, 0), 0);
       for (int it = 0; it < cfg->iters_factors; ++it) {
         const int64_t cnt = iter + it + 1;
         const double rate_i = ad->rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
                               (1.0 - std::pow(cfg->beta1, (double)cnt));
-        factor_iteration(ctx, X, M, A, s_f, L, old_factors, hist, cfg, ad, rate_i, keyed(seed, {t, 3, epoch, it}),
-                         budget, W, ev++, dense ? s_dev : nullptr);
+        SamplesP Sg{};
+        if (!dense) {
+          if (it + 1 < cfg->iters_factors)
+            W.grad.issue(ctx, X, keyed(seed, {t, 3, epoch, it + 1}), budget, code_of(ev + 1, 0), (it + 1) & 1);
+          Sg = sharded(ctx, W.grad.take(ctx, it & 1));
+        }
+        factor_iteration(ctx, X, M, A, s_f, L, old_factors, hist, cfg, ad, rate_i, &Sg, W, ev++,
+                         dense ? s_dev : nullptr);
       }
       comm_sync_flags(ctx);
       fetch_flags(ctx);
       OGCP_CUDA(cudaStreamSynchronize(st));
       int r = check_flags(ctx, X, L.kind, budget, "factor solve", t);
       if (r == 0) break;
-      if (r == 2) W.grad.size(p, q, X->ndim, false);
+      if (r == 2) W.grad.size(p, q, X->ndim, false, cfg->samples.semi_stratified != 0);
       else ctx->slack *= 4.0;
       adam_epoch(ctx, M, A, ad, false);  // restore the epoch-start state (no rate decay)
       ev = ev0;
@@ -944,9 +997,8 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
     draw_sync(ctx, X, keyed(seed, {seed_key, 8}), po, qo, cfg->samples.max_rejects, W.obj, semi);
     So = sharded(ctx, W.obj.sample_set(X));
     precheck_draw(X, p, semi ? 0 : q);
-    W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p));
-    if (W.grad.merged) prepare_buckets(ctx, X, M.ldr);
-    W.grad.semi = semi;
+    W.grad.size(p, q, X->ndim, p > 0 && use_merged(ctx, X, p), semi);
+    if (W.grad.merged()) prepare_buckets(ctx, X, M.ldr);
     budget = budget_of(q, cfg->samples.max_rejects);
   }
   const char* what = "static solve";
@@ -997,6 +1049,7 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
     for (int attempt = 0;; ++attempt) {
       reset_flags(ctx);
       const long long ev0 = ev;
+      if (!dense) W.grad.issue(ctx, X, keyed(seed, {seed_key, 7, epoch, 0}), budget, code_of(ev0, 0), 0);
       for (int it = 0; it < iters; ++it) {
         const long long e = ev++;
         const int64_t cnt = iter + it + 1;
@@ -1024,7 +1077,9 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
                                   code_of(e, 2));
           continue;
         }
-        SamplesP Sg = sharded(ctx, W.grad.draw(ctx, X, keyed(seed, {seed_key, 7, epoch, it}), budget, code_of(e, 0)));
+        if (it + 1 < iters)
+          W.grad.issue(ctx, X, keyed(seed, {seed_key, 7, epoch, it + 1}), budget, code_of(e + 1, 0), (it + 1) & 1);
+        SamplesP Sg = sharded(ctx, W.grad.take(ctx, it & 1));
         // both gradients at the current iterate, before either update
         sgrad_enqueue(ctx, Sg, M, s_f, L, gp, code_of(e, 1));
         int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1));
@@ -1048,7 +1103,7 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
       OGCP_CUDA(cudaStreamSynchronize(st));
       int r = check_flags(ctx, X, L.kind, budget, what, seed_key);
       if (r == 0) break;
-      if (r == 2) W.grad.size(p, q, X->ndim, false);
+      if (r == 2) W.grad.size(p, q, X->ndim, false, cfg->samples.semi_stratified != 0);
       else ctx->slack *= 4.0;
       adam_epoch(ctx, M, A, ad, false);
       weights_epoch(false);

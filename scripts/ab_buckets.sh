@@ -1,2 +1,6 @@
-python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-for r in 64 128; do python scripts/config_bench.py c5 --rank $r --slices 1 2>&1 | tail -1; done
+python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab.json 2> gpurun_out/ab.err
+python -c "
+import json; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); k=d['kernel_ms']; n=d['kernel_launch_brackets']
+print(round(d['value']/1e9,3), d['ms_per_step'], {c: round(k[c]/max(n[c],1),3) for c in k})"
+python scripts/stream_bench.py --config c2 --slices 6 2>&1 | tail -1
