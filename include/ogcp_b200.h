@@ -305,6 +305,10 @@ int ogcp_dense_gaussian_gradients(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp
                                   int64_t t, double reg_factors, double reg_weights, float* const* grads_dev,
                                   double* weight_grad);
 
+/* Diagnostics: a one-rank NCCL communicator round trip through every collective
+ * the multi-GPU solves use (checks the run-time loaded libnccl.so.2 on one GPU). */
+int ogcp_comm_selftest(ogcp_ctx* ctx, int32_t* mismatches);
+
 /* Diagnostics: the gradient sample set a solve iteration would evaluate on
  * this context (merged/bucketed form and multi-GPU share included), keyed
  * rng_at(seed, *key): this rank's nonzero ordinals with multiplicities and its

@@ -126,6 +126,7 @@ _SIGS = {
     "ogcp_dense_gaussian_gradients": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(ModelC), C.POINTER(C.c_void_p),
                                                 c_f64p, c_f64p, c_i64p, C.c_int32, C.c_double, C.c_double,
                                                 C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_void_p), c_f64p]),
+    "ogcp_comm_selftest": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "ogcp_debug_solve_draw": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, c_i64p, C.c_int32, C.c_int64, C.c_int64,
                                         C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, c_i64p, C.c_int64,
                                         C.c_void_p, c_i64p]),

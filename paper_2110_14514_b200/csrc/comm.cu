@@ -120,6 +120,43 @@ void comm_unique_id(uint8_t* out) {
   memcpy(out, &uid, sizeof(uid));
 }
 
+// One-rank communicator round trip through every collective the solves use
+// (fp32 / fp64 sum, int64 min / max): checks the dlopen'd NCCL entry points and
+// their signatures on a single GPU.  Returns the number of mismatches.
+int comm_selftest(Ctx* ctx) {
+  OGCP_CUDA(cudaSetDevice(ctx->device));
+  ncclUniqueId uid;
+  nccl_check(api().GetUniqueId(&uid), "ncclGetUniqueId");
+  ncclComm_t comm;
+  nccl_check(api().CommInitRank(&comm, 1, uid, 0), "ncclCommInitRank");
+  DevBuf buf;
+  char* d = static_cast<char*>(buf.ensure(256));
+  const float hf[4] = {1.5f, -2.f, 3.25f, 0.f};
+  const double hd[2] = {1e300, -7.5};
+  const long long hl[4] = {5, -3, 1LL << 40, 0};
+  OGCP_CUDA(cudaMemcpy(d, hf, sizeof(hf), cudaMemcpyHostToDevice));
+  OGCP_CUDA(cudaMemcpy(d + 64, hd, sizeof(hd), cudaMemcpyHostToDevice));
+  OGCP_CUDA(cudaMemcpy(d + 128, hl, sizeof(hl), cudaMemcpyHostToDevice));
+  cudaStream_t st = ctx->stream;
+  nccl_check(api().AllReduce(d, d, 4, ncclFloat32, ncclSum, comm, st), "ncclAllReduce");
+  nccl_check(api().AllReduce(d + 64, d + 64, 2, ncclFloat64, ncclSum, comm, st), "ncclAllReduce");
+  nccl_check(api().AllReduce(d + 128, d + 128, 2, ncclInt64, ncclMin, comm, st), "ncclAllReduce");
+  nccl_check(api().AllReduce(d + 144, d + 144, 2, ncclInt64, ncclMax, comm, st), "ncclAllReduce");
+  OGCP_CUDA(cudaStreamSynchronize(st));
+  float rf[4];
+  double rd[2];
+  long long rl[4];
+  OGCP_CUDA(cudaMemcpy(rf, d, sizeof(rf), cudaMemcpyDeviceToHost));
+  OGCP_CUDA(cudaMemcpy(rd, d + 64, sizeof(rd), cudaMemcpyDeviceToHost));
+  OGCP_CUDA(cudaMemcpy(rl, d + 128, sizeof(rl), cudaMemcpyDeviceToHost));
+  if (api().CommDestroy) api().CommDestroy(comm);
+  int bad = 0;
+  for (int i = 0; i < 4; ++i) bad += rf[i] != hf[i];
+  for (int i = 0; i < 2; ++i) bad += rd[i] != hd[i];
+  for (int i = 0; i < 4; ++i) bad += rl[i] != hl[i];
+  return bad;
+}
+
 void comm_destroy(Ctx* ctx) {
   if (ctx->comm && api().CommDestroy) api().CommDestroy((ncclComm_t)ctx->comm);
   ctx->comm = nullptr;

@@ -13,5 +13,6 @@ void comm_sync_flags(Ctx* ctx);
 void comm_init(Ctx* ctx, const uint8_t* id, int rank, int world);
 void comm_unique_id(uint8_t* out128);
 void comm_destroy(Ctx* ctx);
+int comm_selftest(Ctx* ctx);
 
 }  // namespace ogcp

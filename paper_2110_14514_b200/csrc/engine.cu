@@ -1744,6 +1744,12 @@ int ogcp_solve_static(ogcp_ctx* ctx, const ogcp_slice* s, const ogcp_solver_conf
   OGCP_API_END
 }
 
+int ogcp_comm_selftest(ogcp_ctx* ctx, int32_t* mismatches) {
+  OGCP_API_BEGIN
+  *mismatches = comm_selftest(ctx);
+  OGCP_API_END
+}
+
 int ogcp_debug_solve_draw(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, const int64_t* key, int32_t nkey,
                           int64_t p, int64_t q, int64_t max_rejects, int32_t ldr, int64_t cap_nz, int32_t* ord_out,
                           uint8_t* cnt_out, int64_t* n_nz, int64_t cap_zero, int32_t* zero_out, int64_t* n_zero) {

@@ -94,3 +94,12 @@ def test_sharded_gradients_sum_to_single_gpu(slice_1e5):
         for k in range(3):
             tot = sum(p_[k] for p_ in parts)
             assert np.linalg.norm(tot - full[k]) <= 1e-5 * np.linalg.norm(full[k])
+
+
+def test_nccl_entry_points_one_rank():
+    """The run-time loaded NCCL (libnccl.so.2) and every collective signature the
+    multi-GPU solves use, exercised on a one-rank communicator."""
+    import ctypes as C
+    bad = C.c_int32(-1)
+    _lib.check(_lib.lib().ogcp_comm_selftest(_lib.ctx(), C.byref(bad)))
+    assert bad.value == 0
