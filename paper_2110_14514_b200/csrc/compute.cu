@@ -1057,31 +1057,61 @@ __global__ void __launch_bounds__(kThreads) k_factor_update_tiled(int64_t rows, 
   extern __shared__ __align__(16) float k5s[];
   float* sm = k5s;                 // [LDR][LDR] Mk (zero padded)
   float* sn = sm + LDR * LDR;      // [LDR][LDR] Nk
-  float* sa = sn + LDR * LDR;      // [TR][LDR] A tile
-  float* so = sa + TR * LDR;       // [TR][LDR] Aold tile
+  float* tiles = sn + LDR * LDR;   // 2 buffers x {A tile, Aold tile} [TR][LDR]
   const bool has_old = Aold != nullptr;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c0 = lane * CPT;
+  const int64_t ntiles = (rows + TR - 1) / TR;
+  // rows of tile t into buffer b by cp.async (A and Aold); rows past the end are zeroed
+  auto stage = [&](int64_t tile, int b) {
+    float* ta = tiles + b * 2 * TR * LDR;
+    float* to = ta + TR * LDR;
+    const int64_t r0 = tile * TR;
+    for (int e = threadIdx.x; e < TR * LDR / 4; e += blockDim.x) {
+      const int rr = e / (LDR / 4);
+      const int64_t at = (r0 + rr) * LDR + (e % (LDR / 4)) * 4;
+      if (r0 + rr < rows) {
+        cp_async16(ta + e * 4, A + at);
+        if (has_old) cp_async16(to + e * 4, Aold + at);
+        else reinterpret_cast<float4*>(to)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        reinterpret_cast<float4*>(ta)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+        reinterpret_cast<float4*>(to)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  };
+  if (blockIdx.x < ntiles) stage(blockIdx.x, 0);
+  cp_async_commit();
   for (int e = threadIdx.x; e < LDR * LDR; e += blockDim.x) {
     const int r = e / LDR, c = e % LDR;
     const bool in = r < rank && c < rank;
     sm[e] = in ? Mk[r * rank + c] : 0.f;
     sn[e] = (in && has_old) ? Nk[r * rank + c] : 0.f;
   }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c0 = lane * CPT;
   bool bad = false;
-  const int64_t ntiles = (rows + TR - 1) / TR;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int buf = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
     const int64_t r0 = tile * TR;
-    __syncthreads();  // previous tile consumed (and Mk / Nk staged on the first pass)
-    for (int e = threadIdx.x; e < TR * LDR / 4; e += blockDim.x) {
-      const int rr = e / (LDR / 4);
-      const bool ok = r0 + rr < rows;
-      const int64_t at = (r0 + rr) * LDR + (e % (LDR / 4)) * 4;
-      reinterpret_cast<float4*>(sa)[e] = ok ? *reinterpret_cast<const float4*>(A + at) : make_float4(0.f, 0.f, 0.f, 0.f);
-      reinterpret_cast<float4*>(so)[e] =
-          (ok && has_old) ? __ldg(reinterpret_cast<const float4*>(Aold + at)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, buf ^ 1);
+    cp_async_commit();
+    // this thread's G / u / v elements, fetched while the tile lands and the product runs
+    float gq[4][CPT], uq[4][CPT], vq[4][CPT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t row = r0 + w * 4 + i;
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const bool ok = row < rows && c0 + j < rank;
+        const int64_t at = row * LDR + c0 + j;
+        gq[i][j] = ok ? __ldg(G + at) : 0.f;
+        uq[i][j] = ok ? u[at] : 0.f;
+        vq[i][j] = ok ? v[at] : 0.f;
+      }
     }
-    __syncthreads();
+    cp_async_wait<1>();
+    __syncthreads();  // tile `buf` (and Mk / Nk on the first pass) visible to all
+    const float* sa = tiles + buf * 2 * TR * LDR;
+    const float* so = sa + TR * LDR;
     float h[4][CPT];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -1111,12 +1141,13 @@ __global__ void __launch_bounds__(kThreads) k_factor_update_tiled(int64_t rows, 
       for (int j = 0; j < CPT; ++j) {
         const int c = c0 + j;
         if (c >= rank) continue;
-        const int64_t at = row * LDR + c;
         const float a = sa[(w * 4 + i) * LDR + c];
-        const float g = __ldg(G + at) + reg * a + h[i][j];
-        if (!adam_regs(A, u, v, at, a, g, u[at], v[at], b1, omb1, b2, omb2, rate_i, eps, lower)) bad = true;
+        const float g = gq[i][j] + reg * a + h[i][j];
+        if (!adam_regs(A, u, v, row * LDR + c, a, g, uq[i][j], vq[i][j], b1, omb1, b2, omb2, rate_i, eps, lower))
+          bad = true;
       }
     }
+    __syncthreads();  // buffer `buf` is restaged two tiles later
   }
   if (bad) report(flags, kFlagDiverge, code, 0);
 }
@@ -1551,7 +1582,7 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
     }
   } else if (Mk && ldr <= 128) {
     auto launch = [&](auto kern, int L) {
-      const size_t smem = ((size_t)2 * L * L + (size_t)2 * kK5TileRows * L) * 4;
+      const size_t smem = ((size_t)2 * L * L + (size_t)4 * kK5TileRows * L) * 4;
       if (smem > 48 * 1024)
         OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int per_sm = 0;
