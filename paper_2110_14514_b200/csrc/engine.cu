@@ -331,7 +331,10 @@ struct DrawPipe {
   cudaEvent_t go = nullptr, done[2] = {nullptr, nullptr};
   void init() {
     if (side) return;
-    OGCP_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;  // the prefetching draws take the lower priority: they fill gaps
+    OGCP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    (void)hi;
+    OGCP_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
     OGCP_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
     for (auto& e : done) OGCP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
