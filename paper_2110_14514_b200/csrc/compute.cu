@@ -16,6 +16,7 @@
 // sampling.py:177-206; gram kernels.py:75-98; _add_reg_and_history
 // solvers.py:159-179; Adam.step adam.py:51-81; _ensure_finite solvers.py:188-194.
 #include <algorithm>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "compute.cuh"
@@ -1339,13 +1340,37 @@ static void dispatch_layout(Layout kind, int ndim, int ldr, F&& f) {
   }
 }
 
+// Opt a kernel into `smem` bytes of dynamic shared memory (> 48 KB), once per size.
+template <class K>
+static void allow_smem(K kern, size_t smem) {
+  if (smem <= 48 * 1024) return;
+  static thread_local std::unordered_map<const void*, size_t> done;
+  size_t& have = done[(const void*)kern];
+  if (have >= smem) return;
+  OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  have = smem;
+}
+
+// Resident blocks per SM of a kernel at kThreads threads and `smem` dynamic bytes,
+// cached per (kernel, smem): the occupancy query is a host API call, and the small
+// streams (c1/c2) launch kernels every few microseconds.
+template <class K>
+static int occupancy(K kern, size_t smem) {
+  static thread_local std::unordered_map<uint64_t, int> cache;
+  const uint64_t key = (uint64_t)(uintptr_t)(const void*)kern * 1000003ull ^ (uint64_t)smem;
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  OGCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  cache.emplace(key, per_sm);
+  return per_sm;
+}
+
 // Grid for a grid-stride sample kernel: enough blocks to cover the samples once,
 // capped at the number that can be co-resident (occupancy API).
 template <class K>
 static int sample_grid(K kern, size_t smem, int64_t total, int G, int U) {
-  int per_sm = 0;
-  OGCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
-  per_sm = std::max(per_sm, 1);
+  const int per_sm = std::max(occupancy(kern, smem), 1);
   const int64_t per_block = (int64_t)(kThreads / G) * U;
   const int64_t need = (total + per_block - 1) / per_block;
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)kNumSMs * per_sm));
@@ -1397,8 +1422,7 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
     constexpr int U = decltype(Uc)::value;
     auto launch = [&](auto kern) {
-      if (smem > 48 * 1024)
-        OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      allow_smem(kern, smem);
       const int grid = sample_grid(kern, smem, total, G, U);
       kern<<<grid, kThreads, smem, ctx->stream>>>(S, M, s_f, L, GP, PV, ctx->flags.as<DevFlags>(), code, split,
                                                   ybuf);
@@ -1486,8 +1510,7 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
     scratch.ensure((size_t)nblk * ngram * ldr * ldr * 8);
     const size_t smem = (size_t)2 * 2 * kGramTcRows * (ldr + 8) * 4;
     auto go = [&](auto kern) {
-      if (smem > 48 * 1024)
-        OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      allow_smem(kern, smem);
       ProfScope prof_scope(ctx, kProfGram);
       kern<<<nblk, kThreads, smem, ctx->stream>>>(A, B ? B : A, rows, rpb, ngram, scratch.as<double>());
       ctx->count();
@@ -1509,8 +1532,7 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
   scratch.ensure((size_t)nblk * ngram * ldr * ldr * 8);
   size_t smem = (size_t)4 * kGramTile * ldr * 4;  // two buffers x (A tile, B tile)
   smem = std::max(smem, (size_t)kThreads * 16 * 8);
-  if (smem > 48 * 1024)
-    OGCP_CUDA(cudaFuncSetAttribute(k_gram2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  allow_smem(k_gram2, smem);
   ProfScope prof_scope(ctx, kProfGram);
   for (int item0 = 0; item0 < nitems; item0 += per_pass) {
     const int n_pass = std::min(per_pass, nitems - item0);
@@ -1563,8 +1585,7 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
     int GR = 1;
     while (GR < rank) GR <<= 1;
     auto launch = [&](auto kern) {
-      int per_sm = 0;
-      OGCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
+      const int per_sm = occupancy(kern, 0);
       const int64_t rows_per_block = (kThreads / GR) * kK5Rows;
       const int grid = (int)std::max<int64_t>(
           1, std::min<int64_t>((rows + rows_per_block - 1) / rows_per_block, (int64_t)kNumSMs * std::max(per_sm, 1)));
@@ -1583,10 +1604,8 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
   } else if (Mk && ldr <= 128) {
     auto launch = [&](auto kern, int L) {
       const size_t smem = ((size_t)2 * L * L + (size_t)4 * kK5TileRows * L) * 4;
-      if (smem > 48 * 1024)
-        OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int per_sm = 0;
-      OGCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+      allow_smem(kern, smem);
+      const int per_sm = occupancy(kern, smem);
       const int64_t tiles = (rows + kK5TileRows - 1) / kK5TileRows;
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)kNumSMs * std::max(per_sm, 1)));
       kern<<<grid, kThreads, smem, ctx->stream>>>(rows, rank, A, Aold, G, u, v, Mk, Nk, (float)reg, (float)rate_i,
@@ -1600,8 +1619,7 @@ void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, 
     const bool stage = need > 0 && need <= 200 * 1024;
     const size_t smem = stage ? need : 0;
     auto launch = [&](auto kern) {
-      if (smem > 48 * 1024)
-        OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      allow_smem(kern, smem);
       const int64_t groups = kThreads / 32;
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + groups - 1) / groups, kNumSMs * 4));
       kern<<<grid, kThreads, smem, ctx->stream>>>(rows, rank, ldr, A, Aold, G, u, v, Mk, Nk, (float)reg,
@@ -1636,8 +1654,7 @@ void hist_penalty_enqueue(Ctx* ctx, int ndim, int rank, const double* Poo, const
     qglobal = static_cast<double*>(qbuf.ensure(need));
     smem = 0;
   }
-  if (smem > 48 * 1024)
-    OGCP_CUDA(cudaFuncSetAttribute(k_hist_penalty, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  allow_smem(k_hist_penalty, smem);
   k_hist_penalty<<<1, 256, smem, ctx->stream>>>(ndim, rank, Poo, Pon, Pnn, window_s, window_coef, H, out, qglobal);
   ctx->count();
   check_launch();
