@@ -113,14 +113,16 @@ struct WordGen {
   }
 };
 
-__device__ __forceinline__ uint64_t block_word0(const long long* w0p) {
-  return (uint64_t)(w0p ? *w0p : 0) + (uint64_t)blockIdx.x * kBlockWords;
+__device__ __forceinline__ uint64_t tile_word0(const long long* w0p, int64_t tile) {
+  return (uint64_t)(w0p ? *w0p : 0) + (uint64_t)tile * kBlockWords;
 }
+__device__ __forceinline__ uint64_t block_word0(const long long* w0p) { return tile_word0(w0p, blockIdx.x); }
 
-// All threads of the block call this (contains __syncthreads).
-__device__ __forceinline__ WordGen block_wordgen(const StreamSpec& sp, const long long* w0p) {
+// All threads of the block call this (contains __syncthreads).  Tile `tile` of the
+// stream = words [tile * kBlockWords, (tile + 1) * kBlockWords) after w0.
+__device__ __forceinline__ WordGen tile_wordgen(const StreamSpec& sp, const long long* w0p, int64_t tile) {
   __shared__ unsigned long long base[2];
-  const uint64_t wb = block_word0(w0p);
+  const uint64_t wb = tile_word0(w0p, tile);
   if (threadIdx.x == 0) {
     const u128 s = state_after(sp, (wb >> 1) + 1);
     base[0] = (unsigned long long)(s >> 64);
@@ -135,6 +137,9 @@ __device__ __forceinline__ WordGen block_wordgen(const StreamSpec& sp, const lon
   g.out = pcg_output(g.st);
   g.half = (int)(wb & 1ull);  // chunk starts share the block's word parity (kChunkWords even)
   return g;
+}
+__device__ __forceinline__ WordGen block_wordgen(const StreamSpec& sp, const long long* w0p) {
+  return tile_wordgen(sp, w0p, blockIdx.x);
 }
 
 template <int NCOL>
@@ -447,6 +452,88 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_hits(ZeroSpec zs, const i
     uint32_t s = 0;
     for (int j = 0; j < kScanThreads / 32; ++j) s += wsum[j];
     bcount[blockIdx.x] = s;
+  }
+}
+
+// Small zero strata (lazy layout): hit test + flagging, the miss scan and the
+// q-th-miss search of passes A / B / locate in one block walking the rows in
+// order; it stops at the tile holding the q-th miss.
+__global__ void __launch_bounds__(kScanThreads) k_zero_fused(ZeroSpec zs, int32_t* __restrict__ cand,
+                                                             const long long* __restrict__ elems_avail,
+                                                             int64_t rows_max,
+                                                             const unsigned long long* __restrict__ table,
+                                                             uint64_t mask, const unsigned int* __restrict__ filter,
+                                                             uint64_t fmask, int64_t q, long long* __restrict__ rows_used,
+                                                             long long* __restrict__ hits_before,
+                                                             long long* __restrict__ misses_out) {
+  __shared__ long long carry;
+  __shared__ int found;
+  __shared__ int wsum[kScanThreads / 32];
+  if (threadIdx.x == 0) {
+    carry = 0;
+    found = 0;
+  }
+  __syncthreads();
+  const int64_t rows = zero_rows_avail(zs, elems_avail, rows_max);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t base = 0; base < rows_max; base += kRowsPerBlock) {
+    const int64_t r0 = base + (int64_t)threadIdx.x * kRowsPerThread;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int j = 0; j < kRowsPerThread; ++j) {
+      const int64_t r = r0 + j;
+      if (r >= rows) continue;
+      uint64_t key = 0;
+      for (int k = 0; k < zs.ndim; ++k) {
+        const int cm = zs.colmap[k];
+        const uint32_t c = cm < 0 ? 0u : (uint32_t)cand[r * zs.ncol + cm];
+        key += (uint64_t)c * zs.st.s[k];
+      }
+      bool present = false;
+      if (table) {
+        present = true;
+        if (filter) {
+          const uint64_t b = filter_bit(mix64(key), fmask);
+          present = (__ldg(filter + (b >> 5)) >> (b & 31)) & 1u;
+        }
+        if (present) present = hash_contains(table, mask, key);
+      }
+      if (present) cand[r * zs.ncol] = -1;  // lazy layout: a hit keeps its slot, flagged
+      else bits |= 1u << j;
+    }
+    const int cnt = __popc(bits);
+    int inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += o;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    int pre = 0, tot = 0;
+    for (int j = 0; j < kScanThreads / 32; ++j) {
+      if (j < w) pre += wsum[j];
+      tot += wsum[j];
+    }
+    const long long c0 = carry;
+    long long rank = c0 + pre + inc - cnt;
+    for (int j = 0; j < kRowsPerThread; ++j) {
+      if (!(bits & (1u << j))) continue;
+      if (rank == q - 1) {
+        *rows_used = r0 + j + 1;
+        *hits_before = (r0 + j) - (q - 1);
+        found = 1;
+      }
+      ++rank;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c0 + tot;
+    __syncthreads();
+    if (found) break;
+  }
+  if (threadIdx.x == 0) {
+    *misses_out = carry;
+    if (!found) *rows_used = rows_max;
   }
 }
 
@@ -780,6 +867,89 @@ __global__ void k_hist_permute(const uint32_t* __restrict__ hist, const int32_t*
   }
 }
 
+// Small draws (c1/c2 shapes): passes 1-3 fused in one block that walks the tiles
+// in order with a running (column, element) carry -- the same chunk maps, scan
+// and staged write as above, in one launch instead of three.
+constexpr int64_t kFusedMaxTiles = 16;
+template <int NCOL>
+__global__ void __launch_bounds__(kScanThreads) k_draw_fused(StreamSpec sp, const long long* w0p, int64_t nchunks,
+                                                             int64_t target, int32_t* __restrict__ out,
+                                                             long long* __restrict__ end_word,
+                                                             long long* __restrict__ elems_total) {
+  __shared__ int32_t stage[kBlockWords];
+  __shared__ long long carry_e;
+  __shared__ int carry_c;
+  if (threadIdx.x == 0) {
+    carry_e = 0;
+    carry_c = 0;
+  }
+  const int64_t ntiles = (nchunks + kScanThreads - 1) / kScanThreads;
+  for (int64_t tile = 0; tile < ntiles; ++tile) {
+    const int64_t chunk = tile * kScanThreads + threadIdx.x;
+    WordGen g = tile_wordgen(sp, w0p, tile);  // syncs: carry from the previous tile is visible
+    const WordGen g0 = g;
+    Map<NCOL> m = identity_map<NCOL>();
+    if (chunk < nchunks) {
+      int col[NCOL];
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) col[c] = c;
+      for (int i = 0; i < kChunkWords; ++i) {
+        const uint32_t w = g.next();
+#pragma unroll
+        for (int c = 0; c < NCOL; ++c) {
+          const int cc = col[c];
+          uint32_t n = sp.n[0], thr = sp.thr[0];
+#pragma unroll
+          for (int j = 1; j < NCOL; ++j)
+            if (j == cc) { n = sp.n[j]; thr = sp.thr[j]; }
+          if ((uint32_t)((uint64_t)w * n) >= thr) {
+            m.c[c] += 1;
+            col[c] = cc + 1 == NCOL ? 0 : cc + 1;
+          }
+        }
+      }
+    }
+    Map<NCOL> excl, agg;
+    block_scan_maps<NCOL>(m, excl, agg);
+    const int bcol = carry_c;
+    const long long eb = carry_e;
+    const uint32_t adv = map_at<NCOL>(excl, bcol);
+    const long long nblk = map_at<NCOL>(agg, bcol);
+    int col = (int)((bcol + adv) % NCOL);
+    long long e = eb + adv;
+    int rel = (int)adv;
+    if (chunk < nchunks && e < target) {
+      g = g0;
+      uint64_t w = tile_word0(w0p, tile) + (uint64_t)threadIdx.x * kChunkWords;
+      for (int i = 0; i < kChunkWords && e < target; ++i, ++w) {
+        const uint32_t word = g.next();
+        uint32_t n = sp.n[0], thr = sp.thr[0];
+#pragma unroll
+        for (int j = 1; j < NCOL; ++j)
+          if (j == col) { n = sp.n[j]; thr = sp.thr[j]; }
+        const uint64_t prod = (uint64_t)word * n;
+        if ((uint32_t)prod >= thr) {
+          stage[rel++] = (int32_t)(prod >> 32);
+          if (e == target - 1 && end_word) *end_word = (long long)(w + 1);
+          ++e;
+          col = col + 1 == NCOL ? 0 : col + 1;
+        }
+      }
+    }
+    __syncthreads();
+    const long long lim = min(nblk, (long long)target - eb);
+    for (long long i = threadIdx.x; i < lim; i += kScanThreads) out[eb + i] = stage[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry_e = eb + nblk;
+      carry_c = (int)((bcol + nblk) % NCOL);
+    }
+    if (eb + nblk >= target) break;  // every element the draw uses is written
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *elems_total = carry_e;
+}
+
 template <int NCOL>
 static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int64_t target, int64_t words,
                        int32_t* out, long long* end_word, long long* elems_total, DrawScratch& scr,
@@ -787,6 +957,12 @@ static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int6
                        unsigned long long* owned = nullptr) {
   const int64_t nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
   const int64_t nblocks = (nchunks + kScanThreads - 1) / kScanThreads;
+  if (!hist && nblocks <= kFusedMaxTiles) {
+    k_draw_fused<NCOL><<<1, kScanThreads, 0, ctx->stream>>>(sp, w0, nchunks, target, out, end_word, elems_total);
+    ctx->count();
+    check_launch();
+    return;
+  }
   scr.tmaps.ensure((size_t)nblocks * kScanThreads * NCOL);
   scr.bagg.ensure((size_t)nblocks * NCOL * 4);
   scr.bstart.ensure((size_t)nblocks * 16);
@@ -985,6 +1161,19 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
     // case for sparse slices) they are the accepted zeros and no compaction runs.
     const bool in_place = ncol == d;
     const bool mark = lazy && in_place;
+    if (mark && rows_max <= kFusedMaxTiles * kRowsPerBlock) {  // small stratum: one fused block
+      k_zero_fused<<<1, kScanThreads, 0, s>>>(zs, scr.cand.as<int32_t>(), z_elems, rows_max, table, X->table_mask,
+                                              X->filter_mask ? X->filter.as<unsigned int>() : nullptr,
+                                              X->filter_mask, q, sc + 8, z_hits_before, z_misses);
+      ctx->count();
+      out.zsub = scr.cand.as<int32_t>();
+      out.q_dev = sc + 8;
+      k_draw_status<<<1, 1, 0, s>>>(nz_stream ? p : 0, nz_avail, q, z_misses, rows_max, ncol, z_elems,
+                                    z_hits_before, (long long)budget, code, ctx->flags.as<DevFlags>());
+      ctx->count();
+      check_launch();
+      return out;
+    }
     unsigned long long* hit_in_q =
         (in_place && !lazy) ? reinterpret_cast<unsigned long long*>(sc + 6) : nullptr;
     k_zero_hits<<<(unsigned)zblocks, kScanThreads, 0, s>>>(zs, scr.cand.as<int32_t>(), z_elems, rows_max, table,
