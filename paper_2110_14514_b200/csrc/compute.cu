@@ -1310,7 +1310,7 @@ static void dispatch_layout(Layout kind, int ndim, int ldr, F&& f) {
       switch (ldr) {
         case 4: f(Dc, IC<1>(), IC<1>(), IC<2>()); break;
         case 8: f(Dc, IC<2>(), IC<1>(), IC<2>()); break;
-        case 16: f(Dc, IC<4>(), IC<1>(), IC<2>()); break;
+        case 16: f(Dc, IC<4>(), IC<1>(), IC<2>()); break;  // measured best of (4,1,2) (2,2,1) (2,2,2) on c3
         // ldr 32: 4 lanes x 2 float4 per row, 8 samples per warp instruction (halves the
         // per-sample index/address work against 8 lanes x 1 float4; c4: 9.04 -> 8.62 ms)
         case 32: f(Dc, IC<4>(), IC<2>(), IC<1>()); break;
