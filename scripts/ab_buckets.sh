@@ -1,3 +1,6 @@
-for lib in libogcp_b200 libogcp_b200_a libogcp_b200_b; do
-  OGCP_LIB=paper_2110_14514_b200/$lib.so python scripts/config_bench.py c3 2>&1 | tail -1 | cut -c1-330
+for lib in libogcp_b200 libogcp_b200_pf libogcp_b200_pf2; do
+  OGCP_LIB=paper_2110_14514_b200/$lib.so python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab.json 2> gpurun_out/ab.err
+  python -c "
+import json; d=json.loads(open('gpurun_out/ab.json').read().strip().splitlines()[-1]); k=d['kernel_ms']; n=d['kernel_launch_brackets']
+print('$lib', round(d['value']/1e9,3), d['ms_per_step'], round(k['sgrad']/n['sgrad'],3))"
 done
