@@ -46,6 +46,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=("c1", "c2"))
     ap.add_argument("--slices", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--profile", action="store_true", help="also report per-kernel-class device ms per slice")
     args = ap.parse_args()
     import torch
     import paper_2110_14514_b200 as P
@@ -78,6 +79,9 @@ def main():
     for X in slices[: args.warmup]:
         P.process_slice(st, X, loss, cfg, exact_loss=False)
     torch.cuda.synchronize()
+    if args.profile:
+        P._lib.lib().ogcp_ctx_profile_reset(P._lib.ctx())
+        P._lib.lib().ogcp_ctx_profile_enable(P._lib.ctx(), 1)
     t0 = time.perf_counter()
     for X in slices[args.warmup: args.warmup + args.slices]:
         P.process_slice(st, X, loss, cfg, exact_loss=False)
@@ -85,8 +89,17 @@ def main():
     dt = time.perf_counter() - t0
     iters = sum(r.epochs_weights * cfg.iters_weights + r.epochs_factors * cfg.iters_factors
                 for r in st.metrics[-args.slices:])
-    print(json.dumps({"config": args.config, "slices_per_s": args.slices / dt, "ms_per_slice": 1e3 * dt / args.slices,
-                      "us_per_iteration": 1e6 * dt / max(iters, 1), "launches": P._lib.launches()}))
+    line = {"config": args.config, "slices_per_s": args.slices / dt, "ms_per_slice": 1e3 * dt / args.slices,
+            "us_per_iteration": 1e6 * dt / max(iters, 1), "launches": P._lib.launches()}
+    if args.profile:
+        import ctypes as C
+        prof = {}
+        for cls, name in enumerate(["draw", "sgrad", "wgrad", "objective", "gram", "update"]):
+            n, tms = C.c_int64(), C.c_double()
+            P._lib.lib().ogcp_ctx_profile_read(P._lib.ctx(), cls, C.byref(n), C.byref(tms))
+            prof[name] = round(tms.value / args.slices, 2)
+        line["device_ms_per_slice"] = prof
+    print(json.dumps(line))
 
 
 if __name__ == "__main__":
