@@ -864,6 +864,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_gram_tc(const float* __restrict
   }
 }
 
+// Grams of every mode of a small model in one launch (blockIdx.y = mode), fp64
+// sums straight into the outputs: out1_k = B1_k' A_k, out2_k = B2_k' A_k (B2 nullable).
+__global__ void k_gram_small(SmallGrams g, int rank, int ldr, double* __restrict__ out1, double* __restrict__ out2) {
+  const int k = blockIdx.y;
+  const int RR = rank * rank;
+  const float* A = g.A[k];
+  const float* B1 = g.B1[k];
+  const float* B2 = g.B2[k];
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+    const int i = e / rank, j = e % rank;
+    double s1 = 0.0, s2 = 0.0;
+    for (int64_t r = 0; r < g.rows[k]; ++r) {
+      const double aj = A[r * ldr + j];
+      s1 += (double)B1[r * ldr + i] * aj;
+      if (B2) s2 += (double)B2[r * ldr + i] * aj;
+    }
+    out1[(int64_t)k * RR + e] = s1;
+    if (B2) out2[(int64_t)k * RR + e] = s2;
+  }
+}
+
+void gram_small_enqueue(Ctx* ctx, const SmallGrams& g, int ndim, int rank, int ldr, double* out1, double* out2) {
+  ProfScope prof_scope(ctx, kProfGram);
+  k_gram_small<<<dim3(1, ndim), kThreads, 0, ctx->stream>>>(g, rank, ldr, out1, out2);
+  ctx->count();
+  check_launch();
+}
+
 // Sum block partials (fixed order) and extract the rank x rank blocks.
 __global__ void k_gram_finalize(const double* __restrict__ partials, int nblk, int ngram, int ldr, int rank,
                                 double* __restrict__ outP, double* __restrict__ outC) {
@@ -965,13 +993,13 @@ __device__ __forceinline__ bool adam_regs(float* __restrict__ A, float* __restri
 constexpr int kK5Rows = 4;
 constexpr int kK5Unroll = 8;
 template <int GR>
-__global__ void __launch_bounds__(kThreads, 3) k_factor_update(int64_t rows, int rank, int ldr, float* __restrict__ A,
-                                                            const float* __restrict__ Aold,
-                                                            const float* __restrict__ G, float* __restrict__ u,
-                                                            float* __restrict__ v, const float* __restrict__ Mk,
-                                                            const float* __restrict__ Nk, float reg, float rate_i,
-                                                            float b1, float omb1, float b2, float omb2, float eps,
-                                                            float lower, DevFlags* flags, long long code) {
+__device__ __forceinline__ void factor_update_rows(int64_t rows, int rank, int ldr, float* __restrict__ A,
+                                                   const float* __restrict__ Aold, const float* __restrict__ G,
+                                                   float* __restrict__ u, float* __restrict__ v,
+                                                   const float* __restrict__ Mk, const float* __restrict__ Nk,
+                                                   float reg, float rate_i, float b1, float omb1, float b2,
+                                                   float omb2, float eps, float lower, DevFlags* flags,
+                                                   long long code) {
   constexpr int RPI = kK5Rows;
   const bool hist = Mk != nullptr;
   const bool has_old = hist && Aold != nullptr;  // dense-Gaussian model term without history
@@ -1035,6 +1063,30 @@ __global__ void __launch_bounds__(kThreads, 3) k_factor_update(int64_t rows, int
         bad = true;
   }
   if (bad) report(flags, kFlagDiverge, code, 0);
+}
+
+template <int GR>
+__global__ void __launch_bounds__(kThreads, 3) k_factor_update(int64_t rows, int rank, int ldr, float* __restrict__ A,
+                                                            const float* __restrict__ Aold,
+                                                            const float* __restrict__ G, float* __restrict__ u,
+                                                            float* __restrict__ v, const float* __restrict__ Mk,
+                                                            const float* __restrict__ Nk, float reg, float rate_i,
+                                                            float b1, float omb1, float b2, float omb2, float eps,
+                                                            float lower, DevFlags* flags, long long code) {
+  factor_update_rows<GR>(rows, rank, ldr, A, Aold, G, u, v, Mk, Nk, reg, rate_i, b1, omb1, b2, omb2, eps, lower,
+                         flags, code);
+}
+
+// Every mode of a small model in one launch (blockIdx.y = mode): the c1/c2
+// shapes are launch-bound, one K5 launch per mode cost more than the update.
+template <int GR>
+__global__ void __launch_bounds__(kThreads, 3) k_factor_update_modes(K5Modes m, int rank, int ldr, float reg,
+                                                                  float rate_i, float b1, float omb1, float b2,
+                                                                  float omb2, float eps, float lower,
+                                                                  DevFlags* flags, long long code) {
+  const int k = blockIdx.y;
+  factor_update_rows<GR>(m.rows[k], rank, ldr, m.A[k], m.Aold[k], m.G[k], m.u[k], m.v[k], m.Mk[k], m.Nk[k], reg,
+                         rate_i, b1, omb1, b2, omb2, eps, lower, flags, code);
 }
 
 // 32 < rank <= 128 with history / model terms: the apply H = A Mk - Aold Nk is
@@ -1380,8 +1432,19 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
                    float* const* grads, long long code) {
   GradPtrs GP;
   for (int k = 0; k < kMaxModes; ++k) GP.g[k] = k < M.ndim ? grads[k] : nullptr;
-  for (int k = 0; k < M.ndim; ++k)
-    OGCP_CUDA(cudaMemsetAsync(grads[k], 0, (size_t)M.dims[k] * M.ldr * 4, ctx->stream));
+  // zero the outputs: one memset when the per-mode buffers are contiguous
+  bool contiguous = true;
+  size_t tot_bytes = 0;
+  for (int k = 0; k < M.ndim; ++k) {
+    if (grads[k] != grads[0] + tot_bytes / 4) contiguous = false;
+    tot_bytes += (size_t)M.dims[k] * M.ldr * 4;
+  }
+  if (contiguous) {
+    OGCP_CUDA(cudaMemsetAsync(grads[0], 0, tot_bytes, ctx->stream));
+  } else {
+    for (int k = 0; k < M.ndim; ++k)
+      OGCP_CUDA(cudaMemsetAsync(grads[k], 0, (size_t)M.dims[k] * M.ldr * 4, ctx->stream));
+  }
   const int64_t total = S.p + S.q;
   if (total == 0) return;
   // privatise small modes in shared memory when the per-CTA flush is cheap
@@ -1570,6 +1633,34 @@ void hist_coeffs_enqueue(Ctx* ctx, int ndim, int rank, const double* P, const do
 void dense_wgrad_enqueue(Ctx* ctx, int ndim, int rank, int ldr, const double* P, const double* b, const double* s,
                          double* out) {
   k_dense_wgrad<<<1, ldr, 0, ctx->stream>>>(ndim, rank, ldr, P, b, s, out);
+  ctx->count();
+  check_launch();
+}
+
+void factor_update_modes_enqueue(Ctx* ctx, const K5Modes& m, int ndim, int rank, int ldr, double reg, double rate_i,
+                                 double beta1, double beta2, double eps, double lower, long long code) {
+  ProfScope prof_scope(ctx, kProfUpdate);
+  const float fb1 = (float)beta1, fomb1 = (float)(1.0 - beta1), fb2 = (float)beta2, fomb2 = (float)(1.0 - beta2);
+  int64_t rmax = 1;
+  for (int k = 0; k < ndim; ++k) rmax = std::max<int64_t>(rmax, m.rows[k]);
+  int GR = 1;
+  while (GR < rank) GR <<= 1;
+  auto launch = [&](auto kern) {
+    const int64_t rows_per_block = (kThreads / GR) * kK5Rows;
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((rmax + rows_per_block - 1) / rows_per_block,
+                                                                (int64_t)kNumSMs * 3));
+    kern<<<dim3(gx, ndim), kThreads, 0, ctx->stream>>>(m, rank, ldr, (float)reg, (float)rate_i, fb1, fomb1, fb2,
+                                                         fomb2, (float)eps, (float)lower, ctx->flags.as<DevFlags>(),
+                                                         code);
+  };
+  switch (GR) {
+    case 1: launch(k_factor_update_modes<1>); break;
+    case 2: launch(k_factor_update_modes<2>); break;
+    case 4: launch(k_factor_update_modes<4>); break;
+    case 8: launch(k_factor_update_modes<8>); break;
+    case 16: launch(k_factor_update_modes<16>); break;
+    default: launch(k_factor_update_modes<32>); break;
+  }
   ctx->count();
   check_launch();
 }

@@ -67,6 +67,27 @@ void hist_coeffs_enqueue(Ctx* ctx, int ndim, int rank, const double* P, const do
 // Dense-Gaussian weight gradient 2((hadamard_m P_m) s - b) into out[ldr] (one block).
 void dense_wgrad_enqueue(Ctx* ctx, int ndim, int rank, int ldr, const double* P, const double* b, const double* s,
                          double* out);
+// Small models (every mode <= kSmallRows rows, ldr <= 32): all modes in one launch.
+constexpr int64_t kSmallRows = 4096;
+struct SmallGrams {
+  const float* A[kMaxModes];
+  const float* B1[kMaxModes];
+  const float* B2[kMaxModes];  // nullable
+  int64_t rows[kMaxModes];
+};
+void gram_small_enqueue(Ctx* ctx, const SmallGrams& g, int ndim, int rank, int ldr, double* out1, double* out2);
+struct K5Modes {
+  float* A[kMaxModes];
+  const float* Aold[kMaxModes];
+  const float* G[kMaxModes];
+  float* u[kMaxModes];
+  float* v[kMaxModes];
+  const float* Mk[kMaxModes];
+  const float* Nk[kMaxModes];
+  int64_t rows[kMaxModes];
+};
+void factor_update_modes_enqueue(Ctx* ctx, const K5Modes& m, int ndim, int rank, int ldr, double reg, double rate_i,
+                                 double beta1, double beta2, double eps, double lower, long long code);
 // K5: g = G + lambda*A + (A Mk - Aold Nk) ; Adam ; clamp ; isfinite  (one mode).
 void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, const float* Aold,
                            const float* G, float* u, float* v, const float* Mk, const float* Nk,

@@ -442,9 +442,27 @@ struct HistBufs {
   DevBuf P, C, Poo, S, Ws, coef, out, Mk, Nk, scratch, part, tmp;
 };
 
+// Small models: every mode in one launch (see compute.cuh kSmallRows).
+static bool small_model(const ModelP& M) {
+  if (M.ldr > 32) return false;
+  for (int k = 0; k < M.ndim; ++k)
+    if (M.dims[k] > kSmallRows) return false;
+  return true;
+}
+
 static void grams_enqueue(Ctx* ctx, const ModelP& M, float* const* other, double* out_per_mode, HistBufs& hb,
                           bool self) {
   const int RR = M.rank * M.rank;
+  if (small_model(M)) {
+    SmallGrams g{};
+    for (int k = 0; k < M.ndim; ++k) {
+      g.A[k] = M.A[k];
+      g.B1[k] = self ? M.A[k] : other[k];
+      g.rows[k] = M.dims[k];
+    }
+    gram_small_enqueue(ctx, g, M.ndim, M.rank, M.ldr, out_per_mode, nullptr);
+    return;
+  }
   for (int k = 0; k < M.ndim; ++k) {
     const float* A = M.A[k];
     const float* B = self ? M.A[k] : other[k];
@@ -455,6 +473,17 @@ static void grams_enqueue(Ctx* ctx, const ModelP& M, float* const* other, double
 // P_m = A_m'A_m and C_m = Aold_m'A_m for every mode, one pass over each A_m.
 static void grams_pc_enqueue(Ctx* ctx, const ModelP& M, float* const* old, HistBufs& hb) {
   const int RR = M.rank * M.rank;
+  if (small_model(M)) {
+    SmallGrams g{};
+    for (int k = 0; k < M.ndim; ++k) {
+      g.A[k] = M.A[k];
+      g.B1[k] = M.A[k];
+      g.B2[k] = old[k];
+      g.rows[k] = M.dims[k];
+    }
+    gram_small_enqueue(ctx, g, M.ndim, M.rank, M.ldr, hb.P.as<double>(), hb.C.as<double>());
+    return;
+  }
   for (int k = 0; k < M.ndim; ++k)
     gram2_enqueue(ctx, M.A[k], old[k], M.dims[k], M.rank, M.ldr, hb.P.as<double>() + (int64_t)k * RR,
                   hb.C.as<double>() + (int64_t)k * RR, hb.scratch);
@@ -823,6 +852,22 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
     hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), hist ? W.hb.C.as<double>() : nullptr,
                         hist ? W.hb.S.as<double>() : nullptr, cfg->hist_weight, W.hb.Mk.as<float>(),
                         W.hb.Nk.as<float>(), dense_s, 2.0);
+  }
+  if (small_model(M)) {  // every mode in one launch
+    K5Modes km{};
+    for (int k = 0; k < M.ndim; ++k) {
+      km.A[k] = A[k];
+      km.Aold[k] = hist ? old_factors[k] : nullptr;
+      km.G[k] = gp[k];
+      km.u[k] = ad->u[k];
+      km.v[k] = ad->v[k];
+      km.Mk[k] = coeffs ? W.hb.Mk.as<float>() + (size_t)k * RR : nullptr;
+      km.Nk[k] = coeffs ? W.hb.Nk.as<float>() + (size_t)k * RR : nullptr;
+      km.rows[k] = M.dims[k];
+    }
+    factor_update_modes_enqueue(ctx, km, M.ndim, M.rank, M.ldr, cfg->reg_factors, rate_i, cfg->beta1, cfg->beta2,
+                                cfg->adam_eps, cfg->lower_bound, code_of(ev, 2));
+    return;
   }
   for (int k = 0; k < M.ndim; ++k) {
     factor_update_enqueue(ctx, M.dims[k], M.rank, M.ldr, A[k], hist ? old_factors[k] : nullptr, gp[k], ad->u[k],
