@@ -82,3 +82,51 @@ def test_semi_stratified_stream_runs():
     assert np.isfinite(m.local_loss_exact)
     _, wtr, ftr = st.trace_log[-1]
     assert all(b <= a for a, b in zip(wtr, wtr[1:])) and all(b <= a for a, b in zip(ftr, ftr[1:]))
+
+
+@pytest.mark.parametrize("p,buckets", [(6000, 1), (None, 1), (None, 4)])
+def test_semi_stream_step_vs_oracle(p, buckets):
+    """A full semi-stratified slice step (weight + factor solves, history) against the
+    oracle restatement: per-draw and merged (count-form) draws, with and without the
+    row-bucketed walk."""
+    dims = (300, 200, 40)
+    subs0, vals = _slice(6, dims, 100_000)
+    rng = np.random.default_rng(7)
+    R = 5
+    init = [rng.uniform(0.2, 1.0, (d, R)) for d in dims]
+    _lib.set_buckets(buckets)
+    try:
+        cfg = P.SolverConfig(max_epochs_weights=1, max_epochs_factors=1, iters_weights=4, iters_factors=4,
+                             rate_weights=0.05, rate_factors=1e-2, hist_weight=1.0, warm_start_weights=True,
+                             samples=P.SamplerConfig(p, 5000, 20000, 20000, seed=3, semi_stratified=True))
+        loss = P.make_loss("poisson")
+        st = P.fresh_state(dims, R, loss, cfg, factors=init)
+        st.window = P.HistoryWindow(capacity=2)
+        for h in (1, 2):
+            s_h = np.full(R, 1.0 + 0.1 * h)
+            st.weights_log.append(s_h)
+            st.window.observe(h, s_h, P.rng_at(3, h, 5))
+        st.t = 2
+        X = P.SparseTensor.from_zero_based(dims, subs0, vals)
+        m = P.process_slice(st, X, loss, cfg, exact_loss=True)
+    finally:
+        _lib.set_buckets(1)
+    ocfg = O.Cfg(kappa_w=1, kappa_f=1, tau_w=4, tau_f=4, rate_w=0.05, rate_f=1e-2, hist_weight=1.0,
+                 warm_weights=True, p=p, q=5000, p_obj=20000, q_obj=20000, seed=3, semi=True)
+    ost = O.new_stream(init, "poisson", ocfg, capacity=2)
+    for h in (1, 2):
+        s_h = np.full(R, 1.0 + 0.1 * h)
+        ost.weights_log.append(s_h)
+        O.window_observe(ost, h, s_h, 3)
+    ost.t = 2
+    Xo = O.Slice(dims, subs0, vals)
+    s_t = O.slice_step(ost, Xo, "poisson", ocfg)
+    want = O.exact_local_loss(Xo, ost.factors, s_t, "poisson")
+    assert m.local_loss_exact == pytest.approx(want, rel=1e-4)
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)
+    for a, b in zip(st.factors, ost.factors):
+        assert rel(a, b) < 1e-4
+    assert rel(st.weights_log[-1], s_t) < 1e-4
+    for (_, w, f), (_, ow, of) in zip(st.trace_log[-1:], ost.traces[-1:]):
+        np.testing.assert_allclose(w, ow, rtol=1e-4)
+        np.testing.assert_allclose(f, of, rtol=1e-4)
