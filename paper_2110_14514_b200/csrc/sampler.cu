@@ -465,7 +465,9 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_fused(ZeroSpec zs, int32_
                                                              uint64_t mask, const unsigned int* __restrict__ filter,
                                                              uint64_t fmask, int64_t q, long long* __restrict__ rows_used,
                                                              long long* __restrict__ hits_before,
-                                                             long long* __restrict__ misses_out) {
+                                                             long long* __restrict__ misses_out, int64_t p,
+                                                             const long long* __restrict__ nz_avail, long long budget,
+                                                             long long code, DevFlags* flags) {
   __shared__ long long carry;
   __shared__ int found;
   __shared__ int wsum[kScanThreads / 32];
@@ -531,9 +533,19 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_fused(ZeroSpec zs, int32_
     __syncthreads();
     if (found) break;
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // k_draw_status, folded
     *misses_out = carry;
     if (!found) *rows_used = rows_max;
+    bool shortfall = p > 0 && nz_avail && *nz_avail < p, exhausted = false;
+    if (carry >= q) {
+      if (*hits_before > budget) exhausted = true;
+    } else if (rows - carry > budget) {
+      exhausted = true;
+    } else {
+      shortfall = true;
+    }
+    if (exhausted) atomicMin(&flags->first_code[kFlagSampling], code);
+    else if (shortfall) atomicMin(&flags->first_code[kFlagShortfall], code);
   }
 }
 
@@ -875,7 +887,8 @@ template <int NCOL>
 __global__ void __launch_bounds__(kScanThreads) k_draw_fused(StreamSpec sp, const long long* w0p, int64_t nchunks,
                                                              int64_t target, int32_t* __restrict__ out,
                                                              long long* __restrict__ end_word,
-                                                             long long* __restrict__ elems_total) {
+                                                             long long* __restrict__ elems_total, DevFlags* report,
+                                                             long long code) {
   __shared__ int32_t stage[kBlockWords];
   __shared__ long long carry_e;
   __shared__ int carry_c;
@@ -947,20 +960,27 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_fused(StreamSpec sp, cons
     if (eb + nblk >= target) break;  // every element the draw uses is written
   }
   __syncthreads();
-  if (threadIdx.x == 0) *elems_total = carry_e;
+  if (threadIdx.x == 0) {
+    *elems_total = carry_e;
+    if (report && carry_e < target) atomicMin(&report->first_code[kFlagShortfall], code);  // k_draw_status, folded
+  }
 }
 
 template <int NCOL>
 static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int64_t target, int64_t words,
                        int32_t* out, long long* end_word, long long* elems_total, DrawScratch& scr,
                        uint32_t* hist = nullptr, uint32_t olo = 0, uint32_t ohi = 0,
-                       unsigned long long* owned = nullptr) {
+                       unsigned long long* owned = nullptr, DevFlags* report = nullptr, long long code = 0,
+                       bool* fused = nullptr) {
   const int64_t nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
   const int64_t nblocks = (nchunks + kScanThreads - 1) / kScanThreads;
+  if (fused) *fused = false;
   if (!hist && nblocks <= kFusedMaxTiles) {
-    k_draw_fused<NCOL><<<1, kScanThreads, 0, ctx->stream>>>(sp, w0, nchunks, target, out, end_word, elems_total);
+    k_draw_fused<NCOL><<<1, kScanThreads, 0, ctx->stream>>>(sp, w0, nchunks, target, out, end_word, elems_total,
+                                                            report, code);
     ctx->count();
     check_launch();
+    if (fused) *fused = true;
     return;
   }
   scr.tmaps.ensure((size_t)nblocks * kScanThreads * NCOL);
@@ -1025,6 +1045,7 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
 
   // ---- nonzero stratum: integers(0, eta, size=p)  (sampling.py:125)
   bool nz_stream = false;
+  bool nz_self_reported = false;
   if (merged && (p == 0 || eta < 2)) throw Error(OGCP_E_INTERNAL, "merged draw needs p > 0 and eta > 1");
   if (p > 0) {
     if (eta == 1) {
@@ -1077,7 +1098,12 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
         ctx->count(3);
         merged->count = sc + 5;
       } else {
-        run_stream_dispatch(1, ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr);
+        if (q == 0) {  // nothing follows: the fused pass reports its own shortfall
+          run_stream<1>(ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr, nullptr, 0, 0, nullptr,
+                        ctx->flags.as<DevFlags>(), code, &nz_self_reported);
+        } else {
+          run_stream_dispatch(1, ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr);
+        }
       }
       nz_stream = true;
     }
@@ -1164,14 +1190,13 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
     if (mark && rows_max <= kFusedMaxTiles * kRowsPerBlock) {  // small stratum: one fused block
       k_zero_fused<<<1, kScanThreads, 0, s>>>(zs, scr.cand.as<int32_t>(), z_elems, rows_max, table, X->table_mask,
                                               X->filter_mask ? X->filter.as<unsigned int>() : nullptr,
-                                              X->filter_mask, q, sc + 8, z_hits_before, z_misses);
-      ctx->count();
-      out.zsub = scr.cand.as<int32_t>();
-      out.q_dev = sc + 8;
-      k_draw_status<<<1, 1, 0, s>>>(nz_stream ? p : 0, nz_avail, q, z_misses, rows_max, ncol, z_elems,
-                                    z_hits_before, (long long)budget, code, ctx->flags.as<DevFlags>());
+                                              X->filter_mask, q, sc + 8, z_hits_before, z_misses,
+                                              nz_stream ? p : 0, nz_avail, (long long)budget, code,
+                                              ctx->flags.as<DevFlags>());
       ctx->count();
       check_launch();
+      out.zsub = scr.cand.as<int32_t>();
+      out.q_dev = sc + 8;
       return out;
     }
     unsigned long long* hit_in_q =
@@ -1206,6 +1231,7 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
       }
     }
   }
+  if (q == 0 && (!nz_stream || nz_self_reported)) return out;  // nothing left to check
   k_draw_status<<<1, 1, 0, s>>>(nz_stream ? p : 0, nz_avail, q, z_misses, rows_max, ncol, z_elems, z_hits_before,
                                 (long long)budget, code, ctx->flags.as<DevFlags>());
   ctx->count();
