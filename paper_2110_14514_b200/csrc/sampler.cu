@@ -888,7 +888,7 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_fused(StreamSpec sp, cons
                                                              int64_t target, int32_t* __restrict__ out,
                                                              long long* __restrict__ end_word,
                                                              long long* __restrict__ elems_total, DevFlags* report,
-                                                             long long code) {
+                                                             long long code, long long* __restrict__ clear) {
   __shared__ int32_t stage[kBlockWords];
   __shared__ long long carry_e;
   __shared__ int carry_c;
@@ -896,6 +896,7 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_fused(StreamSpec sp, cons
     carry_e = 0;
     carry_c = 0;
   }
+  if (clear && threadIdx.x < 16) clear[threadIdx.x] = 0;  // the draw's scalars (instead of a memset)
   const int64_t ntiles = (nchunks + kScanThreads - 1) / kScanThreads;
   for (int64_t tile = 0; tile < ntiles; ++tile) {
     const int64_t chunk = tile * kScanThreads + threadIdx.x;
@@ -971,13 +972,13 @@ static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int6
                        int32_t* out, long long* end_word, long long* elems_total, DrawScratch& scr,
                        uint32_t* hist = nullptr, uint32_t olo = 0, uint32_t ohi = 0,
                        unsigned long long* owned = nullptr, DevFlags* report = nullptr, long long code = 0,
-                       bool* fused = nullptr) {
+                       bool* fused = nullptr, long long* clear = nullptr) {
   const int64_t nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
   const int64_t nblocks = (nchunks + kScanThreads - 1) / kScanThreads;
   if (fused) *fused = false;
   if (!hist && nblocks <= kFusedMaxTiles) {
     k_draw_fused<NCOL><<<1, kScanThreads, 0, ctx->stream>>>(sp, w0, nchunks, target, out, end_word, elems_total,
-                                                            report, code);
+                                                            report, code, clear);
     ctx->count();
     check_launch();
     if (fused) *fused = true;
@@ -1035,7 +1036,15 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
   long long* z_elems = sc + 2;
   long long* z_misses = sc + 3;
   long long* z_hits_before = sc + 4;
-  OGCP_CUDA(cudaMemsetAsync(sc, 0, 16 * 8, s));
+  // the draw's scalars start at zero: a memset, or the first (fused) kernel clears them
+  bool clear_in_kernel = false;
+  if (!merged && p > 0 && eta > 1) {
+    const double r = reject_rate((uint32_t)eta);
+    const double w = ((double)p / (1.0 - r) + 10.0 * std::sqrt((double)p * r) / (1.0 - r) + 2048.0) * ctx->slack;
+    const int64_t nchunks = std::max<int64_t>(1, ((int64_t)w + kChunkWords - 1) / kChunkWords);
+    clear_in_kernel = (nchunks + kScanThreads - 1) / kScanThreads <= kFusedMaxTiles;
+  }
+  if (!clear_in_kernel) OGCP_CUDA(cudaMemsetAsync(sc, 0, 16 * 8, s));
   StreamSpec sp;
   sp.st_hi = (unsigned long long)(g.state >> 64);
   sp.st_lo = (unsigned long long)g.state;
@@ -1098,12 +1107,12 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
         ctx->count(3);
         merged->count = sc + 5;
       } else {
-        if (q == 0) {  // nothing follows: the fused pass reports its own shortfall
-          run_stream<1>(ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr, nullptr, 0, 0, nullptr,
-                        ctx->flags.as<DevFlags>(), code, &nz_self_reported);
-        } else {
-          run_stream_dispatch(1, ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr);
-        }
+        // q == 0: nothing follows, so the fused pass reports its own shortfall
+        run_stream<1>(ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr, nullptr, 0, 0, nullptr,
+                      q == 0 ? ctx->flags.as<DevFlags>() : nullptr, code, &nz_self_reported,
+                      clear_in_kernel ? sc : nullptr);
+        if (clear_in_kernel && !nz_self_reported) throw Error(OGCP_E_INTERNAL, "fused draw expected");
+        if (q != 0) nz_self_reported = false;
       }
       nz_stream = true;
     }
