@@ -262,8 +262,8 @@ def main():
         PD.init_sharded_solves()
     if os.environ.get("OGCP_SPLIT") == "1":  # A/B knob for the two-pass scatter
         _lib.set_split_scatter(True)
-    if os.environ.get("OGCP_BUCKETS") == "0":  # A/B knob for the bucketed merged walk
-        _lib.set_buckets(False)
+    if os.environ.get("OGCP_BUCKETS"):  # A/B knob for the bucketed merged walk: 0 off, k > 1 forces k buckets
+        _lib.set_buckets(int(os.environ["OGCP_BUCKETS"]))
     if os.environ.get("OGCP_MERGE") == "0":  # A/B knob for the merged draws
         _lib.set_merge_draws(False)
     loss = P.make_loss("poisson")

@@ -376,7 +376,7 @@ static bool use_merged(const Ctx* ctx, const Slice* X, int64_t p) {
 
 // Bucketed layout for merged sets (Slice::perm): the largest mode k >= 1 whose
 // factor + gradient rows (2 dims[k] ldr 4 B) exceed 48 MB is cut into
-// power-of-two row buckets of <= 32 MB, so each bucket's rows stay L2-resident
+// power-of-two row buckets of <= 64 MB, so each bucket's rows stay L2-resident
 // while the set's positions inside it are walked.  Built once per slice.
 static void prepare_buckets(Ctx* ctx, const Slice* Xc, int ldr) {
   Slice* X = const_cast<Slice*>(Xc);
@@ -395,7 +395,7 @@ static void prepare_buckets(Ctx* ctx, const Slice* Xc, int ldr) {
     nb = ctx->buckets_force;
   } else {
     if (ws <= 48e6) return;
-    while (nb < 256 && ws / nb > 32e6) nb <<= 1;
+    while (nb < 256 && ws / nb > 64e6) nb <<= 1;  // c4 (256 MB): 4 buckets, measured better than 2 or 8
   }
   int64_t olo = 0, ohi = X->nnz;
   owned_range(ctx, X, &olo, &ohi);
