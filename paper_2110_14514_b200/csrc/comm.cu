@@ -3,11 +3,14 @@
 // engine library itself has no link-time NCCL dependency; the unique id is
 // exchanged by the caller (torch.distributed broadcast, 128 bytes).
 //
-// Per factor iteration the ranks exchange the d factor-gradient matrices
-// (sum, one allreduce over the contiguous gradient buffer); per weight
-// iteration the R-vector gradient; per objective evaluation one fp64 partial;
-// per epoch the error word.  Adam then runs replicated on identical inputs, so
-// the factors stay bitwise identical across ranks.
+// Per factor iteration the ranks exchange the d factor-gradient matrices: for
+// small models one allreduce over the contiguous gradient buffer, then Adam runs
+// replicated on identical inputs; otherwise each rank owns a contiguous 1/N of
+// every mode's rows -- the gradient rows are reduced onto their owner, the owner
+// runs the row Adam (K5) on them alone and broadcasts the new factor rows, so
+// the factors stay bitwise identical across ranks.  Per weight iteration the
+// R-vector gradient is allreduced; per objective evaluation one fp64 partial;
+// per epoch the error word.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -26,6 +29,11 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -43,10 +51,15 @@ NcclApi& api() {
     a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(a.lib, "ncclGetUniqueId"));
     a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(a.lib, "ncclCommInitRank"));
     a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(a.lib, "ncclAllReduce"));
+    a.Reduce = reinterpret_cast<decltype(a.Reduce)>(dlsym(a.lib, "ncclReduce"));
+    a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(dlsym(a.lib, "ncclBroadcast"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.lib, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.lib, "ncclGroupEnd"));
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.lib, "ncclCommDestroy"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(a.lib, "ncclGetErrorString"));
   });
-  if (!a.lib || !a.GetUniqueId || !a.CommInitRank || !a.AllReduce)
+  if (!a.lib || !a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.Reduce || !a.Broadcast || !a.GroupStart ||
+      !a.GroupEnd)
     throw Error(OGCP_E_INTERNAL, "NCCL (libnccl.so.2) is not available for the multi-GPU path");
   return a;
 }
@@ -82,6 +95,42 @@ void comm_allreduce_sum(Ctx* ctx, float* p, size_t n) {
 void comm_allreduce_sum(Ctx* ctx, double* p, size_t n) {
   if (ctx->world <= 1 || n == 0 || !ctx->comm) return;
   nccl_check(api().AllReduce(p, p, n, ncclFloat64, ncclSum, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");
+}
+
+void comm_row_range(int64_t rows, int rank, int world, int64_t* lo, int64_t* hi) {
+  *lo = rows * rank / world;
+  *hi = rows * (rank + 1) / world;
+}
+
+// Owner-computes row blocks: one ncclGroup of (buffers x ranks) in-place reduces /
+// broadcasts, rank r the root of rows [lo_r, hi_r) of every buffer.  Together they
+// move the bytes of one allreduce (a reduce-scatter plus an all-gather) but leave
+// the row update between them to the owner alone.
+static void rows_group(Ctx* ctx, float* const* bufs, const int64_t* rows, int nbuf, int ldr, bool reduce) {
+  if (ctx->world <= 1 || !ctx->comm) return;
+  NcclApi& a = api();
+  ncclComm_t comm = (ncclComm_t)ctx->comm;
+  nccl_check(a.GroupStart(), "ncclGroupStart");
+  for (int k = 0; k < nbuf; ++k) {
+    for (int r = 0; r < ctx->world; ++r) {
+      int64_t lo, hi;
+      comm_row_range(rows[k], r, ctx->world, &lo, &hi);
+      if (hi <= lo) continue;
+      float* p = bufs[k] + (size_t)lo * ldr;
+      const size_t n = (size_t)(hi - lo) * ldr;
+      if (reduce) nccl_check(a.Reduce(p, p, n, ncclFloat32, ncclSum, r, comm, ctx->stream), "ncclReduce");
+      else nccl_check(a.Broadcast(p, p, n, ncclFloat32, r, comm, ctx->stream), "ncclBroadcast");
+    }
+  }
+  nccl_check(a.GroupEnd(), "ncclGroupEnd");
+}
+
+void comm_reduce_rows(Ctx* ctx, float* const* bufs, const int64_t* rows, int nbuf, int ldr) {
+  rows_group(ctx, bufs, rows, nbuf, ldr, true);
+}
+
+void comm_gather_rows(Ctx* ctx, float* const* bufs, const int64_t* rows, int nbuf, int ldr) {
+  rows_group(ctx, bufs, rows, nbuf, ldr, false);
 }
 
 void comm_sync_flags(Ctx* ctx) {
@@ -121,7 +170,7 @@ void comm_unique_id(uint8_t* out) {
 }
 
 // One-rank communicator round trip through every collective the solves use
-// (fp32 / fp64 sum, int64 min / max): checks the dlopen'd NCCL entry points and
+// (fp32 / fp64 sum, int64 min / max, grouped fp32 row reduce / broadcast): checks the dlopen'd NCCL entry points and
 // their signatures on a single GPU.  Returns the number of mismatches.
 int comm_selftest(Ctx* ctx) {
   OGCP_CUDA(cudaSetDevice(ctx->device));
@@ -142,6 +191,10 @@ int comm_selftest(Ctx* ctx) {
   nccl_check(api().AllReduce(d + 64, d + 64, 2, ncclFloat64, ncclSum, comm, st), "ncclAllReduce");
   nccl_check(api().AllReduce(d + 128, d + 128, 2, ncclInt64, ncclMin, comm, st), "ncclAllReduce");
   nccl_check(api().AllReduce(d + 144, d + 144, 2, ncclInt64, ncclMax, comm, st), "ncclAllReduce");
+  nccl_check(api().GroupStart(), "ncclGroupStart");
+  nccl_check(api().Reduce(d, d, 2, ncclFloat32, ncclSum, 0, comm, st), "ncclReduce");
+  nccl_check(api().Broadcast(d + 8, d + 8, 2, ncclFloat32, 0, comm, st), "ncclBroadcast");
+  nccl_check(api().GroupEnd(), "ncclGroupEnd");
   OGCP_CUDA(cudaStreamSynchronize(st));
   float rf[4];
   double rd[2];

@@ -7,6 +7,13 @@ namespace ogcp {
 // In-place sums across the context's ranks on the context stream (no-ops for world == 1).
 void comm_allreduce_sum(Ctx* ctx, float* p, size_t n);
 void comm_allreduce_sum(Ctx* ctx, double* p, size_t n);
+// Rank r's contiguous share [lo, hi) of `rows` rows.
+void comm_row_range(int64_t rows, int rank, int world, int64_t* lo, int64_t* hi);
+// Row-owner collectives over nbuf row-major [rows[k] x ldr] fp32 buffers (no-ops without a
+// communicator): reduce sums every rank's copy of rows [lo_r, hi_r) onto rank r;
+// gather broadcasts each owner's rows to every rank.
+void comm_reduce_rows(Ctx* ctx, float* const* bufs, const int64_t* rows, int nbuf, int ldr);
+void comm_gather_rows(Ctx* ctx, float* const* bufs, const int64_t* rows, int nbuf, int ldr);
 // Make the device error word identical on every rank (min of first codes, OR of bits),
 // so every rank takes the same accept / reject / raise decision.
 void comm_sync_flags(Ctx* ctx);

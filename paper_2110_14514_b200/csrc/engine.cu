@@ -450,6 +450,11 @@ static bool small_model(const ModelP& M) {
   return true;
 }
 
+// Multi-GPU factor solves of models past the small-model size split K5 by rows:
+// rank r updates a contiguous 1/N of every mode's rows.  Also
+// active in shard simulation, where rank r's share is all that runs.
+static bool row_sharded(const Ctx* ctx, const ModelP& M) { return ctx->world > 1 && !small_model(M); }
+
 static void grams_enqueue(Ctx* ctx, const ModelP& M, float* const* other, double* out_per_mode, HistBufs& hb,
                           bool self) {
   const int RR = M.rank * M.rank;
@@ -844,7 +849,11 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
   } else {
     sgrad_enqueue(ctx, *Sdrawn, M, s_f, L, gp, code_of(ev, 1));
   }
-  comm_allreduce_sum(ctx, W.grads.as<float>(), off);  // multi-GPU: sum of the shard gradients
+  // multi-GPU: sum of the shard gradients -- all of it for small models (replicated
+  // K5), else each mode's row block onto its owner (owner-computes K5)
+  const bool rowshard = row_sharded(ctx, M);
+  if (rowshard) comm_reduce_rows(ctx, gp, M.dims, M.ndim, M.ldr);
+  else comm_allreduce_sum(ctx, W.grads.as<float>(), off);
   const bool coeffs = hist || dense;
   if (coeffs) {
     if (hist) grams_pc_enqueue(ctx, M, old_factors, W.hb);
@@ -870,11 +879,15 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
     return;
   }
   for (int k = 0; k < M.ndim; ++k) {
-    factor_update_enqueue(ctx, M.dims[k], M.rank, M.ldr, A[k], hist ? old_factors[k] : nullptr, gp[k], ad->u[k],
-                          ad->v[k], coeffs ? W.hb.Mk.as<float>() + (size_t)k * RR : nullptr,
+    int64_t lo = 0, hi = M.dims[k];
+    if (rowshard) comm_row_range(M.dims[k], ctx->rank, ctx->world, &lo, &hi);
+    const size_t o = (size_t)lo * M.ldr;
+    factor_update_enqueue(ctx, hi - lo, M.rank, M.ldr, A[k] + o, hist ? old_factors[k] + o : nullptr, gp[k] + o,
+                          ad->u[k] + o, ad->v[k] + o, coeffs ? W.hb.Mk.as<float>() + (size_t)k * RR : nullptr,
                           coeffs ? W.hb.Nk.as<float>() + (size_t)k * RR : nullptr, cfg->reg_factors, rate_i,
                           cfg->beta1, cfg->beta2, cfg->adam_eps, cfg->lower_bound, code_of(ev, 2));
   }
+  if (rowshard) comm_gather_rows(ctx, A, M.dims, M.ndim, M.ldr);  // every rank gets the new factors
 }
 
 
@@ -984,6 +997,10 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     }
     ++epochs;
     objv.push_back(fest);
+  }
+  if (row_sharded(ctx, M)) {  // owners hold their rows' Adam moments: leave every rank the full state
+    comm_gather_rows(ctx, ad->u, M.dims, M.ndim, M.ldr);
+    comm_gather_rows(ctx, ad->v, M.dims, M.ndim, M.ldr);
   }
   OGCP_CUDA(cudaStreamSynchronize(st));
   *iteration = iter;

@@ -103,3 +103,61 @@ def test_nccl_entry_points_one_rank():
     bad = C.c_int32(-1)
     _lib.check(_lib.lib().ogcp_comm_selftest(_lib.ctx(), C.byref(bad)))
     assert bad.value == 0
+
+
+def test_row_sharded_update_partitions_rows():
+    """Models past the small-model size run K5 owner-computes across ranks: a
+    shard-simulated rank r of a world-N factor solve updates exactly its
+    contiguous row block [I r/N, I (r+1)/N) of every mode (factors and Adam
+    moments) and leaves every other row untouched; with N = 1 all rows move.
+    The blocks partition the rows, so after the owners' broadcasts every rank
+    holds one full, identical update."""
+    rng = np.random.default_rng(5)
+    dims = (5000, 300, 20)  # mode 0 past kSmallRows (4096): the per-mode K5 path
+    lin = rng.choice(int(np.prod(dims)), size=60_000, replace=False)
+    subs0 = np.array(np.unravel_index(np.sort(lin), dims)).T
+    X = P.SparseTensor.from_zero_based(dims, subs0, rng.integers(1, 4, size=lin.size).astype(float))
+    R = 6
+    init = [rng.uniform(0.2, 1.0, (d, R)) for d in dims]
+    w = np.full(R, 1.1)
+    cfg = P.SolverConfig(max_epochs_factors=1, iters_factors=2, rate_factors=1e-2,
+                         samples=P.SamplerConfig(None, 20000, 5000, 5000, seed=4))
+    loss = P.make_loss("poisson")
+    from paper_2110_14514_b200.solvers import solve_factors_device
+
+    def run(world, rank):
+        _lib.set_shard_sim(rank, world)
+        try:
+            model = P.DeviceModel.from_numpy(init)
+            adam = cfg.make_adam(cfg.rate_factors, loss)
+            adam.init_device(model.dims, model.rank)
+            _, tr = solve_factors_device(X, model, w, None, [], cfg, loss, adam, 0, 1)
+            A = [t[:, :R].double().cpu().numpy() for t in model.tensors]
+            u = [t[:, :R].double().cpu().numpy() for t in adam._buf["u"]]
+            return A, u, tr.rejections
+        finally:
+            _lib.set_shard_sim(0, 1)
+
+    A1, u1, rej = run(1, 0)
+    assert rej == 0
+    for k in range(3):
+        assert np.mean(np.any(A1[k] != init[k], axis=1)) > 0.99 and np.mean(np.any(u1[k] != 0, axis=1)) > 0.99
+    world = 3
+    accepted = 0
+    for r in range(world):
+        # rank r's objective share can reject the epoch, which restores the entry state
+        A, u, rej = run(world, r)
+        accepted += rej == 0
+        for k, d in enumerate(dims):
+            lo, hi = d * r // world, d * (r + 1) // world
+            own = np.zeros(d, bool)
+            own[lo:hi] = True
+            np.testing.assert_array_equal(A[k][~own], init[k][~own].astype(np.float32))
+            assert not np.any(u[k][~own])
+            if rej:
+                np.testing.assert_array_equal(A[k], init[k].astype(np.float32))
+                continue
+            # owned rows move unless rank r's sample share never touched them
+            assert np.mean(np.any(A[k][own] != init[k][own].astype(np.float32), axis=1)) > 0.9
+            assert np.mean(np.any(u[k][own] != 0, axis=1)) > 0.9
+    assert accepted >= 1
