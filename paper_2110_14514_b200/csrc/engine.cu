@@ -455,8 +455,23 @@ static bool small_model(const ModelP& M) {
 // active in shard simulation, where rank r's share is all that runs.
 static bool row_sharded(const Ctx* ctx, const ModelP& M) { return ctx->world > 1 && !small_model(M); }
 
+// Rows [lo, hi) of mode k this rank's Gram partials cover: all of them, or the
+// owned block when `shard` (the factor solves' per-iteration Grams of a
+// row-sharded solve; the partials are then all-reduced, 2dR^2 fp64).  An empty block zero-fills its outputs and returns false.
+static bool gram_rows(Ctx* ctx, const ModelP& M, bool shard, int k, int64_t* lo, int64_t* hi, double* o1,
+                      double* o2) {
+  *lo = 0;
+  *hi = M.dims[k];
+  if (shard) comm_row_range(M.dims[k], ctx->rank, ctx->world, lo, hi);
+  if (*hi > *lo) return true;
+  const size_t b = (size_t)M.rank * M.rank * 8;
+  OGCP_CUDA(cudaMemsetAsync(o1, 0, b, ctx->stream));
+  if (o2) OGCP_CUDA(cudaMemsetAsync(o2, 0, b, ctx->stream));
+  return false;
+}
+
 static void grams_enqueue(Ctx* ctx, const ModelP& M, float* const* other, double* out_per_mode, HistBufs& hb,
-                          bool self) {
+                          bool self, bool shard_rows = false) {
   const int RR = M.rank * M.rank;
   if (small_model(M)) {
     SmallGrams g{};
@@ -468,15 +483,21 @@ static void grams_enqueue(Ctx* ctx, const ModelP& M, float* const* other, double
     gram_small_enqueue(ctx, g, M.ndim, M.rank, M.ldr, out_per_mode, nullptr);
     return;
   }
+  const bool shard = shard_rows && row_sharded(ctx, M);
   for (int k = 0; k < M.ndim; ++k) {
-    const float* A = M.A[k];
-    const float* B = self ? M.A[k] : other[k];
-    gram_enqueue(ctx, A, B, M.dims[k], M.rank, M.ldr, out_per_mode + (int64_t)k * RR, hb.scratch);
+    int64_t lo, hi;
+    double* o = out_per_mode + (int64_t)k * RR;
+    if (!gram_rows(ctx, M, shard, k, &lo, &hi, o, nullptr)) continue;
+    const size_t off = (size_t)lo * M.ldr;
+    const float* A = M.A[k] + off;
+    const float* B = (self ? M.A[k] : other[k]) + off;
+    gram_enqueue(ctx, A, B, hi - lo, M.rank, M.ldr, o, hb.scratch);
   }
+  if (shard) comm_allreduce_sum(ctx, out_per_mode, (size_t)M.ndim * RR);
 }
 
 // P_m = A_m'A_m and C_m = Aold_m'A_m for every mode, one pass over each A_m.
-static void grams_pc_enqueue(Ctx* ctx, const ModelP& M, float* const* old, HistBufs& hb) {
+static void grams_pc_enqueue(Ctx* ctx, const ModelP& M, float* const* old, HistBufs& hb, bool shard_rows = false) {
   const int RR = M.rank * M.rank;
   if (small_model(M)) {
     SmallGrams g{};
@@ -489,9 +510,19 @@ static void grams_pc_enqueue(Ctx* ctx, const ModelP& M, float* const* old, HistB
     gram_small_enqueue(ctx, g, M.ndim, M.rank, M.ldr, hb.P.as<double>(), hb.C.as<double>());
     return;
   }
-  for (int k = 0; k < M.ndim; ++k)
-    gram2_enqueue(ctx, M.A[k], old[k], M.dims[k], M.rank, M.ldr, hb.P.as<double>() + (int64_t)k * RR,
-                  hb.C.as<double>() + (int64_t)k * RR, hb.scratch);
+  const bool shard = shard_rows && row_sharded(ctx, M);
+  for (int k = 0; k < M.ndim; ++k) {
+    int64_t lo, hi;
+    double* oP = hb.P.as<double>() + (int64_t)k * RR;
+    double* oC = hb.C.as<double>() + (int64_t)k * RR;
+    if (!gram_rows(ctx, M, shard, k, &lo, &hi, oP, oC)) continue;
+    const size_t off = (size_t)lo * M.ldr;
+    gram2_enqueue(ctx, M.A[k] + off, old[k] + off, hi - lo, M.rank, M.ldr, oP, oC, hb.scratch);
+  }
+  if (shard) {
+    comm_allreduce_sum(ctx, hb.P.as<double>(), (size_t)M.ndim * RR);
+    comm_allreduce_sum(ctx, hb.C.as<double>(), (size_t)M.ndim * RR);
+  }
 }
 
 // Device objective for a fixed sample set: returns data term + history + regs.
@@ -785,8 +816,8 @@ static double factor_objective(Ctx* ctx, const Slice* X, const SamplesP& So, con
   const bool reg = cfg->reg_factors != 0.0;
   std::vector<double> Ph;
   if (hist || reg || dense) {
-    if (hist) grams_pc_enqueue(ctx, M, old_factors, hb);
-    else grams_enqueue(ctx, M, nullptr, hb.P.as<double>(), hb, true);
+    if (hist) grams_pc_enqueue(ctx, M, old_factors, hb, collective);
+    else grams_enqueue(ctx, M, nullptr, hb.P.as<double>(), hb, true, collective);
     if (reg) {
       k_trace_sum<<<1, 1, 0, st>>>(M.ndim, M.rank, hb.P.as<double>(), dsc + 2);
       ctx->count();
@@ -856,8 +887,8 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
   else comm_allreduce_sum(ctx, W.grads.as<float>(), off);
   const bool coeffs = hist || dense;
   if (coeffs) {
-    if (hist) grams_pc_enqueue(ctx, M, old_factors, W.hb);
-    else grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true);
+    if (hist) grams_pc_enqueue(ctx, M, old_factors, W.hb, true);
+    else grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true, true);
     hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), hist ? W.hb.C.as<double>() : nullptr,
                         hist ? W.hb.S.as<double>() : nullptr, cfg->hist_weight, W.hb.Mk.as<float>(),
                         W.hb.Nk.as<float>(), dense_s, 2.0);
