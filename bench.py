@@ -381,7 +381,7 @@ def main():
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "nnz_per_slice": int(p), "q": Q, "p_obj": POBJ, "q_obj": QOBJ,
                        "rank": RANK, "iterations_per_step": steps_iters,
-                       "parallelism": f"samples{world} (sample-sharded, NCCL allreduce)" if world > 1 else "single",
+                       "parallelism": f"samples{world} (sample-sharded; NCCL row-owner reduce/broadcast around K5)" if world > 1 else "single",
                        "l2": "inputs larger than L2 (slice 1.6 GB + factors 256 MB)"},
             "slices_per_s": 1000.0 * args.steps / ms_max,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -3,10 +3,12 @@
 The reference is single-process.  Its sampled estimators are
 sums over samples, so the per-slice solve shards by samples: each rank
 evaluates a contiguous 1/world of every gradient and objective sample set
-(the same draws on every rank -- they are keyed, sampling.py:39-42), and the
-engine sums the factor gradients, the temporal-row gradient and the objective
-with NCCL over NVLink before the replicated fused Adam step.  Factors stay
-bitwise identical across ranks.
+(the same draws on every rank -- they are keyed, sampling.py:39-42).  The
+engine sums the temporal-row gradient and the objective with NCCL allreduces.
+Factor updates are owner-computes: rank r owns a contiguous 1/world of every
+mode's rows, the factor-gradient rows are reduced onto their owner, the owner
+runs the fused Adam (K5) and broadcasts the new rows (small models keep one
+allreduce and a replicated K5).  Factors stay bitwise identical across ranks.
 
     import torch.distributed as dist
     dist.init_process_group("nccl")
