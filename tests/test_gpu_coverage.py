@@ -80,6 +80,36 @@ def test_factor_solve_vs_oracle_ranks(R):
         assert rel_err(a, b) < 1e-4
 
 
+@pytest.mark.parametrize("R", [3, 20, 32])
+def test_factor_solve_vs_oracle_per_mode_k5(R):
+    """solve_factors with history + regularisation on a model past the small-model
+    size (a 5000-row mode): the per-mode K5 launches (shared-memory staged history
+    apply for R >= 4, shuffles below) against the oracle."""
+    dims = (5000, 30, 12)
+    subs0, vals = _slice(R + 7, dims, 3000)
+    rng = np.random.default_rng(R + 1)
+    A = [rng.uniform(0.2, 1.0, (d, R)) for d in dims]
+    Aold = [a * (1 + 0.02 * rng.uniform(-1, 1, a.shape)) for a in A]
+    s = rng.uniform(0.5, 1.5, R)
+    window = [(1, rng.uniform(0.1, 1.0, R)), (2, rng.uniform(0.1, 1.0, R))]
+    cfg = P.SolverConfig(max_epochs_factors=2, iters_factors=4, rate_factors=1e-2, hist_weight=2.0, hist_decay=0.9,
+                         reg_factors=0.05, samples=P.SamplerConfig(1500, 1500, 3000, 3000, seed=6))
+    loss = P.make_loss("poisson")
+    adam = cfg.make_adam(cfg.rate_factors, loss)
+    adam.init([a.copy() for a in A])
+    X = P.SparseTensor.from_zero_based(dims, subs0, vals)
+    res = P.solve_factors(X, A, s, Aold, window, cfg, loss, adam, 0, t=3)
+    ocfg = O.Cfg(kappa_f=2, tau_f=4, rate_f=1e-2, hist_weight=2.0, hist_decay=0.9, reg_factors=0.05, p=1500, q=1500,
+                 p_obj=3000, q_obj=3000, seed=6)
+    oadam = O.AdamOracle(1e-2, lower=0.0)
+    oadam.init([a.copy() for a in A])
+    fo, it, tr, _, _ = O.factor_solve(O.Slice(dims, subs0, vals), A, s, Aold, window, ocfg, "poisson", oadam, 0, 3)
+    assert res.iteration == it
+    np.testing.assert_allclose(res.trace.objective, tr, rtol=1e-4)
+    for a, b in zip(res.factors, fo):
+        assert rel_err(a, b) < 1e-4
+
+
 def test_errors_carry_reference_messages():
     dims = (20, 15, 10)
     subs0, vals = _slice(9, dims, 300)
