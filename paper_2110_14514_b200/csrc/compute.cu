@@ -1007,6 +1007,7 @@ __device__ __forceinline__ void factor_update_rows(int64_t rows, int rank, int l
   const int c = lane & (GR - 1);
   const bool col_on = c < rank;
   __shared__ float sm_m[GR * GR], sm_n[GR * GR];
+  __shared__ __align__(16) float sm_rows[(kThreads / 32) * 2 * RPI * 32];
   if (hist) {
     for (int e = threadIdx.x; e < GR * GR; e += blockDim.x) {
       const int r = e / GR, cc = e % GR;
@@ -1035,7 +1036,44 @@ __device__ __forceinline__ void factor_update_rows(int64_t rows, int rank, int l
       uo[q] = ok[q] ? u[at] : 0.f;
       vo[q] = ok[q] ? v[at] : 0.f;
     }
-    if (hist) {
+    if (hist && GR >= 4) {
+      // rows staged per warp in shared memory, read back as float4 broadcasts:
+      // 2 GR / 4 LDS.128 per row instead of 2 GR shuffles (K5 was MIO-bound)
+      const int w = threadIdx.x >> 5;
+      const int gb = lane & ~(GR - 1);  // first lane of this row group
+      float* sa = sm_rows + (size_t)w * (2 * RPI * 32);
+      float* so = sa + RPI * 32;
+#pragma unroll
+      for (int q = 0; q < RPI; ++q) {
+        sa[q * 32 + lane] = a[q];
+        if (has_old) so[q * 32 + lane] = ao[q];
+      }
+      __syncwarp();
+      float h[RPI];
+#pragma unroll
+      for (int q = 0; q < RPI; ++q) h[q] = 0.f;
+#pragma unroll 2
+      for (int r4 = 0; r4 < GR / 4; ++r4) {
+        float mr[4], nr[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          mr[j] = sm_m[(4 * r4 + j) * GR + c];
+          nr[j] = sm_n[(4 * r4 + j) * GR + c];
+        }
+#pragma unroll
+        for (int q = 0; q < RPI; ++q) {
+          const float4 av = *reinterpret_cast<const float4*>(sa + q * 32 + gb + 4 * r4);
+          h[q] += av.x * mr[0] + av.y * mr[1] + av.z * mr[2] + av.w * mr[3];
+          if (has_old) {
+            const float4 ov = *reinterpret_cast<const float4*>(so + q * 32 + gb + 4 * r4);
+            h[q] -= ov.x * nr[0] + ov.y * nr[1] + ov.z * nr[2] + ov.w * nr[3];
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < RPI; ++q) gv[q] += h[q];
+    } else if (hist) {
       float h[RPI];
 #pragma unroll
       for (int q = 0; q < RPI; ++q) h[q] = 0.f;
