@@ -766,15 +766,19 @@ __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], 
 }
 
 constexpr int kGramTcRows = 32;
+// rows per staged tile: ldr 32 rows are short, so a longer tile (and two CTAs
+// per SM, see gram2_enqueue) keeps enough bytes in flight per SM
+__host__ __device__ constexpr int gram_tc_rows(int ldr) { return ldr == 32 ? 128 : kGramTcRows; }
 template <int LDR>
 __global__ void __launch_bounds__(kThreads, 1) k_gram_tc(const float* __restrict__ A, const float* __restrict__ B,
                                                          int64_t rows, int64_t rows_per_block, int ngram,
                                                          double* __restrict__ partials) {
+  constexpr int TR = gram_tc_rows(LDR);
   constexpr int LDP = LDR + 8;
   constexpr int IB = LDR / 16, JB = LDR / 8;
   constexpr int WPI = 8 / IB;        // warps per i-block
   constexpr int JPW = JB / WPI;      // j-blocks per warp
-  constexpr int TILE = kGramTcRows * LDP;
+  constexpr int TILE = TR * LDP;
   extern __shared__ __align__(16) float gts[];  // [2 buffers][A tile, B tile]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gid = lane >> 2, tig = lane & 3;
@@ -791,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gram_tc(const float* __restrict
   auto stage = [&](int64_t rb, int buf) {
     float* da = gts + buf * 2 * TILE;
     float* db = da + TILE;
-    for (int e = threadIdx.x; e < kGramTcRows * (LDR / 4); e += blockDim.x) {
+    for (int e = threadIdx.x; e < TR * (LDR / 4); e += blockDim.x) {
       const int rr = e / (LDR / 4), c4 = e % (LDR / 4);
       const int64_t row = rb + rr;
       float* pa = da + rr * LDP + c4 * 4;
@@ -808,15 +812,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_gram_tc(const float* __restrict
   if (r0 < r1) stage(r0, 0);
   cp_async_commit();
   int buf = 0;
-  for (int64_t rb = r0; rb < r1; rb += kGramTcRows, buf ^= 1) {
-    if (rb + kGramTcRows < r1) stage(rb + kGramTcRows, buf ^ 1);
+  for (int64_t rb = r0; rb < r1; rb += TR, buf ^= 1) {
+    if (rb + TR < r1) stage(rb + TR, buf ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const float* ta = gts + buf * 2 * TILE;
     const float* tb = ta + TILE;
 #pragma unroll
-    for (int k0 = 0; k0 < kGramTcRows; k0 += 8) {
+    for (int k0 = 0; k0 < TR; k0 += 8) {
       // operand "A" of the MMA: L^T (16 x 8) from L = A (P) or B (C); operand "B": A (8 x 8)
       uint32_t ah[2][4], al[2][4];
 #pragma unroll
@@ -984,12 +988,15 @@ __device__ __forceinline__ bool adam_regs(float* __restrict__ A, float* __restri
 
 // rank <= 32: one group of GR lanes per row, lane c owns column c; Mk and Nk
 // are staged in shared memory (lane c reads column c, conflict-free) and rows
-// of A / Aold are broadcast across the group with shuffles.  RPI rows per group
+// of A / Aold reach the group through a per-warp shared-memory stage read as
+// float4 broadcasts (GR < 4: shuffles).  RPI rows per group
 // per pass with all five row streams (A, Aold, G, u, v) issued before any use:
 // one memory round trip per pass, and the small register footprint keeps
 // enough CTAs resident to cover the HBM latency.
 // K5 tuning (c4, measured): 4 rows per group pass, history loop unrolled by 8,
-// >= 3 CTAs per SM (80 registers, no spills): 0.27 -> 0.21 ms per launch.
+// >= 3 CTAs per SM (80 registers, no spills): 0.27 -> 0.21 ms per launch;
+// float4 broadcasts from the row stage instead of 2 GR shuffles per row: the
+// c4 average per launch 0.275 -> 0.189 ms (the shuffle form was MIO-bound).
 constexpr int kK5Rows = 4;
 constexpr int kK5Unroll = 8;
 template <int GR>
@@ -1605,11 +1612,12 @@ void sum_partials_enqueue(Ctx* ctx, const double* partials, int nblk, int len, d
 void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* outP,
                    double* outC, DevBuf& scratch) {
   const int ngram = B ? 2 : 1;
-  if (ldr == 64 || ldr == 128) {  // tensor-core path
-    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, kNumSMs));
+  if (ldr == 32 || ldr == 64 || ldr == 128) {  // tensor-core path
+    // ldr 32: two CTAs per SM (80 KB of tiles each) to cover the load latency
+    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, kNumSMs * (ldr == 32 ? 2 : 1)));
     const int64_t rpb = (rows + nblk - 1) / nblk;
     scratch.ensure((size_t)nblk * ngram * ldr * ldr * 8);
-    const size_t smem = (size_t)2 * 2 * kGramTcRows * (ldr + 8) * 4;
+    const size_t smem = (size_t)2 * 2 * gram_tc_rows(ldr) * (ldr + 8) * 4;
     auto go = [&](auto kern) {
       allow_smem(kern, smem);
       ProfScope prof_scope(ctx, kProfGram);
@@ -1620,7 +1628,8 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
       ctx->count();
       check_launch();
     };
-    if (ldr == 64) go(k_gram_tc<64>);
+    if (ldr == 32) go(k_gram_tc<32>);
+    else if (ldr == 64) go(k_gram_tc<64>);
     else go(k_gram_tc<128>);
     return;
   }
