@@ -160,61 +160,129 @@ def cpu_baseline_oracle(subs0, vals, dims, factors, weights, old, window, t, pq,
     return 2 * pq / best, best
 
 
-def run_reference(args):
-    """--impl reference: the oracle port of the reference path on the host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    import torch
-    import paper_2110_14514_b200 as P
-    from paper_2110_14514_b200.synthetic import gen_slice
-    torch.cuda.set_device(0)
-    X, factors, mix, total = gen_slice(DIMS, args.nnz, RANK, "poisson", seed=42)
-    subs0, vals = X.subs0, X.vals
-    del X
-    torch.cuda.empty_cache()
-    rng = np.random.default_rng(11)
+def _ref_import():
+    """The UNMODIFIED reference package ``ogcp`` 0.1.0, installed into baseline/_ref with
+    ``pip install --no-index --no-deps --target baseline/_ref``."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "ogcp")):
+        return None
+    sys.path.insert(0, path)
+    import ogcp
+    return ogcp
+
+
+def _ref_state(ogcp, dims, nnz, log):
+    """c4 slice + near-fit state for the reference arm, built without the product package:
+    oracle/planted.py (numpy; same planted model and seed as the GPU arm's generator, numpy
+    event draws) and the reference's own SparseTensor."""
+    from oracle.planted import gen_slice_np
+    t0 = time.perf_counter()
+    subs0, vals, factors, mix, total = gen_slice_np(dims, nnz, RANK, "poisson", seed=42)
+    log["generate_s"] = round(time.perf_counter() - t0, 1)
+    t0 = time.perf_counter()
+    X = ogcp.SparseTensor.from_zero_based(dims, subs0, vals)
+    log["sparse_tensor_s"] = round(time.perf_counter() - t0, 1)
+    rng = np.random.default_rng(11)  # same perturbation as make_state (GPU arm)
     init = [a * (1.0 + 0.05 * rng.uniform(-1, 1, a.shape)) for a in factors]
     w = total * np.asarray(mix)
     window = [(h, w * (1.0 + 0.05 * rng.uniform(-1, 1, w.shape))) for h in range(1, H + 1)]
-    from oracle import ogcp_oracle as O
-    Xo = O.Slice(DIMS, subs0, vals)
-    adam = O.AdamOracle(1e-3, lower=0.0)
-    adam.init(init)
-    pq = CPU_SAMPLE_PQ
-    # All host cores, sample-sharded (SURVEY 8(d) multi-process bound): each of n forked
-    # workers draws and evaluates (p+q)/n samples of the step (sampled_gradient_tensor and
-    # the sampled MTTKRP of factor_gradients on its share, factors shared copy-on-write,
-    # one BLAS thread each); the state-sized terms -- history Grams (multithreaded BLAS)
-    # and the Adam step -- run once in the parent.  The cross-process sum of the partial
-    # gradients is not timed (best case for the CPU).
+    return X, init, w, window
+
+
+def _ref_iteration(ogcp, X, factors, w, window, adam, loss, pq, key, it):
+    """One reference factor iteration: the body of solve_factors' loop (solvers.py:345-355)."""
+    from ogcp.sampling import sampled_gradient_tensor, rng_at
+    from ogcp.solvers import factor_gradients
+    Y = sampled_gradient_tensor(X, factors, w, loss, pq, pq, rng_at(7, *key))
+    grads = factor_gradients(Y, factors, w, old_factors=factors, window=window, hist_weight=1.0,
+                             hist_decay=1.0, t=H + 1, reg_factors=0.0)
+    return adam.step(factors, grads, it)
+
+
+def run_reference(args):
+    """--impl reference: the reference package's own CPU path on this host's cores.
+
+    Each step is one reference factor iteration at p = q = CPU_SAMPLE_PQ on the c4 slice,
+    sample-sharded over every host core (SURVEY 8(d) multi-process bound): n forked workers
+    each run the reference's sampled_gradient_tensor + sampled_mttkrp (x s) on (p+q)/n
+    samples; the parent runs the state-sized terms (history Grams, factor_gradients with an
+    empty Y) and the reference Adam step; the cross-process sum of the workers' partial
+    gradients is left out (best case for the CPU).  Before the timed steps, one single-process
+    iteration at two sample sizes splits the per-iteration cost into a fixed (state) part and
+    a per-sample part, extrapolated to the GPU arm's p = all (1e8 draws) / q = 2^24 and
+    labelled as such."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ogcp = _ref_import()
+    if ogcp is None:
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref/ogcp not installed"}), flush=True)
+        return
+    log = {}
+    X, init, w, window = _ref_state(ogcp, DIMS, args.nnz, log)
+    loss = ogcp.make_loss("poisson")
+    cfg = ogcp.SolverConfig(rate_factors=1e-3)
+    from threadpoolctl import threadpool_limits
+    # single process, two sizes: t(n) = t_fixed + n * t_sample (n = p + q)
+    single = {}
+    for pq in (CPU_SAMPLE_PQ // 4, CPU_SAMPLE_PQ):
+        adam = cfg.make_adam(1e-3, loss)
+        adam.init(init)
+        t0 = time.perf_counter()
+        _ref_iteration(ogcp, X, [a.copy() for a in init], w, window, adam, loss, pq,
+                       (H + 1, 3, 9, pq), 1)
+        single[pq] = time.perf_counter() - t0
+    n1, n2 = 2 * (CPU_SAMPLE_PQ // 4), 2 * CPU_SAMPLE_PQ
+    t_sample = max((single[CPU_SAMPLE_PQ] - single[CPU_SAMPLE_PQ // 4]) / (n2 - n1), 1e-12)
+    t_fixed = max(single[CPU_SAMPLE_PQ] - n2 * t_sample, 0.0)
+    n_full = args.nnz + Q
+    extrap = n_full / (t_fixed + n_full * t_sample)
+
     ncores = os.cpu_count() or 1
     nproc = max(1, min(ncores, REF_MAX_PROCS))
-    _REF.update(X=Xo, init=init, w=w, window=window, pq=max(1, pq // nproc))
+    _REF.update(ogcp=ogcp, X=X, init=init, w=w, loss=loss, pq=max(1, CPU_SAMPLE_PQ // nproc), nproc=nproc)
     import multiprocessing as mp
     pool = mp.get_context("fork").Pool(nproc) if nproc > 1 else None
+    from ogcp.solvers import factor_gradients
+    empty = ogcp.SparseTensor.from_zero_based(DIMS, np.empty((0, 3), np.int64), np.empty(0),
+                                              allow_zero_values=True)
+    adam = cfg.make_adam(1e-3, loss)
+    adam.init(init)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
         jobs = [(i, k) for k in range(nproc)]
         list(pool.map(_ref_share, jobs)) if pool else [_ref_share(j) for j in jobs]
-        state = O.assemble_factor_grads(np.empty((0, 3), np.int64), np.empty(0), DIMS, init, w, init, window, 1.0,
-                                        1.0, H + 1, 0.0)
-        adam.step([a.copy() for a in init], state, i + 1)
+        grads = factor_gradients(empty, init, w, old_factors=init, window=window, hist_weight=1.0,
+                                 hist_decay=1.0, t=H + 1, reg_factors=0.0)
+        adam.step([a.copy() for a in init], grads, i + 1)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
     if pool:
         pool.close()
     tot = sum(times)
-    value = args.steps * 2 * _REF["pq"] * nproc / tot
-    sample = (f"one factor iteration per step at p=q=2^19 on the c4 slice, sample-sharded over {nproc} forked "
-              f"processes (oracle numpy port; {ncores} host cores, at most {REF_MAX_PROCS} workers for memory)")
+    pq_done = _REF["pq"] * nproc
+    value = args.steps * 2 * pq_done / tot
+    sample = (f"one reference factor iteration per step (ogcp 0.1.0 from baseline/_ref: sampled_gradient_tensor"
+              f" + factor_gradients + Adam.step, solvers.py:345-355) at p=q={pq_done} on the c4 slice, "
+              f"sample-sharded over {nproc} forked processes ({ncores} host cores); slice from "
+              f"oracle/planted.py (same planted model/seed as the GPU arm, numpy event draws)")
     line = {"metric": "sampled GCP gradient entries/s", "value": value, "unit": "entries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD, "sample_per_step": sample},
-            "cpu_baseline": {"value": value, "unit": "entries/s", "cores": nproc, "kind": "port", "sample": sample},
+            "config": _config(1),
+            "config_note": (f"same workload as the GPU arm except the per-iteration sample: p=q={pq_done} "
+                            f"instead of p=all ({args.nnz} draws), q=2^24; see extrapolated"),
+            "cpu_baseline": {"value": value, "unit": "entries/s", "cores": nproc, "kind": "reference",
+                             "sample": sample},
+            "single_process": {"cores": 1, "seconds": {str(2 * k): round(v, 3) for k, v in single.items()},
+                               "fixed_s": round(t_fixed, 3), "per_sample_us": round(1e6 * t_sample, 4),
+                               "entries_per_s_at_pq": 2 * CPU_SAMPLE_PQ / single[CPU_SAMPLE_PQ],
+                               "extrapolated": {"value": extrap, "unit": "entries/s",
+                                                "note": f"EXTRAPOLATED to p+q={n_full} from the two "
+                                                        "single-process sizes (fixed + per-sample model)"}},
+            "setup": log,
             "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -224,17 +292,27 @@ REF_MAX_PROCS = 32
 
 
 def _ref_share(job):
-    """One worker's share of a reference-arm step (see run_reference): its samples' draw,
-    merged gradient tensor and sampled MTTKRP (times s) for every mode."""
-    from oracle import ogcp_oracle as O
+    """One worker's share of a reference-arm step: the reference's own draw + merged gradient
+    tensor (sampled_gradient_tensor) and sampled MTTKRP x s (factor_gradients' first term,
+    solvers.py:138-140) on (p+q)/n samples, scaled by 1/n so the shares sum to one estimate."""
+    from ogcp.kernels import sampled_mttkrp
+    from ogcp.sampling import rng_at, sampled_gradient_tensor
     from threadpoolctl import threadpool_limits
     step, k = job
     R = _REF
     with threadpool_limits(1):
-        _, ys, yv = O.sampled_y(R["X"], R["init"], R["w"], "poisson", R["pq"], R["pq"],
-                                O.keyed_rng(7, H + 1, 3, step, k))
-        g = [O.mttkrp(ys, yv, DIMS, R["init"], m) * R["w"][None, :] for m in range(len(DIMS))]
-    return float(g[0][0, 0])
+        Y = sampled_gradient_tensor(R["X"], R["init"], R["w"], R["loss"], R["pq"], R["pq"],
+                                    rng_at(7, H + 1, 3, step, k))
+        parts = [sampled_mttkrp(Y, R["init"], m) * (R["w"][None, :] / R["nproc"]) for m in range(len(DIMS))]
+    # the cross-process sum of the partial gradients is not timed (best case for the CPU arm)
+    return float(sum(p[0, 0] for p in parts))
+
+
+def _config(world):
+    return {"workload": WORKLOAD, "nnz_per_slice": NNZ, "q": Q, "p_obj": POBJ, "q_obj": QOBJ, "rank": RANK,
+            "iterations_per_step": 200,
+            "parallelism": f"samples{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2 (slice 1.6 GB + factors 256 MB)"}
 
 
 def main():
@@ -379,10 +457,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "nnz_per_slice": int(p), "q": Q, "p_obj": POBJ, "q_obj": QOBJ,
-                       "rank": RANK, "iterations_per_step": steps_iters,
-                       "parallelism": f"samples{world} (sample-sharded; NCCL row-owner reduce/broadcast around K5)" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (slice 1.6 GB + factors 256 MB)"},
+            "config": _config(world),
             "slices_per_s": 1000.0 * args.steps / ms_max,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgrad (K2+K3 fused eval/scatter)",

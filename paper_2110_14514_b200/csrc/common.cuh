@@ -193,6 +193,15 @@ struct Ctx {
   DevFlags* host_flags = nullptr;  // pinned
   void count(int n = 1) { launches += n; }
 };
+// Restores ctx->slack when a retry loop ends: the over-provisioning raised by a
+// draw shortfall applies to the retried draw/epoch only, not to every later one.
+struct SlackScope {
+  Ctx* ctx;
+  double saved;
+  explicit SlackScope(Ctx* c) : ctx(c), saved(c->slack) {}
+  ~SlackScope() { ctx->slack = saved; }
+};
+
 
 // RAII event bracket around the launches of one kernel class.
 struct ProfScope {

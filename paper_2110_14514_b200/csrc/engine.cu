@@ -415,6 +415,7 @@ static void draw_sync(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64
   b.size(p, q, X->ndim);
   b.semi = semi;
   const int64_t budget = budget_of(q, max_rejects);
+  SlackScope slack_scope(ctx);  // a shortfall raises the slack for this retry only
   for (int attempt = 0;; ++attempt) {
     reset_flags(ctx);
     const DrawOut o = draw_enqueue(ctx, X, g, p, q, budget, b.ord.as<int32_t>(), b.zero.as<int32_t>(), 0, b.scr,
@@ -685,6 +686,7 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   for (int epoch = 0; epoch < cfg->max_epochs_weights; ++epoch) {
     if (!(fest > cfg->tol_weights)) break;
     const double fold = fest;
+    SlackScope slack_scope(ctx);  // a shortfall raises the slack for this retry only
     for (int attempt = 0;; ++attempt) {
       reset_flags(ctx);
       const long long ev0 = ev;
@@ -985,6 +987,7 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
   for (int epoch = 0; epoch < cfg->max_epochs_factors; ++epoch) {
     if (!(fest > cfg->tol_factors)) break;
     const double fold = fest;
+    SlackScope slack_scope(ctx);  // a shortfall raises the slack for this retry only
     for (int attempt = 0;; ++attempt) {
       reset_flags(ctx);
       const long long ev0 = ev;
@@ -1142,6 +1145,7 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
   for (int epoch = 0; epoch < max_epochs; ++epoch) {
     if (!(fest > tol)) break;
     const double fold = fest;
+    SlackScope slack_scope(ctx);  // a shortfall raises the slack for this retry only
     for (int attempt = 0;; ++attempt) {
       reset_flags(ctx);
       const long long ev0 = ev;
@@ -1516,6 +1520,7 @@ int ogcp_draw_samples_ex(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, cons
   precheck_draw(s, p, semi ? 0 : q);
   const int64_t budget = budget_of(q, max_rejects);
   static thread_local DrawScratch scr;
+  SlackScope slack_scope(ctx);  // a shortfall raises the slack for this retry only
   for (int attempt = 0;; ++attempt) {
     reset_flags(ctx);
     const int32_t* z =

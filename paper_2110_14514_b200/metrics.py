@@ -63,6 +63,7 @@ def local_loss(X, model, loss, *, mode: str = "exact", p: Optional[int] = None, 
             raise DataError("sampled local loss needs an rng")
         if not isinstance(rng, RngKey):
             raise TypeError("pass a generator made by rng_at(seed, *key)")
+        rng._consume()
         key, kp = _lib.i64arr(list(rng.key) or [0])
         _lib.check(_lib.lib().ogcp_local_loss(
             _lib.ctx(), X._handle, C.byref(dm.c()), wp, C.byref(loss._c()), 1, -1 if p is None else int(p),

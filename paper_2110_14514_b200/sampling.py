@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from .exceptions import DataError
+from .exceptions import DataError, SamplingError
 from .losses import LossFunction
 from .tensor import DeviceModel, SparseTensor
 
@@ -36,13 +36,25 @@ class RngKey:
     """A keyed generator handle, ``rng_at(seed, *key)`` (sampling.py:39-42).
 
     The engine derives the PCG64 stream from (seed, key) itself; host-side
-    scalar draws (reservoir window) use the engine's host restatement."""
+    scalar draws (reservoir window) use the engine's host restatement.  Every
+    draw replays the keyed stream from its start, so a handle serves exactly one
+    draw (the reference makes a fresh rng_at per draw: sampling.py:39-42,
+    solvers.py:227-345, streaming.py:51); a second use raises instead of
+    silently repeating the first draw's values."""
 
     def __init__(self, seed: int, key: tuple):
         self.seed = int(seed)
         self.key = tuple(int(k) for k in key)
+        self._used = False
+
+    def _consume(self):
+        if self._used:
+            raise SamplingError(f"{self!r} was already drawn from; keyed streams replay from their start, "
+                                "so make a fresh rng_at(seed, *key) for every draw")
+        self._used = True
 
     def integers(self, low, high=None, size=None):
+        self._consume()
         if high is None:
             low, high = 0, low
         if size is None:
@@ -147,6 +159,7 @@ class SampleSet:
 
 def _key_of(rng) -> RngKey:
     if isinstance(rng, RngKey):
+        rng._consume()
         return rng
     raise TypeError("pass a generator made by rng_at(seed, *key); the engine replays that keyed stream")
 

@@ -98,8 +98,9 @@ class SparseTensor:
         if vals.ndim != 1 or vals.shape[0] != subs0.shape[0]:
             raise DataError("vals must be a vector matching the entry count")
         self.dims = dims
-        self._subs0_host = subs0
-        self._vals_host = vals
+        # read-only views: the caller's own arrays stay writable
+        self._subs0_host = subs0.view()
+        self._vals_host = vals.view()
         self._nnz = int(vals.shape[0])
         self._fetch = None
         dev = torch.cuda.current_device() if torch.cuda.is_available() else None

@@ -1,0 +1,86 @@
+"""Sampler parity at the bench scale (BASELINE configs[3]): the
+1M x 1M x 1K planted Poisson slice with 1e8 nonzeros, p = "all" (eta = 1e8 draws
+with replacement) and q = 2^24 zeros, keyed like a factor-solve iteration.
+
+* The engine's draw (ogcp_draw_samples) equals numpy's keyed stream bit for bit:
+  ordinals = rng.integers(0, eta, p) (sampling.py:125) and the zero rows of the
+  batched rejection loop (sampling.py:133-150) against the stored set.
+* The merged (count) form the solve evaluates -- the ordinal histogram, permuted
+  into the row-bucketed walk -- equals np.bincount of those ordinals, entry for
+  entry, with the same accepted zero rows (sampled_gradient_tensor's merge,
+  sampling.py:233-237).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2110_14514_b200 as P
+from paper_2110_14514_b200 import _lib
+from paper_2110_14514_b200.synthetic import gen_slice
+from oracle import ogcp_oracle as O
+
+DIMS = (1_000_000, 1_000_000, 1_000)
+NNZ = 100_000_000
+Q = 1 << 24
+KEY = (31, 3, 0, 17)   # (t, PHASE_FACTOR_GRAD, epoch, it) of rng_at(seed, ...), solvers.py:345
+
+
+@pytest.fixture(scope="module")
+def c4():
+    X, factors, mix, total = gen_slice(DIMS, NNZ, 32, "poisson", seed=42)
+    subs0 = X.subs0
+    lin = subs0 @ O.strides_of(DIMS)
+    assert lin.size == NNZ and bool(np.all(np.diff(lin) > 0))  # stored in ascending linear order
+    yield X, lin
+    del X
+    torch.cuda.empty_cache()
+
+
+def numpy_draw(lin_sorted, p, q, seed, key):
+    """sampling.py:108-153 on the keyed numpy stream, membership by binary search (tensor.py:163-169)."""
+    gen = O.keyed_rng(seed, *key)
+    ords = gen.integers(0, lin_sorted.size, size=p)
+    hi = np.asarray(DIMS, dtype=np.int64)
+    st = O.strides_of(DIMS)
+    kept, need = [], q
+    while need > 0:
+        cand = gen.integers(0, hi, size=(need, len(DIMS)), dtype=np.int64)
+        cl = cand @ st
+        pos = np.minimum(np.searchsorted(lin_sorted, cl), lin_sorted.size - 1)
+        miss = lin_sorted[pos] != cl
+        kept.append(cand[miss])
+        need -= int(miss.sum())
+    return ords, np.concatenate(kept)
+
+
+def test_c4_draw_bit_exact(c4):
+    X, lin = c4
+    s = P.draw_samples(X, NNZ, Q, P.rng_at(7, *KEY))
+    ords, zeros = numpy_draw(lin, NNZ, Q, 7, KEY)
+    got = s.ord_dev.cpu().numpy()
+    assert got.shape == (NNZ,)
+    assert np.array_equal(got.astype(np.int64), ords)
+    assert np.array_equal(s.zero_subs0, zeros)
+
+
+@pytest.mark.parametrize("buckets", [0, 4])
+def test_c4_merged_counts_equal_bincount(c4, buckets):
+    X, lin = c4
+    ords, zeros = numpy_draw(lin, NNZ, Q, 7, KEY)
+    counts = np.bincount(ords, minlength=NNZ)
+    del ords
+    _lib.set_buckets(buckets)  # 0: plain ordinal order; 4: the bench's row-bucketed walk
+    try:
+        o, c, z = _lib.debug_solve_draw(X, 7, KEY, None, Q, ldr=32)
+    finally:
+        _lib.set_buckets(1)
+    order = np.argsort(o, kind="stable")
+    o, c = o[order], c[order]
+    nzr = np.flatnonzero(counts)
+    assert np.array_equal(o, nzr), "merged ordinals differ from the distinct drawn ordinals"
+    assert np.array_equal(c, counts[nzr]), "multiplicities differ from np.bincount"
+    assert int(c.sum()) == NNZ
+    assert np.array_equal(z, zeros)

@@ -68,3 +68,15 @@ def test_config_validation_mirrors_reference():
     c = SolverConfig(samples=SamplerConfig(None, 5, None, 7, seed=3))
     cc = c._c(__import__("paper_2110_14514_b200").make_loss("poisson"))
     assert cc.samples.grad_nonzeros == -1 and cc.samples.obj_zeros == 7 and cc.lower_bound == 0.0
+
+
+def test_rng_handle_is_single_use():
+    """A keyed handle replays its stream from the start, so a second draw from it raises
+    instead of silently repeating the first one (reference: fresh rng_at per draw)."""
+    from paper_2110_14514_b200.exceptions import SamplingError
+    g = rng_at(3, 1, 5)
+    first = g.integers(1, 10)
+    assert 1 <= first < 10
+    with pytest.raises(SamplingError):
+        g.integers(1, 10)
+    assert rng_at(3, 1, 5).integers(1, 10) == first
