@@ -264,6 +264,11 @@ def debug_solve_draw(X, seed: int, key, p, q: int, ldr: int, max_rejects=None):
     return ords[:nn.value].astype(np.int64), cnts[:nn.value].astype(np.int64), zeros[:nz.value].astype(np.int64)
 
 
+def set_sort_zeros(on: bool):
+    """Engine option OGCP_OPT_SORT_ZEROS: zero rows of bucketed merged draws in walk order."""
+    check(lib().ogcp_ctx_set_option(ctx(), 5, int(bool(on))))
+
+
 def set_split_scatter(on: bool):
     """Engine option OGCP_OPT_SPLIT_SCATTER for the current device's context."""
     check(lib().ogcp_ctx_set_option(ctx(), 2, int(bool(on))))

@@ -166,6 +166,7 @@ struct Ctx {
   // c4 it measured 19.2 ms vs 10.2 ms for the fused pass (profiles/), the second
   // pass repeating the gather latency chain without saving enough traffic.
   bool split_scatter = false;
+  bool sort_zeros = true;       // bucketed merged draws: zero rows sorted by (bucket, mode-0 row)
   bool buckets = true;          // bucketed layout for merged sets of large slices (OGCP_OPT_BUCKETS)
   int buckets_force = 0;        // > 1: always bucket, with this many buckets (tests)
   DevBuf ybuf;                  // per-sample y of the split scatter

@@ -25,6 +25,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "hash.cuh"
 #include "sampler.cuh"
@@ -1016,6 +1018,80 @@ static void run_stream_dispatch(int ncol, Ctx* ctx, const StreamSpec& sp, const 
 
 static double reject_rate(uint32_t n) { return (double)lemire_threshold(n) / 4294967296.0; }
 
+// Sorted zero stratum (bucketed merged solves).  Key of candidate row r =
+// (row bucket of its bucket-mode coordinate) << b0 | (mode-0 row >> s0), the
+// order of the bucketed nonzero walk (Slice::perm); rejected candidates (first
+// coordinate -1) and rows past the q-th miss get the sentinel 1 << kb, so a
+// stable radix sort on kb + 1 bits lists the q accepted rows first, in
+// (bucket, mode-0 row, draw) order -- a fixed permutation of the reference's
+// zero set, so the walk (and its float sums) stays deterministic.
+__global__ void k_zero_sort_keys(const int32_t* __restrict__ cand, int ndim, int64_t rows,
+                                 const long long* __restrict__ q_rows, int bmode, long long bdim, int nb, int b0,
+                                 int s0, int kb, uint32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const int64_t R = *q_rows;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t* c = cand + i * ndim;
+    const int32_t c0 = c[0];
+    uint32_t key = 1u << kb;
+    if (i < R && c0 >= 0) {
+      const uint32_t b = (uint32_t)(((long long)c[bmode] * nb) / bdim);
+      key = (b << b0) | ((uint32_t)c0 >> s0);
+    }
+    keys[i] = key;
+    vals[i] = (int32_t)i;
+  }
+}
+
+__global__ void k_zero_sorted_gather(const int32_t* __restrict__ cand, int ndim, const int32_t* __restrict__ idx,
+                                     int64_t q, int32_t* __restrict__ out) {
+  const int64_t total = q * ndim;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / ndim;
+    out[e] = __ldg(cand + (int64_t)__ldg(idx + j) * ndim + (e - j * ndim));
+  }
+}
+
+static int bits_for(int64_t n) {  // bits to hold values 0 .. n-1
+  int b = 0;
+  while (b < 62 && ((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+// Sort the lazy layout's accepted zero rows into the bucketed walk order (see
+// k_zero_sort_keys); returns the [q x ndim] sorted rows in scr.zsorted.
+static const int32_t* sort_zero_rows(Ctx* ctx, const Slice* X, DrawScratch& scr, int64_t rows, int64_t q,
+                                     const long long* q_rows) {
+  cudaStream_t s = ctx->stream;
+  const int d = X->ndim;
+  const int nbb = bits_for(X->nbuckets);
+  const int i0b = bits_for(X->dims[0]);
+  const int b0 = std::min(i0b, 30 - nbb);
+  const int s0 = i0b - b0;
+  const int kb = nbb + b0;
+  scr.zkey.ensure((size_t)rows * 4);
+  scr.zkey_s.ensure((size_t)rows * 4);
+  scr.zval.ensure((size_t)rows * 4);
+  scr.zval_s.ensure((size_t)rows * 4);
+  scr.zsorted.ensure((size_t)std::max<int64_t>(q, 1) * d * 4);
+  const int grid = (int)std::min<int64_t>((rows + 255) / 256, (int64_t)kNumSMs * 8);
+  k_zero_sort_keys<<<grid, 256, 0, s>>>(scr.cand.as<int32_t>(), d, rows, q_rows, X->bucket_mode,
+                                        (long long)X->dims[X->bucket_mode], X->nbuckets, b0, s0, kb,
+                                        scr.zkey.as<uint32_t>(), scr.zval.as<int32_t>());
+  size_t tb = 0;
+  OGCP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, scr.zkey.as<uint32_t>(), scr.zkey_s.as<uint32_t>(),
+                                            scr.zval.as<int32_t>(), scr.zval_s.as<int32_t>(), (int)rows, 0, kb + 1,
+                                            s));
+  scr.ztmp.ensure(tb);
+  OGCP_CUDA(cub::DeviceRadixSort::SortPairs(scr.ztmp.ptr, tb, scr.zkey.as<uint32_t>(), scr.zkey_s.as<uint32_t>(),
+                                            scr.zval.as<int32_t>(), scr.zval_s.as<int32_t>(), (int)rows, 0, kb + 1,
+                                            s));
+  const int ggrid = (int)std::min<int64_t>((q * d + 255) / 256, (int64_t)kNumSMs * 8);
+  k_zero_sorted_gather<<<ggrid, 256, 0, s>>>(scr.cand.as<int32_t>(), d, scr.zval_s.as<int32_t>(), q,
+                                             scr.zsorted.as<int32_t>());
+  ctx->count(2 + (kb + 8) / 8);
+  return scr.zsorted.as<int32_t>();
+}
+
 // Enqueue one stratified draw.  ordinals: int32 [p]; zero_subs: int32 [q x ndim].
 // code: event code (event*4) recorded on sampling errors / shortfall.
 DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
@@ -1222,8 +1298,13 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
       k_zero_locate<<<1, kScanThreads, 0, s>>>(scr.zcount.as<uint32_t>(), scr.zoff.as<long long>(), zblocks,
                                                scr.miss.as<uint8_t>(), rows_max, q, sc + 8, z_hits_before);
       ctx->count();
-      out.zsub = scr.cand.as<int32_t>();
-      out.q_dev = sc + 8;
+      if (merged && merged->perm && ctx->sort_zeros && X->bucket_mode > 0 && q >= 65536 && rows_max < INT32_MAX) {
+        out.zsub = sort_zero_rows(ctx, X, scr, rows_max, q, sc + 8);  // exactly q rows, walk order
+        out.q_dev = nullptr;
+      } else {
+        out.zsub = scr.cand.as<int32_t>();
+        out.q_dev = sc + 8;
+      }
     } else {
       const size_t smem = (size_t)kRowsPerBlock * d * 4;
       if (smem > 48 * 1024)

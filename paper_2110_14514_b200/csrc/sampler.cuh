@@ -5,6 +5,7 @@ namespace ogcp {
 
 struct DrawScratch {
   DevBuf tmaps, bagg, bstart, scal, cand, miss, zcount, zoff;
+  DevBuf zkey, zkey_s, zval, zval_s, zsorted, ztmp;  // sorted zero rows (bucketed merged solves)
 };
 
 // Merged nonzero stratum of a draw: the distinct drawn ordinals in ascending

@@ -83,4 +83,9 @@ def test_c4_merged_counts_equal_bincount(c4, buckets):
     assert np.array_equal(o, nzr), "merged ordinals differ from the distinct drawn ordinals"
     assert np.array_equal(c, counts[nzr]), "multiplicities differ from np.bincount"
     assert int(c.sum()) == NNZ
+    if buckets:
+        # bucketed solves walk the zero rows sorted (stably) by (row bucket of mode 1, mode-0 row):
+        # the same rows as the reference's draw, in the walk order (sampler.cu k_zero_sort_keys)
+        key = (zeros[:, 1] * buckets // DIMS[1]) * DIMS[0] + zeros[:, 0]
+        zeros = zeros[np.argsort(key, kind="stable")]
     assert np.array_equal(z, zeros)
