@@ -342,8 +342,10 @@ def main():
         _lib.set_split_scatter(True)
     if os.environ.get("OGCP_BUCKETS"):  # A/B knob for the bucketed merged walk: 0 off, k > 1 forces k buckets
         _lib.set_buckets(int(os.environ["OGCP_BUCKETS"]))
-    if os.environ.get("OGCP_SORT_ZEROS") == "0":  # A/B knob for the sorted zero rows
-        _lib.set_sort_zeros(False)
+    if os.environ.get("OGCP_SORT_ZEROS"):  # A/B knob for the sorted zero rows
+        _lib.set_sort_zeros(os.environ["OGCP_SORT_ZEROS"] == "1")
+    if os.environ.get("OGCP_LEAN") == "0":  # A/B knob for the lean 3-way walk kernels
+        _lib.set_lean_walks(False)
     if os.environ.get("OGCP_MERGE") == "0":  # A/B knob for the merged draws
         _lib.set_merge_draws(False)
     loss = P.make_loss("poisson")

@@ -155,12 +155,15 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * communicator -- the solves then run rank `rank`'s share of a world-`world`
  * multi-GPU solve with the collectives skipped (single-process tests of the
  * shard partition); world 1 (or 0) restores the single-GPU context. */
-/* OGCP_OPT_SORT_ZEROS (default 1): in a bucketed merged solve, the accepted zero
+/* OGCP_OPT_SORT_ZEROS (default 0): in a bucketed merged solve, the accepted zero
  * rows of every draw are sorted (stable radix sort) by (row bucket, mode-0 row) so
  * the zero part of the walk meets the same L2-resident bucket rows and streams
  * mode 0 in order like the nonzero part; 0 keeps the draw order (lazy layout). */
 enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 3, OGCP_OPT_SHARD_SIM = 4,
-       OGCP_OPT_SORT_ZEROS = 5 };
+       OGCP_OPT_SORT_ZEROS = 5, OGCP_OPT_LEAN_WALKS = 6 };
+/* OGCP_OPT_LEAN_WALKS (default 1): merged sample sets of 3-way slices
+ * are evaluated by the specialised walk kernels (csrc/walk3.cuh, ldr 16 / 32); 0 uses the
+ * generic sample kernels. */
 int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value);
 
 /* Multi-GPU (the reference is single-process): the

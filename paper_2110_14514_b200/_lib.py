@@ -269,6 +269,11 @@ def set_sort_zeros(on: bool):
     check(lib().ogcp_ctx_set_option(ctx(), 5, int(bool(on))))
 
 
+def set_lean_walks(on: bool):
+    """Engine option OGCP_OPT_LEAN_WALKS: specialised 3-way walk kernels for merged sets."""
+    check(lib().ogcp_ctx_set_option(ctx(), 6, int(bool(on))))
+
+
 def set_split_scatter(on: bool):
     """Engine option OGCP_OPT_SPLIT_SCATTER for the current device's context."""
     check(lib().ogcp_ctx_set_option(ctx(), 2, int(bool(on))))

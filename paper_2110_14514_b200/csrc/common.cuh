@@ -166,7 +166,9 @@ struct Ctx {
   // c4 it measured 19.2 ms vs 10.2 ms for the fused pass (profiles/), the second
   // pass repeating the gather latency chain without saving enough traffic.
   bool split_scatter = false;
-  bool sort_zeros = true;       // bucketed merged draws: zero rows sorted by (bucket, mode-0 row)
+  bool sort_zeros = false;      // bucketed merged draws: zero rows sorted by (bucket, mode-0 row);
+                                // off: c4 measured +0.5 ms per draw for -0.3 ms of k_sgrad
+  bool lean_walks = true;       // walk3.cuh kernels for merged 3-way sets
   bool buckets = true;          // bucketed layout for merged sets of large slices (OGCP_OPT_BUCKETS)
   int buckets_force = 0;        // > 1: always bucket, with this many buckets (tests)
   DevBuf ybuf;                  // per-sample y of the split scatter

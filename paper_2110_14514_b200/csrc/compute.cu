@@ -1398,6 +1398,8 @@ using IC = std::integral_constant<int, N>;
 // mode), the reductions (weight gradient, objective) prefer 4 lanes x 2 chunks
 // (half the per-sample scalar work per warp instruction).  U = 2 keeps the
 // pipelined gathers below ~130 registers.
+#include "walk3.cuh"
+
 enum class Layout { Scatter, Reduce };
 
 template <class F>
@@ -1473,6 +1475,67 @@ static int sample_grid(K kern, size_t smem, int64_t total, int G, int U) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)kNumSMs * per_sm));
 }
 
+// The lean 3-way walks (walk3.cuh) serve merged sets of 3-way slices at ldr 16 / 32
+// (at ldr 64 the double-buffered rows exceed the register budget).
+static bool lean_walk(const Ctx* ctx, const SamplesP& S, const ModelP& M) {
+  return ctx->lean_walks && M.ndim == 3 && S.cnt != nullptr && S.rec_ints == 4 && !S.semi &&
+         (M.ldr == 16 || M.ldr == 32) && (S.shard_world <= 1 || S.zshard);
+}
+
+template <bool ZERO>
+static walk3::Walk<ZERO> walk_of(const SamplesP& S) {
+  walk3::Walk<ZERO> W;
+  W.pos = S.ord;
+  W.cnt = S.cnt;
+  W.rec = S.rec;
+  W.zsub = S.zsub;
+  W.n_dev = ZERO ? S.q_dev : S.p_dev;
+  W.n_host = ZERO ? S.q : S.p;
+  W.shard_rank = S.shard_rank;
+  W.shard_world = ZERO && S.zshard ? S.shard_world : 1;
+  return W;
+}
+
+// Launch a lean walk kernel over an (upper-bound) entry count; returns the grid.
+template <class K, class... A>
+static int lean_launch(Ctx* ctx, K kern, int64_t n_est, A... args) {
+  const int per_sm = std::max(occupancy(kern, 0), 1);
+  const int64_t need = (n_est + (kThreads / 32) * walk3::kChunk - 1) / ((kThreads / 32) * walk3::kChunk);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)kNumSMs * per_sm));
+  kern<<<grid, kThreads, 0, ctx->stream>>>(args...);
+  ctx->count();
+  return grid;
+}
+
+template <int V>
+static void sgrad3_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                           const GradPtrs& GP, long long code) {
+  DevFlags* fl = ctx->flags.as<DevFlags>();
+  if (S.p > 0)
+    lean_launch(ctx, walk3::k_sgrad3<V, false>, S.p, walk_of<false>(S), M, s_f, L, (float)S.nz_scale, GP, fl, code);
+  if (S.q > 0) {
+    const int64_t zest = S.q_dev ? S.q + S.q / 64 + 1024 : S.q;
+    lean_launch(ctx, walk3::k_sgrad3<V, true>, zest / std::max(S.zshard ? S.shard_world : 1, 1), walk_of<true>(S),
+                M, s_f, L, (float)S.zero_scale, GP, fl, code);
+  }
+}
+
+template <int V>
+static int wgrad3_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                          double* partials, long long code) {
+  DevFlags* fl = ctx->flags.as<DevFlags>();
+  int nb = 0;
+  if (S.p > 0)
+    nb += lean_launch(ctx, walk3::k_wgrad3<V, false>, S.p, walk_of<false>(S), M, s_f, L, (float)S.nz_scale,
+                      partials, fl, code);
+  if (S.q > 0) {
+    const int64_t zest = S.q_dev ? S.q + S.q / 64 + 1024 : S.q;
+    nb += lean_launch(ctx, walk3::k_wgrad3<V, true>, zest / std::max(S.zshard ? S.shard_world : 1, 1),
+                      walk_of<true>(S), M, s_f, L, (float)S.zero_scale, partials + (int64_t)nb * M.ldr, fl, code);
+  }
+  return std::max(nb, 1);
+}
+
 void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
                    float* const* grads, long long code) {
   GradPtrs GP;
@@ -1524,6 +1587,13 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
       }
     }
   }
+  if (PV.nmodes == 0 && split < 0 && lean_walk(ctx, S, M)) {
+    ProfScope prof_scope(ctx, kProfSgrad);
+    if (M.ldr == 16) sgrad3_enqueue<1>(ctx, S, M, s_f, L, GP, code);
+    else sgrad3_enqueue<2>(ctx, S, M, s_f, L, GP, code);
+    check_launch();
+    return;
+  }
   float* ybuf = split >= 0 ? static_cast<float*>(ctx->ybuf.ensure((size_t)total * 4)) : nullptr;
   ProfScope prof_scope(ctx, kProfSgrad);
   dispatch_layout(Layout::Scatter, M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc, auto Uc) {
@@ -1553,6 +1623,12 @@ int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f
   const int64_t total = S.p + S.q;
   int grid = 1;
   ProfScope prof_scope(ctx, kProfWgrad);
+  if (lean_walk(ctx, S, M) && total > 0) {
+    if (M.ldr == 16) grid = wgrad3_enqueue<1>(ctx, S, M, s_f, L, partials, code);
+    else grid = wgrad3_enqueue<2>(ctx, S, M, s_f, L, partials, code);
+    check_launch();
+    return grid;
+  }
   dispatch_layout(Layout::Reduce, M.ndim, M.ldr, [&](auto Dc, auto Gc, auto Vc, auto Uc) {
     constexpr int D = decltype(Dc)::value, G = decltype(Gc)::value, V = decltype(Vc)::value;
     constexpr int U = decltype(Uc)::value;

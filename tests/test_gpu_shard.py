@@ -63,12 +63,12 @@ def test_plain_draw_shards_partition(slice_1e5):
     np.testing.assert_array_equal(np.concatenate([q[2] for q in parts]), z)
 
 
-def test_sharded_gradients_sum_to_single_gpu(slice_1e5):
+@pytest.mark.parametrize("R", [6, 20])
+def test_sharded_gradients_sum_to_single_gpu(slice_1e5, R):
     """Shard-simulated factor solves of one iteration with rate ~0: every rank's
     K3 output is its partial gradient, so the per-rank first Adam moments
-    (u = (1-b1) g) must sum to the single-GPU one."""
+    (u = (1-b1) g) must sum to the single-GPU one (R = 20: the lean 3-way walks)."""
     X = slice_1e5
-    R = 6
     rng = np.random.default_rng(2)
     init = [rng.uniform(0.2, 1.0, (d, R)) for d in X.dims]
     w = np.full(R, 1.1)
@@ -161,3 +161,36 @@ def test_row_sharded_update_partitions_rows():
             assert np.mean(np.any(A[k][own] != init[k][own].astype(np.float32), axis=1)) > 0.9
             assert np.mean(np.any(u[k][own] != 0, axis=1)) > 0.9
     assert accepted >= 1
+
+
+@pytest.mark.parametrize("R", [12, 20])
+@pytest.mark.parametrize("buckets", [1, 4])
+def test_lean_walk_gradient_matches_generic(slice_1e5, R, buckets):
+    """One factor iteration with rate ~0 (u = (1-b1) g): the lean 3-way walk kernels
+    and the generic sample kernels give the same factor gradients (fp32 reduction
+    order only)."""
+    X = slice_1e5
+    rng = np.random.default_rng(5)
+    init = [rng.uniform(0.2, 1.0, (d, R)) for d in X.dims]
+    w = np.full(R, 0.9)
+    cfg = P.SolverConfig(max_epochs_factors=1, iters_factors=1, rate_factors=1e-30,
+                         samples=P.SamplerConfig(None, 7000, 5000, 5000, seed=9))
+    loss = P.make_loss("poisson")
+
+    def u_of(lean):
+        _lib.set_lean_walks(lean)
+        _lib.set_buckets(buckets)
+        try:
+            model = P.DeviceModel.from_numpy(init)
+            adam = cfg.make_adam(cfg.rate_factors, loss)
+            adam.init_device(model.dims, model.rank)
+            from paper_2110_14514_b200.solvers import solve_factors_device
+            solve_factors_device(X, model, w, None, [], cfg, loss, adam, 0, 1)
+            return [t[:, :R].double().cpu().numpy() for t in adam._buf["u"]]
+        finally:
+            _lib.set_lean_walks(True)
+            _lib.set_buckets(1)
+
+    a, b = u_of(True), u_of(False)
+    for k in range(3):
+        assert np.linalg.norm(a[k] - b[k]) <= 1e-6 * np.linalg.norm(b[k])
