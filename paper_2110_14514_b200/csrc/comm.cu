@@ -32,6 +32,9 @@ struct NcclApi {
   ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
                          cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
@@ -53,13 +56,15 @@ NcclApi& api() {
     a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(a.lib, "ncclAllReduce"));
     a.Reduce = reinterpret_cast<decltype(a.Reduce)>(dlsym(a.lib, "ncclReduce"));
     a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(dlsym(a.lib, "ncclBroadcast"));
+    a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(dlsym(a.lib, "ncclReduceScatter"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(a.lib, "ncclAllGather"));
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.lib, "ncclGroupStart"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.lib, "ncclGroupEnd"));
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.lib, "ncclCommDestroy"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(a.lib, "ncclGetErrorString"));
   });
   if (!a.lib || !a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.Reduce || !a.Broadcast || !a.GroupStart ||
-      !a.GroupEnd)
+      !a.GroupEnd || !a.ReduceScatter || !a.AllGather)
     throw Error(OGCP_E_INTERNAL, "NCCL (libnccl.so.2) is not available for the multi-GPU path");
   return a;
 }
@@ -102,19 +107,33 @@ void comm_row_range(int64_t rows, int rank, int world, int64_t* lo, int64_t* hi)
   *hi = rows * (rank + 1) / world;
 }
 
-// Owner-computes row blocks: one ncclGroup of (buffers x ranks) in-place reduces /
-// broadcasts, rank r the root of rows [lo_r, hi_r) of every buffer.  Together they
-// move the bytes of one allreduce (a reduce-scatter plus an all-gather) but leave
-// the row update between them to the owner alone.
+// Owner-computes row blocks.  Rank r owns rows [lo_r, hi_r) of every buffer
+// (comm_row_range).  A buffer whose row count divides by the world size has equal
+// blocks, so its reduction onto the owners is one in-place ncclReduceScatter and
+// the return trip one in-place ncclAllGather -- the collectives NCCL runs
+// ring/NVLS-optimal on NVSwitch (every c4 mode: 1e6 and 1e3 rows at N = 2/4/8).
+// Other buffers fall back to one in-place ncclReduce / ncclBroadcast per owner.
+// Both forms move the bytes of one allreduce but leave the row update between
+// them to the owner alone; all calls of a step go out as one NCCL group.
 static void rows_group(Ctx* ctx, float* const* bufs, const int64_t* rows, int nbuf, int ldr, bool reduce) {
   if (ctx->world <= 1 || !ctx->comm) return;
   NcclApi& a = api();
   ncclComm_t comm = (ncclComm_t)ctx->comm;
+  const int W = ctx->world;
   nccl_check(a.GroupStart(), "ncclGroupStart");
   for (int k = 0; k < nbuf; ++k) {
-    for (int r = 0; r < ctx->world; ++r) {
+    if (rows[k] % W == 0) {
+      const size_t blk = (size_t)(rows[k] / W) * ldr;
+      float* own = bufs[k] + blk * ctx->rank;
+      if (reduce)
+        nccl_check(a.ReduceScatter(bufs[k], own, blk, ncclFloat32, ncclSum, comm, ctx->stream), "ncclReduceScatter");
+      else
+        nccl_check(a.AllGather(own, bufs[k], blk, ncclFloat32, comm, ctx->stream), "ncclAllGather");
+      continue;
+    }
+    for (int r = 0; r < W; ++r) {
       int64_t lo, hi;
-      comm_row_range(rows[k], r, ctx->world, &lo, &hi);
+      comm_row_range(rows[k], r, W, &lo, &hi);
       if (hi <= lo) continue;
       float* p = bufs[k] + (size_t)lo * ldr;
       const size_t n = (size_t)(hi - lo) * ldr;
@@ -170,7 +189,8 @@ void comm_unique_id(uint8_t* out) {
 }
 
 // One-rank communicator round trip through every collective the solves use
-// (fp32 / fp64 sum, int64 min / max, grouped fp32 row reduce / broadcast): checks the dlopen'd NCCL entry points and
+// (fp32 / fp64 sum, int64 min / max, grouped fp32 row reduce / broadcast / reduce-scatter /
+// all-gather): checks the dlopen'd NCCL entry points and
 // their signatures on a single GPU.  Returns the number of mismatches.
 int comm_selftest(Ctx* ctx) {
   OGCP_CUDA(cudaSetDevice(ctx->device));
@@ -194,6 +214,8 @@ int comm_selftest(Ctx* ctx) {
   nccl_check(api().GroupStart(), "ncclGroupStart");
   nccl_check(api().Reduce(d, d, 2, ncclFloat32, ncclSum, 0, comm, st), "ncclReduce");
   nccl_check(api().Broadcast(d + 8, d + 8, 2, ncclFloat32, 0, comm, st), "ncclBroadcast");
+  nccl_check(api().ReduceScatter(d, d, 2, ncclFloat32, ncclSum, comm, st), "ncclReduceScatter");
+  nccl_check(api().AllGather(d + 8, d + 8, 2, ncclFloat32, comm, st), "ncclAllGather");
   nccl_check(api().GroupEnd(), "ncclGroupEnd");
   OGCP_CUDA(cudaStreamSynchronize(st));
   float rf[4];

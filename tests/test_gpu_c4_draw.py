@@ -66,25 +66,27 @@ def test_c4_draw_bit_exact(c4):
     assert np.array_equal(s.zero_subs0, zeros)
 
 
-@pytest.mark.parametrize("buckets", [0, 4])
-def test_c4_merged_counts_equal_bincount(c4, buckets):
+@pytest.mark.parametrize("buckets,sort_zeros", [(0, False), (4, False), (4, True)])
+def test_c4_merged_counts_equal_bincount(c4, buckets, sort_zeros):
     X, lin = c4
     ords, zeros = numpy_draw(lin, NNZ, Q, 7, KEY)
     counts = np.bincount(ords, minlength=NNZ)
     del ords
     _lib.set_buckets(buckets)  # 0: plain ordinal order; 4: the bench's row-bucketed walk
+    _lib.set_sort_zeros(sort_zeros)
     try:
         o, c, z = _lib.debug_solve_draw(X, 7, KEY, None, Q, ldr=32)
     finally:
         _lib.set_buckets(1)
+        _lib.set_sort_zeros(False)
     order = np.argsort(o, kind="stable")
     o, c = o[order], c[order]
     nzr = np.flatnonzero(counts)
     assert np.array_equal(o, nzr), "merged ordinals differ from the distinct drawn ordinals"
     assert np.array_equal(c, counts[nzr]), "multiplicities differ from np.bincount"
     assert int(c.sum()) == NNZ
-    if buckets:
-        # bucketed solves walk the zero rows sorted (stably) by (row bucket of mode 1, mode-0 row):
+    if sort_zeros:
+        # OGCP_OPT_SORT_ZEROS: bucketed solves walk the zero rows sorted (stably) by (row bucket of mode 1, mode-0 row):
         # the same rows as the reference's draw, in the walk order (sampler.cu k_zero_sort_keys)
         key = (zeros[:, 1] * buckets // DIMS[1]) * DIMS[0] + zeros[:, 0]
         zeros = zeros[np.argsort(key, kind="stable")]
