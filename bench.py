@@ -344,8 +344,10 @@ def main():
         _lib.set_buckets(int(os.environ["OGCP_BUCKETS"]))
     if os.environ.get("OGCP_SORT_ZEROS"):  # A/B knob for the sorted zero rows
         _lib.set_sort_zeros(os.environ["OGCP_SORT_ZEROS"] == "1")
-    if os.environ.get("OGCP_LEAN") == "0":  # A/B knob for the lean 3-way walk kernels
-        _lib.set_lean_walks(False)
+    if os.environ.get("OGCP_LEAN"):  # A/B knob for the register-pipelined 3-way walk kernels
+        _lib.set_lean_walks(os.environ["OGCP_LEAN"] == "1")
+    if os.environ.get("OGCP_TMA"):  # A/B knob for the TMA-fed 3-way walk kernels
+        _lib.set_tma_walks(os.environ["OGCP_TMA"] == "1")
     if os.environ.get("OGCP_MERGE") == "0":  # A/B knob for the merged draws
         _lib.set_merge_draws(False)
     loss = P.make_loss("poisson")

@@ -160,8 +160,11 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * the zero part of the walk meets the same L2-resident bucket rows and streams
  * mode 0 in order like the nonzero part; 0 keeps the draw order (lazy layout). */
 enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 3, OGCP_OPT_SHARD_SIM = 4,
-       OGCP_OPT_SORT_ZEROS = 5, OGCP_OPT_LEAN_WALKS = 6 };
-/* OGCP_OPT_LEAN_WALKS (default 1): merged sample sets of 3-way slices
+       OGCP_OPT_SORT_ZEROS = 5, OGCP_OPT_LEAN_WALKS = 6, OGCP_OPT_TMA_WALKS = 7 };
+/* OGCP_OPT_TMA_WALKS (default 1): merged sample sets of 3-way slices (ldr 16 / 32)
+ * are evaluated by warp-specialised kernels whose factor-row gathers are TMA
+ * tile::gather4 loads into a 16-stage shared-memory ring (csrc/walk_tma.cuh).
+ * OGCP_OPT_LEAN_WALKS (default 0; used when TMA walks are off): merged sample sets of 3-way slices
  * are evaluated by the specialised walk kernels (csrc/walk3.cuh, ldr 16 / 32); 0 uses the
  * generic sample kernels. */
 int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value);

@@ -274,6 +274,17 @@ def set_lean_walks(on: bool):
     check(lib().ogcp_ctx_set_option(ctx(), 6, int(bool(on))))
 
 
+def set_tma_walks(on: bool):
+    """Engine option OGCP_OPT_TMA_WALKS: TMA-fed warp-specialised walks for merged 3-way sets."""
+    check(lib().ogcp_ctx_set_option(ctx(), 7, int(bool(on))))
+
+
+def set_walk_impl(impl: str):
+    """Select the sample-walk kernels for merged 3-way sets: "tma" (default), "lean" or "generic"."""
+    set_tma_walks(impl == "tma")
+    set_lean_walks(impl == "lean")
+
+
 def set_split_scatter(on: bool):
     """Engine option OGCP_OPT_SPLIT_SCATTER for the current device's context."""
     check(lib().ogcp_ctx_set_option(ctx(), 2, int(bool(on))))

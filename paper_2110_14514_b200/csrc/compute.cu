@@ -15,6 +15,9 @@
 // weight_gradient_mttkrp kernels.py:59-72; estimate_objective
 // sampling.py:177-206; gram kernels.py:75-98; _add_reg_and_history
 // solvers.py:159-179; Adam.step adam.py:51-81; _ensure_finite solvers.py:188-194.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <unordered_map>
 
@@ -1399,6 +1402,7 @@ using IC = std::integral_constant<int, N>;
 // (half the per-sample scalar work per warp instruction).  U = 2 keeps the
 // pipelined gathers below ~130 registers.
 #include "walk3.cuh"
+#include "walk_tma.cuh"
 
 enum class Layout { Scatter, Reduce };
 
@@ -1478,7 +1482,7 @@ static int sample_grid(K kern, size_t smem, int64_t total, int G, int U) {
 // The lean 3-way walks (walk3.cuh) serve merged sets of 3-way slices at ldr 16 / 32
 // (at ldr 64 the double-buffered rows exceed the register budget).
 static bool lean_walk(const Ctx* ctx, const SamplesP& S, const ModelP& M) {
-  return ctx->lean_walks && M.ndim == 3 && S.cnt != nullptr && S.rec_ints == 4 && !S.semi &&
+  return (ctx->lean_walks || ctx->tma_walks) && M.ndim == 3 && S.cnt != nullptr && S.rec_ints == 4 && !S.semi &&
          (M.ldr == 16 || M.ldr == 32) && (S.shard_world <= 1 || S.zshard);
 }
 
@@ -1536,6 +1540,69 @@ static int wgrad3_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const fl
   return std::max(nb, 1);
 }
 
+// ---- TMA-fed walks (walk_tma.cuh): tensor maps of the three factor matrices
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    OGCP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw Error(OGCP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// [rows x ldr] fp32 rows, box {ldr, 1}: the unit of a tile::gather4 row gather.
+static CUtensorMap row_map(const float* A, int64_t rows, int ldr) {
+  CUtensorMap tm;
+  cuuint64_t gdim[2] = {(cuuint64_t)ldr, (cuuint64_t)std::max<int64_t>(rows, 1)};
+  cuuint64_t gstride[1] = {(cuuint64_t)ldr * 4};
+  cuuint32_t box[2] = {(cuuint32_t)ldr, 1};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), gdim, gstride, box,
+                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(OGCP_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return tm;
+}
+
+template <int V, int MODE, bool ZERO>
+static int tma_launch(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L, float scale,
+                      const GradPtrs& GP, double* partials, long long code) {
+  auto kern = walkt::k_walk_tma<V, MODE, ZERO>;
+  const int smem = walkt::StageLayout<V>::kSmem;
+  static thread_local bool attr = false;
+  if (!attr) {
+    OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  walkt::Maps maps;
+  for (int k = 0; k < 3; ++k) maps.a[k] = row_map(M.A[k], M.dims[k], M.ldr);
+  kern<<<kNumSMs, walkt::kThreadsT, smem, ctx->stream>>>(maps, walk_of<ZERO>(S), M, s_f, L, scale, GP, partials,
+                                                          ctx->flags.as<DevFlags>(), code);
+  ctx->count();
+  return kNumSMs;
+}
+
+template <int V>
+static void sgrad_tma_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                              const GradPtrs& GP, long long code) {
+  if (S.p > 0) tma_launch<V, 0, false>(ctx, S, M, s_f, L, (float)S.nz_scale, GP, nullptr, code);
+  if (S.q > 0) tma_launch<V, 0, true>(ctx, S, M, s_f, L, (float)S.zero_scale, GP, nullptr, code);
+}
+
+template <int V>
+static int wgrad_tma_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                             double* partials, long long code) {
+  GradPtrs none{};
+  int nb = 0;
+  if (S.p > 0) nb += tma_launch<V, 1, false>(ctx, S, M, s_f, L, (float)S.nz_scale, none, partials, code);
+  if (S.q > 0)
+    nb += tma_launch<V, 1, true>(ctx, S, M, s_f, L, (float)S.zero_scale, none, partials + (int64_t)nb * M.ldr, code);
+  return std::max(nb, 1);
+}
+
 void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
                    float* const* grads, long long code) {
   GradPtrs GP;
@@ -1589,8 +1656,14 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
   }
   if (PV.nmodes == 0 && split < 0 && lean_walk(ctx, S, M)) {
     ProfScope prof_scope(ctx, kProfSgrad);
-    if (M.ldr == 16) sgrad3_enqueue<1>(ctx, S, M, s_f, L, GP, code);
-    else sgrad3_enqueue<2>(ctx, S, M, s_f, L, GP, code);
+    if (ctx->tma_walks) {
+      if (M.ldr == 16) sgrad_tma_enqueue<1>(ctx, S, M, s_f, L, GP, code);
+      else sgrad_tma_enqueue<2>(ctx, S, M, s_f, L, GP, code);
+    } else if (M.ldr == 16) {
+      sgrad3_enqueue<1>(ctx, S, M, s_f, L, GP, code);
+    } else {
+      sgrad3_enqueue<2>(ctx, S, M, s_f, L, GP, code);
+    }
     check_launch();
     return;
   }
@@ -1624,7 +1697,9 @@ int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f
   int grid = 1;
   ProfScope prof_scope(ctx, kProfWgrad);
   if (lean_walk(ctx, S, M) && total > 0) {
-    if (M.ldr == 16) grid = wgrad3_enqueue<1>(ctx, S, M, s_f, L, partials, code);
+    if (ctx->tma_walks) grid = M.ldr == 16 ? wgrad_tma_enqueue<1>(ctx, S, M, s_f, L, partials, code)
+                                           : wgrad_tma_enqueue<2>(ctx, S, M, s_f, L, partials, code);
+    else if (M.ldr == 16) grid = wgrad3_enqueue<1>(ctx, S, M, s_f, L, partials, code);
     else grid = wgrad3_enqueue<2>(ctx, S, M, s_f, L, partials, code);
     check_launch();
     return grid;

@@ -1,0 +1,312 @@
+// TMA-fed sample walks (sm_100a): the merged nonzero set and the zero stratum of
+// a 3-way slice, evaluated by warp-specialised CTAs whose factor-row gathers are
+// issued by the Tensor Memory Accelerator.  Included by compute.cu after
+// walk3.cuh (shares its Walk descriptor and loss helpers).
+//
+// Why: the register-pipelined walks keep one or two 8-sample batches of rows in
+// flight per warp; with 16 warps per SM that is ~128 samples of gathers per SM,
+// and ncu shows them long-scoreboard bound at ~55% of L2 throughput.  Here the
+// rows of 16 stages x 32 samples (512 samples, ~200 KB) are in flight per SM
+// without costing registers:
+//
+// * 8 producer warps fetch each tile's metadata (position -> record, or the
+//   zero row) with a two-deep register pipeline, write it to the stage and
+//   issue the row gathers as cp.async.bulk.tensor.2d ... tile::gather4 (four
+//   128-byte factor rows per instruction, UTMALDG.2D.GATHER4), completing on
+//   the stage's mbarrier with an expect_tx byte count.
+// * 8 consumer warps wait on the stage, read rows and metadata from shared
+//   memory (no global latency on their critical path), evaluate y and either
+//   scatter the sampled-MTTKRP contributions (K3: mode 0 summed per row segment
+//   in registers, modes 1/2 by 16-byte vector reductions into L2) or
+//   accumulate the weight gradient (K2w, fixed-order fp64 reduction), then
+//   release the stage to its producer through a second mbarrier.
+// * Tiles are dealt to CTAs round-robin (tile t of CTA b is b + t * gridDim),
+//   so all SMs stay inside the same window of the bucketed walk and the
+//   bucket's mode-1 rows stay L2-resident.
+//
+// The tile -> producer -> stage -> consumer assignment is static, so the weight
+// gradient's summation order is fixed (deterministic); the K3 reductions into
+// modes 1 and 2 are float atomics (order-dependent in the last bits).
+
+namespace walkt {
+
+constexpr int kT = 32;          // samples per stage (tile)
+constexpr int kStages = 16;     // smem ring depth
+constexpr int kProducers = 8;   // producer warps
+constexpr int kConsumers = 8;   // consumer warps
+constexpr int kThreadsT = 32 * (kProducers + kConsumers);
+
+template <int V>
+struct StageLayout {
+  static constexpr int kLdr = 16 * V;
+  static constexpr int kRowBytes = kLdr * 4;
+  static constexpr int kRowsBytes = 3 * kT * kRowBytes;             // rows[mode][sample][ldr]
+  static constexpr int kMetaBytes = 5 * kT * 4;                     // i0, i1, i2, x, mult
+  static constexpr int kBytes = (kRowsBytes + kMetaBytes + 127) / 128 * 128;
+  static constexpr int kSmem = kStages * kBytes + 2 * kStages * 8 + 128;  // + barriers + alignment slack
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const uint32_t a = smem_u32(bar);
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// Four rows (r0..r3) of a [rows x ldr] fp32 tensor map -> 4 consecutive rows at dst.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct Maps {
+  CUtensorMap a[3];
+};
+
+// MODE 0: K2+K3 scatter into GP; MODE 1: K2w weight-gradient partials.
+template <int V, int MODE, bool ZERO>
+__global__ void __launch_bounds__(kThreadsT, 1)
+    k_walk_tma(const __grid_constant__ Maps maps, walk3::Walk<ZERO> W, ModelP M, const float* __restrict__ s_f,
+               LossP L, float scale, GradPtrs GP, double* __restrict__ partials, DevFlags* flags, long long code) {
+  using SL = StageLayout<V>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * SL::kBytes);
+  uint64_t* empty = full + kStages;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  W.resolve();
+  const int64_t ntiles = (W.n + kT - 1) / kT;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t my_tiles = ntiles > b ? (ntiles - b + G - 1) / G : 0;  // tile i of this CTA: b + i * G
+
+  if (warp < kProducers) {
+    // ------------------------------------------------------------ producers
+    const int p = warp;
+    auto tile_of = [&](int64_t k) -> int64_t { return p + k * kProducers; };  // k-th tile (CTA-local index)
+    const int64_t nk = my_tiles > p ? (my_tiles - p + kProducers - 1) / kProducers : 0;
+    // stage A: the entry's position (+ multiplicity); stage B: its record
+    auto head = [&](int64_t k, int& pos, float& mult) {
+      pos = -1;
+      mult = 0.0f;
+      if (k >= nk) return;
+      const int64_t e = (b + tile_of(k) * G) * kT + lane;
+      if (e >= W.n) return;
+      if (ZERO) {
+        pos = 0;
+        mult = 1.0f;
+      } else {
+        pos = __ldg(W.pos + e);
+        mult = (float)__ldg(W.cnt + e);
+      }
+    };
+    auto record = [&](int64_t k, int pos) -> int4 {
+      if (pos < 0) return make_int4(-1, 0, 0, 0);
+      if (ZERO) {
+        const int64_t e = (b + tile_of(k) * G) * kT + lane;
+        const int32_t* z = W.zsub + (W.zlo + e) * 3;
+        return make_int4(__ldg(z), __ldg(z + 1), __ldg(z + 2), 0);
+      }
+      return walk3::ld_stream_i4(W.rec + (int64_t)pos * 4);
+    };
+    int pos_a, pos_b;
+    float mult_a, mult_b;
+    head(0, pos_a, mult_a);
+    head(1, pos_b, mult_b);
+    int4 rec_a = record(0, pos_a);
+    for (int64_t k = 0; k < nk; ++k) {
+      int pos_c;
+      float mult_c;
+      head(k + 2, pos_c, mult_c);
+      const int4 rec_b = record(k + 1, pos_b);
+      // ---- fill the stage of tile k
+      const int64_t i = tile_of(k);
+      const int s = (int)(i % kStages);
+      const int64_t u = i / kStages;
+      if (u > 0) mbar_wait(empty + s, (unsigned)((u - 1) & 1));
+      unsigned char* st = smem + s * SL::kBytes;
+      int* meta = reinterpret_cast<int*>(st + SL::kRowsBytes);
+      const bool valid = rec_a.x >= 0;
+      meta[lane] = rec_a.x;
+      meta[kT + lane] = rec_a.y;
+      meta[2 * kT + lane] = rec_a.z;
+      meta[3 * kT + lane] = rec_a.w;
+      reinterpret_cast<float*>(meta)[4 * kT + lane] = mult_a;
+      const int r0 = valid ? rec_a.x : 0, r1 = valid ? rec_a.y : 0, r2 = valid ? rec_a.z : 0;
+      // lane l < 24 gathers mode l >> 3 of samples 4q .. 4q+3 (q = l & 7)
+      const int q = lane & 7, m = lane >> 3;
+      int g[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int src = 4 * q + j;
+        const int v0 = __shfl_sync(kFull, r0, src), v1 = __shfl_sync(kFull, r1, src), v2 = __shfl_sync(kFull, r2, src);
+        g[j] = m == 0 ? v0 : (m == 1 ? v1 : v2);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_tx(full + s, (unsigned)SL::kRowsBytes);
+      __syncwarp();
+      if (lane < 24)
+        tma_gather4(st + (m * kT + 4 * q) * SL::kRowBytes, &maps.a[m], g[0], g[1], g[2], g[3], full + s);
+      rec_a = rec_b;
+      mult_a = mult_b;
+      pos_b = pos_c;
+      mult_b = mult_c;
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int c = warp - kProducers;
+  const int gl = lane & 3, grp = lane >> 2;
+  const int ldr = SL::kLdr;
+  float4 s4[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) s4[v] = __ldg(reinterpret_cast<const float4*>(s_f) + v * 4 + gl);
+  unsigned bits = 0;
+  double acc[V][4];
+  float4 part[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    acc[v][0] = acc[v][1] = acc[v][2] = acc[v][3] = 0.0;
+    part[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int64_t i = c; i < my_tiles; i += kConsumers) {
+    const int s = (int)(i % kStages);
+    mbar_wait(full + s, (unsigned)((i / kStages) & 1));
+    const unsigned char* st = smem + s * SL::kBytes;
+    const int* meta = reinterpret_cast<const int*>(st + SL::kRowsBytes);
+    const float4* rows = reinterpret_cast<const float4*>(st);
+    int seg_row = -1;
+    float4 seg[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) seg[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int smp = 4 * grp + j;
+      const int i0 = meta[smp], i1 = meta[kT + smp], i2 = meta[2 * kT + smp];
+      const float x = __int_as_float(meta[3 * kT + smp]);
+      const float mult = reinterpret_cast<const float*>(meta)[4 * kT + smp];
+      const bool valid = i0 >= 0;
+      float4 a0[V], a1[V], a2[V], p01[V];
+      float mpart = 0.0f;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        a0[v] = rows[(0 * kT + smp) * (ldr / 4) + v * 4 + gl];
+        a1[v] = rows[(1 * kT + smp) * (ldr / 4) + v * 4 + gl];
+        a2[v] = rows[(2 * kT + smp) * (ldr / 4) + v * 4 + gl];
+        p01[v] = mul4(a0[v], a1[v]);
+        mpart += dot4(mul4(p01[v], a2[v]), s4[v]);
+      }
+      mpart += __shfl_xor_sync(kFull, mpart, 1);
+      mpart += __shfl_xor_sync(kFull, mpart, 2);
+      if (!valid) continue;
+      bits |= domain_bits(L.kind, mpart);
+      const float y = dloss(L.kind, x, mpart, L.eps) * (ZERO ? scale : scale * mult);
+      if (MODE == 0) {
+        if (i0 != seg_row) {
+          if (seg_row >= 0) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) red_add_v4(GP.g[0] + (int64_t)seg_row * ldr + (v * 4 + gl) * 4, seg[v]);
+          }
+          seg_row = i0;
+#pragma unroll
+          for (int v = 0; v < V; ++v) seg[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float* g1 = GP.g[1] + (int64_t)i1 * ldr;
+        float* g2 = GP.g[2] + (int64_t)i2 * ldr;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const float4 ys = make_float4(y * s4[v].x, y * s4[v].y, y * s4[v].z, y * s4[v].w);
+          const float4 t = mul4(ys, a2[v]);
+          const float4 c0 = mul4(t, a1[v]);
+          seg[v].x += c0.x;
+          seg[v].y += c0.y;
+          seg[v].z += c0.z;
+          seg[v].w += c0.w;
+          red_add_v4(g1 + (v * 4 + gl) * 4, mul4(t, a0[v]));
+          red_add_v4(g2 + (v * 4 + gl) * 4, mul4(ys, p01[v]));
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const float4 pr = mul4(p01[v], a2[v]);
+          part[v].x += y * pr.x;
+          part[v].y += y * pr.y;
+          part[v].z += y * pr.z;
+          part[v].w += y * pr.w;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);  // the stage's rows and metadata are consumed
+    if (MODE == 0) {
+      if (seg_row >= 0) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) red_add_v4(GP.g[0] + (int64_t)seg_row * ldr + (v * 4 + gl) * 4, seg[v]);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        acc[v][0] += (double)part[v].x;
+        acc[v][1] += (double)part[v].y;
+        acc[v][2] += (double)part[v].z;
+        acc[v][3] += (double)part[v].w;
+        part[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  if (bits) report(flags, kFlagData, code, bits);
+  if (MODE == 1) {
+    // lanes with the same columns, then the consumer warps in fixed order
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[v][e] += __shfl_xor_sync(kFull, acc[v][e], o);
+    // reuse stage 0's row area (all stages are consumed once every consumer is past its loop)
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumers) : "memory");
+    double* red = reinterpret_cast<double*>(smem);
+    if (lane < 4) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) red[c * 16 * V + (v * 4 + lane) * 4 + e] = acc[v][e];
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumers) : "memory");
+    for (int col = threadIdx.x - 32 * kProducers; col < 16 * V; col += 32 * kConsumers) {
+      double t = 0.0;
+      for (int j = 0; j < kConsumers; ++j) t += red[j * 16 * V + col];
+      partials[blockIdx.x * (int64_t)(16 * V) + col] = t;
+    }
+  }
+}
+
+}  // namespace walkt

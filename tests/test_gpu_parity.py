@@ -203,13 +203,15 @@ def test_stream_fit_vs_reference(golden_dir, name):
     assert st.window.step_ids() == c("window_ids").tolist()
 
 
-@pytest.mark.parametrize("merge,buckets,R,lean", [(True, 1, 6, True), (False, 1, 6, True), (True, 4, 6, True),
-                                                  (True, 32, 6, True), (True, 4, 12, True), (True, 1, 20, True),
-                                                  (True, 4, 20, True), (True, 32, 20, True), (True, 4, 20, False)])
-def test_dense_draw_solve_vs_oracle(merge, buckets, R, lean):
+@pytest.mark.parametrize("merge,buckets,R,impl", [(True, 1, 6, "tma"), (False, 1, 6, "tma"), (True, 4, 6, "tma"),
+                                                  (True, 32, 6, "tma"), (True, 4, 12, "tma"), (True, 1, 20, "tma"),
+                                                  (True, 4, 20, "tma"), (True, 32, 20, "tma"), (True, 4, 20, "lean"),
+                                                  (True, 4, 20, "generic"), (True, 1, 12, "lean")])
+def test_dense_draw_solve_vs_oracle(merge, buckets, R, impl):
     """p = all nonzeros on a 1e5-nnz slice: the merged (count) form -- walked in
-    ordinal order or in the slice's row-bucket order, by the lean 3-way walk
-    kernels (ldr 16 / 32, csrc/walk3.cuh) or the generic ones -- and the per-draw
+    ordinal order or in the slice's row-bucket order, by the TMA-fed or the
+    register-pipelined 3-way walk kernels (ldr 16 / 32, csrc/walk_tma.cuh,
+    csrc/walk3.cuh) or the generic ones -- and the per-draw
     form of the solve all match the oracle's slice step."""
     rng = np.random.default_rng(21)
     dims = (300, 200, 40)
@@ -219,7 +221,7 @@ def test_dense_draw_solve_vs_oracle(merge, buckets, R, lean):
     init = [rng.uniform(0.2, 1.0, (d, R)) for d in dims]
     _lib.set_merge_draws(merge)
     _lib.set_buckets(buckets)
-    _lib.set_lean_walks(lean)
+    _lib.set_walk_impl(impl)
     try:
         X = P.SparseTensor.from_zero_based(dims, subs0, vals)
         cfg = P.SolverConfig(max_epochs_weights=1, max_epochs_factors=1, iters_weights=4, iters_factors=4,
@@ -237,7 +239,7 @@ def test_dense_draw_solve_vs_oracle(merge, buckets, R, lean):
     finally:
         _lib.set_merge_draws(True)
         _lib.set_buckets(1)
-        _lib.set_lean_walks(True)
+        _lib.set_walk_impl("tma")
     ocfg = O.Cfg(kappa_w=1, kappa_f=1, tau_w=4, tau_f=4, rate_w=0.05, rate_f=1e-2, hist_weight=1.0,
                  warm_weights=True, p=None, q=5000, p_obj=20000, q_obj=20000, seed=3)
     ost = O.new_stream(init, "poisson", ocfg, capacity=2)

@@ -163,12 +163,13 @@ def test_row_sharded_update_partitions_rows():
     assert accepted >= 1
 
 
+@pytest.mark.parametrize("impl", ["tma", "lean"])
 @pytest.mark.parametrize("R", [12, 20])
 @pytest.mark.parametrize("buckets", [1, 4])
-def test_lean_walk_gradient_matches_generic(slice_1e5, R, buckets):
-    """One factor iteration with rate ~0 (u = (1-b1) g): the lean 3-way walk kernels
-    and the generic sample kernels give the same factor gradients (fp32 reduction
-    order only)."""
+def test_walk_kernels_gradient_match_generic(slice_1e5, impl, R, buckets):
+    """One factor iteration with rate ~0 (u = (1-b1) g): the TMA-fed / register-pipelined
+    3-way walk kernels and the generic sample kernels give the same factor gradients
+    (fp32 reduction order only)."""
     X = slice_1e5
     rng = np.random.default_rng(5)
     init = [rng.uniform(0.2, 1.0, (d, R)) for d in X.dims]
@@ -177,8 +178,8 @@ def test_lean_walk_gradient_matches_generic(slice_1e5, R, buckets):
                          samples=P.SamplerConfig(None, 7000, 5000, 5000, seed=9))
     loss = P.make_loss("poisson")
 
-    def u_of(lean):
-        _lib.set_lean_walks(lean)
+    def u_of(which):
+        _lib.set_walk_impl(which)
         _lib.set_buckets(buckets)
         try:
             model = P.DeviceModel.from_numpy(init)
@@ -188,9 +189,9 @@ def test_lean_walk_gradient_matches_generic(slice_1e5, R, buckets):
             solve_factors_device(X, model, w, None, [], cfg, loss, adam, 0, 1)
             return [t[:, :R].double().cpu().numpy() for t in adam._buf["u"]]
         finally:
-            _lib.set_lean_walks(True)
+            _lib.set_walk_impl("tma")
             _lib.set_buckets(1)
 
-    a, b = u_of(True), u_of(False)
+    a, b = u_of(impl), u_of("generic")
     for k in range(3):
         assert np.linalg.norm(a[k] - b[k]) <= 1e-6 * np.linalg.norm(b[k])
