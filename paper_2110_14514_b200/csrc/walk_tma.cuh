@@ -10,14 +10,17 @@
 // without costing registers:
 //
 // * 8 producer warps fetch each tile's metadata (position -> record, or the
-//   zero row) with a two-deep register pipeline, write it to the stage and
+//   zero row) with a register pipeline two tiles deep per stage, write it to the stage and
 //   issue the row gathers as cp.async.bulk.tensor.2d ... tile::gather4 (four
 //   128-byte factor rows per instruction, UTMALDG.2D.GATHER4), completing on
 //   the stage's mbarrier with an expect_tx byte count.
 // * 8 consumer warps wait on the stage, read rows and metadata from shared
 //   memory (no global latency on their critical path), evaluate y and either
 //   scatter the sampled-MTTKRP contributions (K3: mode 0 summed per row segment
-//   in registers, modes 1/2 by 16-byte vector reductions into L2) or
+//   in registers; the mode-1 / mode-2 contribution rows are written back into
+//   the stage and sent as TMA bulk reductions, cp.reduce.async.bulk ... add.f32
+//   = UBLKRED, one per row, so the L2 atomics no longer pass through the SM's
+//   load/store pipe, which bound the register-fed kernels) or
 //   accumulate the weight gradient (K2w, fixed-order fp64 reduction), then
 //   release the stage to its producer through a second mbarrier.
 // * Tiles are dealt to CTAs round-robin (tile t of CTA b is b + t * gridDim),
@@ -78,6 +81,18 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, in
       : "memory");
 }
 
+// Bulk reduction of `bytes` of fp32 from shared into global memory (TMA,
+// UBLKRED.G.S.ADD.F32): the add happens at L2, off the SM's load/store pipe.
+__device__ __forceinline__ void bulk_red_add(float* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 struct Maps {
   CUtensorMap a[3];
 };
@@ -136,16 +151,25 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       }
       return walk3::ld_stream_i4(W.rec + (int64_t)pos * 4);
     };
-    int pos_a, pos_b;
-    float mult_a, mult_b;
-    head(0, pos_a, mult_a);
-    head(1, pos_b, mult_b);
-    int4 rec_a = record(0, pos_a);
+    // two-tile lead for both stages: the head of tile k+4 and the record of tile
+    // k+2 are in flight while tile k's stage is filled
+    int pq0, pq1;      // heads of tiles k+2, k+3
+    float mq[4];       // multiplicities of tiles k .. k+3
+    int4 rq0, rq1;     // records of tiles k, k+1
+    {
+      int p0, p1;
+      head(0, p0, mq[0]);
+      head(1, p1, mq[1]);
+      head(2, pq0, mq[2]);
+      head(3, pq1, mq[3]);
+      rq0 = record(0, p0);
+      rq1 = record(1, p1);
+    }
     for (int64_t k = 0; k < nk; ++k) {
-      int pos_c;
-      float mult_c;
-      head(k + 2, pos_c, mult_c);
-      const int4 rec_b = record(k + 1, pos_b);
+      int pn;
+      float mn;
+      head(k + 4, pn, mn);
+      const int4 rn = record(k + 2, pq0);
       // ---- fill the stage of tile k
       const int64_t i = tile_of(k);
       const int s = (int)(i % kStages);
@@ -153,13 +177,13 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       if (u > 0) mbar_wait(empty + s, (unsigned)((u - 1) & 1));
       unsigned char* st = smem + s * SL::kBytes;
       int* meta = reinterpret_cast<int*>(st + SL::kRowsBytes);
-      const bool valid = rec_a.x >= 0;
-      meta[lane] = rec_a.x;
-      meta[kT + lane] = rec_a.y;
-      meta[2 * kT + lane] = rec_a.z;
-      meta[3 * kT + lane] = rec_a.w;
-      reinterpret_cast<float*>(meta)[4 * kT + lane] = mult_a;
-      const int r0 = valid ? rec_a.x : 0, r1 = valid ? rec_a.y : 0, r2 = valid ? rec_a.z : 0;
+      const bool valid = rq0.x >= 0;
+      meta[lane] = rq0.x;
+      meta[kT + lane] = rq0.y;
+      meta[2 * kT + lane] = rq0.z;
+      meta[3 * kT + lane] = rq0.w;
+      reinterpret_cast<float*>(meta)[4 * kT + lane] = mq[0];
+      const int r0 = valid ? rq0.x : 0, r1 = valid ? rq0.y : 0, r2 = valid ? rq0.z : 0;
       // lane l < 24 gathers mode l >> 3 of samples 4q .. 4q+3 (q = l & 7)
       const int q = lane & 7, m = lane >> 3;
       int g[4];
@@ -174,10 +198,14 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       __syncwarp();
       if (lane < 24)
         tma_gather4(st + (m * kT + 4 * q) * SL::kRowBytes, &maps.a[m], g[0], g[1], g[2], g[3], full + s);
-      rec_a = rec_b;
-      mult_a = mult_b;
-      pos_b = pos_c;
-      mult_b = mult_c;
+      rq0 = rq1;
+      rq1 = rn;
+      pq0 = pq1;
+      pq1 = pn;
+      mq[0] = mq[1];
+      mq[1] = mq[2];
+      mq[2] = mq[3];
+      mq[3] = mn;
     }
     return;
   }
@@ -239,8 +267,10 @@ __global__ void __launch_bounds__(kThreadsT, 1)
 #pragma unroll
           for (int v = 0; v < V; ++v) seg[v] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        float* g1 = GP.g[1] + (int64_t)i1 * ldr;
-        float* g2 = GP.g[2] + (int64_t)i2 * ldr;
+        // modes 1 / 2: the contributions overwrite this sample's a1 / a2 rows in the
+        // stage (only this group reads them) and leave as TMA bulk reductions below
+        float4* c1row = const_cast<float4*>(rows) + (1 * kT + smp) * (ldr / 4);
+        float4* c2row = const_cast<float4*>(rows) + (2 * kT + smp) * (ldr / 4);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const float4 ys = make_float4(y * s4[v].x, y * s4[v].y, y * s4[v].z, y * s4[v].w);
@@ -250,8 +280,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           seg[v].y += c0.y;
           seg[v].z += c0.z;
           seg[v].w += c0.w;
-          red_add_v4(g1 + (v * 4 + gl) * 4, mul4(t, a0[v]));
-          red_add_v4(g2 + (v * 4 + gl) * 4, mul4(ys, p01[v]));
+          c1row[v * 4 + gl] = mul4(t, a0[v]);
+          c2row[v * 4 + gl] = mul4(ys, p01[v]);
         }
       } else {
 #pragma unroll
@@ -263,6 +293,19 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           part[v].w += y * pr.w;
         }
       }
+    }
+    if (MODE == 0) {
+      // lane l sends sample l's mode-1 and mode-2 rows: two bulk reductions of one row each
+      fence_async_smem();
+      __syncwarp();
+      const int i0l = meta[lane];
+      if (i0l >= 0) {
+        bulk_red_add(GP.g[1] + (int64_t)meta[kT + lane] * ldr, rows + (1 * kT + lane) * (ldr / 4), SL::kRowBytes);
+        bulk_red_add(GP.g[2] + (int64_t)meta[2 * kT + lane] * ldr, rows + (2 * kT + lane) * (ldr / 4),
+                     SL::kRowBytes);
+      }
+      bulk_commit();
+      bulk_wait_read();  // the stage may be refilled once the TMA has read the rows
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);  // the stage's rows and metadata are consumed
@@ -282,6 +325,7 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       }
     }
   }
+  if (MODE == 0) bulk_wait_all();  // the reductions are complete before the kernel ends
   if (bits) report(flags, kFlagData, code, bits);
   if (MODE == 1) {
     // lanes with the same columns, then the consumer warps in fixed order
