@@ -161,9 +161,11 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * mode 0 in order like the nonzero part; 0 keeps the draw order (lazy layout). */
 enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 3, OGCP_OPT_SHARD_SIM = 4,
        OGCP_OPT_SORT_ZEROS = 5, OGCP_OPT_LEAN_WALKS = 6, OGCP_OPT_TMA_WALKS = 7 };
-/* OGCP_OPT_TMA_WALKS (default 1): merged sample sets of 3-way slices (ldr 16 / 32)
- * are evaluated by warp-specialised kernels whose factor-row gathers are TMA
- * tile::gather4 loads into a 16-stage shared-memory ring (csrc/walk_tma.cuh).
+/* OGCP_OPT_TMA_WALKS (default 1): bit 0 -- the K3 walk of merged sample sets of
+ * 3-way slices (ldr 16 / 32) runs in warp-specialised kernels whose factor-row
+ * gathers are TMA tile::gather4 loads into a 16-stage shared-memory ring
+ * (csrc/walk_tma.cuh); bit 1 -- the weight-gradient walk too (off by default:
+ * measured slower than the generic kernel at c4).
  * OGCP_OPT_LEAN_WALKS (default 0; used when TMA walks are off): merged sample sets of 3-way slices
  * are evaluated by the specialised walk kernels (csrc/walk3.cuh, ldr 16 / 32); 0 uses the
  * generic sample kernels. */

@@ -274,14 +274,16 @@ def set_lean_walks(on: bool):
     check(lib().ogcp_ctx_set_option(ctx(), 6, int(bool(on))))
 
 
-def set_tma_walks(on: bool):
-    """Engine option OGCP_OPT_TMA_WALKS: TMA-fed warp-specialised walks for merged 3-way sets."""
-    check(lib().ogcp_ctx_set_option(ctx(), 7, int(bool(on))))
+def set_tma_walks(on: bool, wgrad: bool = False):
+    """Engine option OGCP_OPT_TMA_WALKS: TMA-fed warp-specialised walks for merged 3-way sets
+    (the K3 walk; `wgrad` also the weight-gradient walk)."""
+    check(lib().ogcp_ctx_set_option(ctx(), 7, int(bool(on)) | (2 if wgrad else 0)))
 
 
 def set_walk_impl(impl: str):
-    """Select the sample-walk kernels for merged 3-way sets: "tma" (default), "lean" or "generic"."""
-    set_tma_walks(impl == "tma")
+    """Select the sample-walk kernels for merged 3-way sets: "tma" (default: TMA K3 walk,
+    generic weight walk), "tma-all" (both walks TMA-fed), "lean" or "generic"."""
+    set_tma_walks(impl in ("tma", "tma-all"), wgrad=impl == "tma-all")
     set_lean_walks(impl == "lean")
 
 

@@ -1448,7 +1448,10 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   else if (option == OGCP_OPT_SPLIT_SCATTER) ctx->split_scatter = value != 0;
   else if (option == OGCP_OPT_SORT_ZEROS) ctx->sort_zeros = value != 0;
   else if (option == OGCP_OPT_LEAN_WALKS) ctx->lean_walks = value != 0;
-  else if (option == OGCP_OPT_TMA_WALKS) ctx->tma_walks = value != 0;
+  else if (option == OGCP_OPT_TMA_WALKS) {
+    ctx->tma_walks = (value & 1) != 0;
+    ctx->tma_wgrad = (value & 2) != 0;
+  }
   else if (option == OGCP_OPT_SHARD_SIM) {
     if (ctx->comm) throw Error(OGCP_E_USAGE, "shard simulation needs a context without a communicator");
     const int r = (int)(value & 0xffff), w = (int)(value >> 16);

@@ -17,10 +17,9 @@
 // * 8 consumer warps wait on the stage, read rows and metadata from shared
 //   memory (no global latency on their critical path), evaluate y and either
 //   scatter the sampled-MTTKRP contributions (K3: mode 0 summed per row segment
-//   in registers; the mode-1 / mode-2 contribution rows are written back into
-//   the stage and sent as TMA bulk reductions, cp.reduce.async.bulk ... add.f32
-//   = UBLKRED, one per row, so the L2 atomics no longer pass through the SM's
-//   load/store pipe, which bound the register-fed kernels) or
+//   in registers, modes 1/2 by 16-byte vector reductions into L2; sending them
+//   as TMA bulk reductions from the stage instead, cp.reduce.async.bulk add.f32,
+//   measured slower: 7.4 -> 9.5 ms at c4) or
 //   accumulate the weight gradient (K2w, fixed-order fp64 reduction), then
 //   release the stage to its producer through a second mbarrier.
 // * Tiles are dealt to CTAs round-robin (tile t of CTA b is b + t * gridDim),
@@ -80,18 +79,6 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, in
       "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
       : "memory");
 }
-
-// Bulk reduction of `bytes` of fp32 from shared into global memory (TMA,
-// UBLKRED.G.S.ADD.F32): the add happens at L2, off the SM's load/store pipe.
-__device__ __forceinline__ void bulk_red_add(float* gdst, const void* ssrc, unsigned bytes) {
-  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
-               "r"(smem_u32(ssrc)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 struct Maps {
   CUtensorMap a[3];
@@ -267,10 +254,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
 #pragma unroll
           for (int v = 0; v < V; ++v) seg[v] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        // modes 1 / 2: the contributions overwrite this sample's a1 / a2 rows in the
-        // stage (only this group reads them) and leave as TMA bulk reductions below
-        float4* c1row = const_cast<float4*>(rows) + (1 * kT + smp) * (ldr / 4);
-        float4* c2row = const_cast<float4*>(rows) + (2 * kT + smp) * (ldr / 4);
+        float* g1 = GP.g[1] + (int64_t)i1 * ldr;
+        float* g2 = GP.g[2] + (int64_t)i2 * ldr;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const float4 ys = make_float4(y * s4[v].x, y * s4[v].y, y * s4[v].z, y * s4[v].w);
@@ -280,8 +265,8 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           seg[v].y += c0.y;
           seg[v].z += c0.z;
           seg[v].w += c0.w;
-          c1row[v * 4 + gl] = mul4(t, a0[v]);
-          c2row[v * 4 + gl] = mul4(ys, p01[v]);
+          red_add_v4(g1 + (v * 4 + gl) * 4, mul4(t, a0[v]));
+          red_add_v4(g2 + (v * 4 + gl) * 4, mul4(ys, p01[v]));
         }
       } else {
 #pragma unroll
@@ -293,19 +278,6 @@ __global__ void __launch_bounds__(kThreadsT, 1)
           part[v].w += y * pr.w;
         }
       }
-    }
-    if (MODE == 0) {
-      // lane l sends sample l's mode-1 and mode-2 rows: two bulk reductions of one row each
-      fence_async_smem();
-      __syncwarp();
-      const int i0l = meta[lane];
-      if (i0l >= 0) {
-        bulk_red_add(GP.g[1] + (int64_t)meta[kT + lane] * ldr, rows + (1 * kT + lane) * (ldr / 4), SL::kRowBytes);
-        bulk_red_add(GP.g[2] + (int64_t)meta[2 * kT + lane] * ldr, rows + (2 * kT + lane) * (ldr / 4),
-                     SL::kRowBytes);
-      }
-      bulk_commit();
-      bulk_wait_read();  // the stage may be refilled once the TMA has read the rows
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);  // the stage's rows and metadata are consumed
@@ -325,7 +297,6 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       }
     }
   }
-  if (MODE == 0) bulk_wait_all();  // the reductions are complete before the kernel ends
   if (bits) report(flags, kFlagData, code, bits);
   if (MODE == 1) {
     // lanes with the same columns, then the consumer warps in fixed order
