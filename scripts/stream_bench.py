@@ -1,14 +1,16 @@
-"""Slices/s of small streaming configs (BASELINE configs[0] c1 and configs[1] c2).
+"""Slices/s of the small streaming configs on their reference streams (BASELINE configs[0] c1,
+configs[1] c2), resumed from the reference's own warm-start checkpoint.
 
-    python scripts/stream_bench.py [--config c1|c2] [--slices N]
+    python scripts/stream_bench.py [--config c1|c2] [--slices N] [--warmup W] [--profile]
 
-c1: dense Gaussian 30x40x50 per slice, R = 5, preset synthetic-gaussian schedule
-    (kappa_w = 20, kappa_f = 5, tau = 100, p = p' = 10000, q = q' = 0, H = 50).
-c2: Chicago-shaped Poisson 32x77x24 per slice, ~906 nnz/slice, R = 10, chicago-binary
-    schedule with Poisson loss (kappa = 5/5, tau = 100, p = p' = all, q = 1000,
-    q' = 10000, w = 10, H = 500, warm weights).
-These are latency-bound (microseconds of work per iteration); reported beside the
-c4 throughput line, not as the headline.
+c1: gen_gaussian 30x40x50 per slice, R = 5, synthetic-gaussian preset (kappa_w = 20, kappa_f = 5,
+    tau = 100, p = p' = 10000, q = q' = 0, H = 50).
+c2: gen_poisson 32x77x24 per slice (~906 nnz), R = 10, chicago-binary schedule with Poisson loss
+    (kappa 5/5, tau = 100, p = p' = all, q = 1000, q' = 10000, w = 10, H = 500, warm weights).
+The data is regenerated bit-exactly (oracle/synthetic_ref.py, pinned by the reference's SHA-256)
+and the per-slice fits are compared with the reference's (tests/golden/stream_<cfg>.npz), so the
+timing is of the same stream the parity test checks.  Latency-bound: microseconds of work per
+iteration; reported beside the c4 throughput line, not as the headline.
 """
 
 from __future__ import annotations
@@ -21,84 +23,62 @@ import time
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-
-
-def planted(dims, rank, seed, kind):
-    rng = np.random.default_rng(seed)
-    if kind == "gaussian":
-        A = [rng.uniform(size=(d, rank)) for d in dims]
-        dense = np.einsum("ir,jr,kr,tr->ijkt", *A) + rng.normal(0.0, 0.2, size=dims)
-        dense[dense == 0] = 1e-300
-        subs0 = np.indices(dims).reshape(len(dims), -1).T
-        return subs0, dense.ravel(), A[:-1]
-    # sparse Poisson counts at ~1.6% density
-    cells = int(np.prod(dims))
-    lin = np.unique(rng.integers(0, cells, size=int(cells * 0.0162)))
-    subs0 = np.array(np.unravel_index(lin, dims)).T
-    vals = rng.poisson(1.0, size=lin.size).astype(float) + 1.0
-    A = [rng.uniform(0.05, 1.0, size=(d, rank)) for d in dims[:-1]]
-    return subs0, vals, A
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2", choices=("c1", "c2"))
-    ap.add_argument("--slices", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--slices", type=int, default=0, help="timed slices (0: the rest of the stream)")
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--profile", action="store_true", help="also report per-kernel-class device ms per slice")
     args = ap.parse_args()
     import torch
     import paper_2110_14514_b200 as P
-
-    if args.config == "c1":
-        dims, R, kind = (30, 40, 50, args.slices + args.warmup + 1), 5, "gaussian"
-        cfg = P.SolverConfig(max_epochs_weights=20, max_epochs_factors=5, rate_weights=10.0, rate_factors=1e-4,
-                             hist_weight=1.0, samples=P.SamplerConfig(10000, 0, 10000, 0, seed=7))
-        H = 50
-    else:
-        dims, R, kind = (32, 77, 24, args.slices + args.warmup + 1), 10, "poisson"
-        cfg = P.SolverConfig(max_epochs_weights=5, max_epochs_factors=5, rate_weights=0.1, rate_factors=1e-3,
-                             hist_weight=10.0, warm_start_weights=True,
-                             samples=P.SamplerConfig(None, 1000, None, 10000, seed=7))
-        H = 500
-    subs0, vals, A = planted(dims, R, 42, kind)
-    loss = P.make_loss(kind)
-    st = P.fresh_state(dims[:-1], R, loss, cfg, factors=A)
-    st.window = P.HistoryWindow(capacity=H)
-    rng = np.random.default_rng(3)
-    for h in range(1, 21):
-        s_h = rng.uniform(0.5, 1.5, R) * (vals.sum() / dims[-1] / R if kind == "poisson" else 1.0)
-        st.weights_log.append(s_h)
-        st.window.observe(h, s_h, P.rng_at(7, h, 5))
-    st.t = 20
+    from test_gpu_streams import stream_config, stream_data, ckpt_path
+    golden = os.path.join(ROOT, "tests", "golden")
+    g = np.load(os.path.join(golden, f"stream_{args.config}.npz"))
+    cfg, loss = stream_config(args.config)
+    dims, subs0, vals = stream_data(g)
+    from oracle.synthetic_ref import slice_of
+    t0s = int(g["t_first"]) - 1
+    st = P.load_checkpoint(ckpt_path(golden, args.config, t0s), loss, cfg)
+    n_all = int(g["metrics"].shape[0])
+    n = args.slices or (n_all - args.warmup)
     slices = []
-    for t in range(dims[-1]):
-        m = subs0[:, -1] == t
-        slices.append(P.SparseTensor.from_zero_based(dims[:-1], subs0[m, :-1], vals[m]))
+    for t in range(t0s + 1, t0s + args.warmup + n + 1):
+        s, v = slice_of(subs0, vals, t)
+        slices.append(P.SparseTensor.from_zero_based(dims[:-1], s, v))
     for X in slices[: args.warmup]:
         P.process_slice(st, X, loss, cfg, exact_loss=False)
     torch.cuda.synchronize()
     if args.profile:
         P._lib.lib().ogcp_ctx_profile_reset(P._lib.ctx())
         P._lib.lib().ogcp_ctx_profile_enable(P._lib.ctx(), 1)
+    l0 = P._lib.launches()
     t0 = time.perf_counter()
-    for X in slices[args.warmup: args.warmup + args.slices]:
-        P.process_slice(st, X, loss, cfg, exact_loss=False)
+    rows = [P.process_slice(st, X, loss, cfg, exact_loss=False) for X in slices[args.warmup:]]
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    iters = sum(r.epochs_weights * cfg.iters_weights + r.epochs_factors * cfg.iters_factors
-                for r in st.metrics[-args.slices:])
-    line = {"config": args.config, "slices_per_s": args.slices / dt, "ms_per_slice": 1e3 * dt / args.slices,
-            "us_per_iteration": 1e6 * dt / max(iters, 1), "launches": P._lib.launches()}
+    iters = sum(r.epochs_weights * cfg.iters_weights + r.epochs_factors * cfg.iters_factors for r in rows)
+    ref = g["metrics"]
+    ours = np.array([[r.t, r.local_loss_sampled] for r in rows])
+    sel = ref[np.isin(ref[:, 0], ours[:, 0])]
+    rel = np.abs(ours[:, 1] - sel[:, 1]) / np.abs(sel[:, 1])
+    line = {"config": args.config, "slices": n, "slices_per_s": n / dt, "ms_per_slice": 1e3 * dt / n,
+            "us_per_iteration": 1e6 * dt / max(iters, 1), "launches_per_iteration": (P._lib.launches() - l0) / max(iters, 1),
+            "max_rel_sampled_fit_vs_reference": float(rel.max()),
+            "reference_s_per_slice": float(g["ref_seconds"]) / n_all}
     if args.profile:
         import ctypes as C
         prof = {}
         for cls, name in enumerate(["draw", "sgrad", "wgrad", "objective", "gram", "update"]):
-            n, tms = C.c_int64(), C.c_double()
-            P._lib.lib().ogcp_ctx_profile_read(P._lib.ctx(), cls, C.byref(n), C.byref(tms))
-            prof[name] = round(tms.value / args.slices, 2)
-        line["device_ms_per_slice"] = prof
+            nb, tms = C.c_int64(), C.c_double()
+            P._lib.lib().ogcp_ctx_profile_read(P._lib.ctx(), cls, C.byref(nb), C.byref(tms))
+            prof[name] = round(tms.value / n, 3)
+        line["bracket_ms_per_slice"] = prof
     print(json.dumps(line))
 
 
