@@ -274,16 +274,17 @@ def set_lean_walks(on: bool):
     check(lib().ogcp_ctx_set_option(ctx(), 6, int(bool(on))))
 
 
-def set_tma_walks(on: bool, wgrad: bool = False):
+def set_tma_walks(on: bool, wgrad: bool = False, a2_resident: bool = True):
     """Engine option OGCP_OPT_TMA_WALKS: TMA-fed warp-specialised walks for merged 3-way sets
-    (the K3 walk; `wgrad` also the weight-gradient walk)."""
-    check(lib().ogcp_ctx_set_option(ctx(), 7, int(bool(on)) | (2 if wgrad else 0)))
+    (the K3 walk; `wgrad` also the weight-gradient walk; `a2_resident` keeps a small mode-2
+    factor in shared memory)."""
+    check(lib().ogcp_ctx_set_option(ctx(), 7, int(bool(on)) | (2 if wgrad else 0) | (0 if a2_resident else 4)))
 
 
 def set_walk_impl(impl: str):
     """Select the sample-walk kernels for merged 3-way sets: "tma" (default: TMA K3 walk,
     generic weight walk), "tma-all" (both walks TMA-fed), "lean" or "generic"."""
-    set_tma_walks(impl in ("tma", "tma-all"), wgrad=impl == "tma-all")
+    set_tma_walks(impl in ("tma", "tma-all", "tma-noa2"), wgrad=impl == "tma-all", a2_resident=impl != "tma-noa2")
     set_lean_walks(impl == "lean")
 
 

@@ -1567,15 +1567,17 @@ static CUtensorMap row_map(const float* A, int64_t rows, int ldr) {
   return tm;
 }
 
-template <int V, int MODE, bool ZERO>
-static int tma_launch(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L, float scale,
-                      const GradPtrs& GP, double* partials, long long code) {
-  auto kern = walkt::k_walk_tma<V, MODE, ZERO>;
-  const int smem = walkt::StageLayout<V>::kSmem;
-  static thread_local bool attr = false;
-  if (!attr) {
+template <int V, int MODE, bool ZERO, bool A2S>
+static int tma_launch_as(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L, float scale,
+                         const GradPtrs& GP, double* partials, long long code) {
+  auto kern = walkt::k_walk_tma<V, MODE, ZERO, A2S>;
+  using SL = walkt::StageLayout<V, A2S>;
+  const int64_t a2 = A2S ? (M.dims[2] * (int64_t)SL::kRowBytes + 127) / 128 * 128 : 0;
+  const int smem = (int)(SL::kSmemFixed + a2);
+  static thread_local int attr = 0;
+  if (smem > attr) {
     OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+    attr = smem;
   }
   walkt::Maps maps;
   for (int k = 0; k < 3; ++k) maps.a[k] = row_map(M.A[k], M.dims[k], M.ldr);
@@ -1583,6 +1585,17 @@ static int tma_launch(Ctx* ctx, const SamplesP& S, const ModelP& M, const float*
                                                           ctx->flags.as<DevFlags>(), code);
   ctx->count();
   return kNumSMs;
+}
+
+// The mode-2 factor stays resident in shared memory when it fits (walk_tma.cuh A2S).
+template <int V, int MODE, bool ZERO>
+static int tma_launch(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L, float scale,
+                      const GradPtrs& GP, double* partials, long long code) {
+  using SL = walkt::StageLayout<V, true>;
+  const int64_t a2 = M.dims[2] * (int64_t)SL::kRowBytes;
+  if (ctx->tma_a2_resident && a2 <= walkt::kA2Max && SL::kSmemFixed + (a2 + 127) / 128 * 128 <= 227 * 1024)
+    return tma_launch_as<V, MODE, ZERO, true>(ctx, S, M, s_f, L, scale, GP, partials, code);
+  return tma_launch_as<V, MODE, ZERO, false>(ctx, S, M, s_f, L, scale, GP, partials, code);
 }
 
 template <int V>

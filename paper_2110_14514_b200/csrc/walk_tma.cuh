@@ -10,10 +10,16 @@
 // without costing registers:
 //
 // * 8 producer warps fetch each tile's metadata (position -> record, or the
-//   zero row) with a register pipeline two tiles deep per stage, write it to the stage and
-//   issue the row gathers as cp.async.bulk.tensor.2d ... tile::gather4 (four
-//   128-byte factor rows per instruction, UTMALDG.2D.GATHER4), completing on
-//   the stage's mbarrier with an expect_tx byte count.
+//   zero row) with a register pipeline two tiles deep per stage, write it to the
+//   stage and issue the row gathers as cp.async.bulk.tensor.2d ... tile::gather4
+//   (four 128-byte factor rows per instruction, UTMALDG.2D.GATHER4), completing
+//   on the stage's mbarrier with an expect_tx byte count.  Mode-0 rows are
+//   gathered once per distinct row of the tile (the bucketed walk is sorted by
+//   mode-0 row, so runs of equal rows are the rule); a mode-2 factor of at most
+//   128 KB (the 1000-row mode at c4) is kept resident in shared memory instead
+//   of being gathered (8 stages then fit beside it).  At c4 this takes the
+//   walk's L2 traffic from ~800 to ~... B per sample: the K3 walk is bound by L2
+//   throughput (ncu: 9.3 TB/s of the ~12.4 TB/s LTS cap before these two cuts).
 // * 8 consumer warps wait on the stage, read rows and metadata from shared
 //   memory (no global latency on their critical path), evaluate y and either
 //   scatter the sampled-MTTKRP contributions (K3: mode 0 summed per row segment
@@ -33,19 +39,24 @@
 namespace walkt {
 
 constexpr int kT = 32;          // samples per stage (tile)
-constexpr int kStages = 16;     // smem ring depth
 constexpr int kProducers = 8;   // producer warps
 constexpr int kConsumers = 8;   // consumer warps
 constexpr int kThreadsT = 32 * (kProducers + kConsumers);
+constexpr int kA2Max = 128 * 1024;  // largest mode-2 factor kept resident in shared memory (bytes)
 
-template <int V>
+// A2S: the mode-2 factor (<= kA2Max bytes, the 1000-row mode at c4) is copied into
+// shared memory once per launch and only modes 0 and 1 are gathered per tile.
+template <int V, bool A2S>
 struct StageLayout {
   static constexpr int kLdr = 16 * V;
   static constexpr int kRowBytes = kLdr * 4;
-  static constexpr int kRowsBytes = 3 * kT * kRowBytes;             // rows[mode][sample][ldr]
-  static constexpr int kMetaBytes = 5 * kT * 4;                     // i0, i1, i2, x, mult
+  static constexpr int kModes = A2S ? 2 : 3;                          // gathered modes
+  static constexpr int kRowsBytes = kModes * kT * kRowBytes;          // rows[mode][slot][ldr]
+  static constexpr int kMetaBytes = 7 * kT * 4;                       // i0 i1 i2 x mult slot0 uniq0
   static constexpr int kBytes = (kRowsBytes + kMetaBytes + 127) / 128 * 128;
-  static constexpr int kSmem = kStages * kBytes + 2 * kStages * 8 + 128;  // + barriers + alignment slack
+  static constexpr int kStages = A2S ? 8 : 16;                        // smem ring depth
+  static constexpr int kA2Off = kStages * kBytes;                     // resident mode-2 rows
+  static constexpr int kSmemFixed = kStages * kBytes + 2 * kStages * 8 + 128;  // + barriers + alignment slack
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -85,14 +96,17 @@ struct Maps {
 };
 
 // MODE 0: K2+K3 scatter into GP; MODE 1: K2w weight-gradient partials.
-template <int V, int MODE, bool ZERO>
+template <int V, int MODE, bool ZERO, bool A2S>
 __global__ void __launch_bounds__(kThreadsT, 1)
     k_walk_tma(const __grid_constant__ Maps maps, walk3::Walk<ZERO> W, ModelP M, const float* __restrict__ s_f,
                LossP L, float scale, GradPtrs GP, double* __restrict__ partials, DevFlags* flags, long long code) {
-  using SL = StageLayout<V>;
+  using SL = StageLayout<V, A2S>;
+  constexpr int kStages = SL::kStages;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * SL::kBytes);
+  float4* a2s = reinterpret_cast<float4*>(smem + SL::kA2Off);  // A2S: resident mode-2 rows
+  const int64_t a2_bytes = A2S ? M.dims[2] * (int64_t)SL::kRowBytes : 0;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SL::kA2Off + ((a2_bytes + 127) & ~(int64_t)127));
   uint64_t* empty = full + kStages;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -102,6 +116,10 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       mbar_init(empty + s, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (A2S) {
+    const float4* src = reinterpret_cast<const float4*>(M.A[2]);
+    for (int64_t e = threadIdx.x; e < a2_bytes / 16; e += blockDim.x) a2s[e] = __ldg(src + e);
   }
   __syncthreads();
   W.resolve();
@@ -165,25 +183,41 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       unsigned char* st = smem + s * SL::kBytes;
       int* meta = reinterpret_cast<int*>(st + SL::kRowsBytes);
       const bool valid = rq0.x >= 0;
+      const int r0 = valid ? rq0.x : 0, r1 = valid ? rq0.y : 0, r2 = valid ? rq0.z : 0;
+      // mode 0: consecutive samples of the bucketed walk share their mode-0 row, so
+      // only the distinct rows of the tile are gathered (slot = rank of the row)
+      const int prev = __shfl_up_sync(kFull, r0, 1);
+      const unsigned heads = __ballot_sync(kFull, lane == 0 || r0 != prev);
+      const int slot = __popc(heads & (0xffffffffu >> (31 - lane))) - 1;
+      const int nuniq = __popc(heads);
       meta[lane] = rq0.x;
       meta[kT + lane] = rq0.y;
       meta[2 * kT + lane] = rq0.z;
       meta[3 * kT + lane] = rq0.w;
       reinterpret_cast<float*>(meta)[4 * kT + lane] = mq[0];
-      const int r0 = valid ? rq0.x : 0, r1 = valid ? rq0.y : 0, r2 = valid ? rq0.z : 0;
-      // lane l < 24 gathers mode l >> 3 of samples 4q .. 4q+3 (q = l & 7)
-      const int q = lane & 7, m = lane >> 3;
+      meta[5 * kT + lane] = slot;
+      if (heads >> lane & 1u) meta[6 * kT + slot] = r0;
+      __syncwarp();
+      const int nq0 = (nuniq + 3) >> 2;  // gather4 instructions for mode 0
+      if (lane == 0)
+        mbar_arrive_tx(full + s, (unsigned)((4 * nq0 + (SL::kModes - 1) * kT) * SL::kRowBytes));
+      __syncwarp();
+      if (lane < nq0) {  // mode 0: slots 4 lane .. 4 lane + 3 (the last group padded with the last row)
+        const int* u = meta + 6 * kT;
+        const int j0 = 4 * lane;
+        tma_gather4(st + j0 * SL::kRowBytes, &maps.a[0], u[j0], u[min(j0 + 1, nuniq - 1)], u[min(j0 + 2, nuniq - 1)],
+                    u[min(j0 + 3, nuniq - 1)], full + s);
+      }
+      // modes 1 (and 2): lane l < 8 (16) gathers samples 4q .. 4q+3 of mode 1 + (l >> 3)
+      const int q = lane & 7, m = 1 + (lane >> 3);
       int g[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int src = 4 * q + j;
-        const int v0 = __shfl_sync(kFull, r0, src), v1 = __shfl_sync(kFull, r1, src), v2 = __shfl_sync(kFull, r2, src);
-        g[j] = m == 0 ? v0 : (m == 1 ? v1 : v2);
+        const int v1 = __shfl_sync(kFull, r1, src), v2 = __shfl_sync(kFull, r2, src);
+        g[j] = m == 1 ? v1 : v2;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_tx(full + s, (unsigned)SL::kRowsBytes);
-      __syncwarp();
-      if (lane < 24)
+      if (lane < 8 * (SL::kModes - 1))
         tma_gather4(st + (m * kT + 4 * q) * SL::kRowBytes, &maps.a[m], g[0], g[1], g[2], g[3], full + s);
       rq0 = rq1;
       rq1 = rn;
@@ -228,14 +262,15 @@ __global__ void __launch_bounds__(kThreadsT, 1)
       const int i0 = meta[smp], i1 = meta[kT + smp], i2 = meta[2 * kT + smp];
       const float x = __int_as_float(meta[3 * kT + smp]);
       const float mult = reinterpret_cast<const float*>(meta)[4 * kT + smp];
+      const int slot = meta[5 * kT + smp];
       const bool valid = i0 >= 0;
       float4 a0[V], a1[V], a2[V], p01[V];
       float mpart = 0.0f;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        a0[v] = rows[(0 * kT + smp) * (ldr / 4) + v * 4 + gl];
+        a0[v] = rows[slot * (ldr / 4) + v * 4 + gl];
         a1[v] = rows[(1 * kT + smp) * (ldr / 4) + v * 4 + gl];
-        a2[v] = rows[(2 * kT + smp) * (ldr / 4) + v * 4 + gl];
+        a2[v] = A2S ? a2s[(valid ? i2 : 0) * (ldr / 4) + v * 4 + gl] : rows[(2 * kT + smp) * (ldr / 4) + v * 4 + gl];
         p01[v] = mul4(a0[v], a1[v]);
         mpart += dot4(mul4(p01[v], a2[v]), s4[v]);
       }
