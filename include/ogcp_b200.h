@@ -165,8 +165,9 @@ enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 
  * 3-way slices (ldr 16 / 32) runs in warp-specialised kernels whose factor-row
  * gathers are TMA tile::gather4 loads into a 16-stage shared-memory ring
  * (csrc/walk_tma.cuh); bit 1 -- the weight-gradient walk too (off by default:
- * measured slower than the generic kernel at c4); bit 2 -- do NOT keep a small
- * (<= 128 KB) mode-2 factor resident in shared memory (A/B knob).
+ * measured slower than the generic kernel at c4); bit 2 -- keep a small
+ * (<= 128 KB) mode-2 factor resident in shared memory (off by default: the
+ * ring then holds 8 stages instead of 16, measured slower at c4).
  * OGCP_OPT_LEAN_WALKS (default 0; used when TMA walks are off): merged sample sets of 3-way slices
  * are evaluated by the specialised walk kernels (csrc/walk3.cuh, ldr 16 / 32); 0 uses the
  * generic sample kernels. */

@@ -274,17 +274,18 @@ def set_lean_walks(on: bool):
     check(lib().ogcp_ctx_set_option(ctx(), 6, int(bool(on))))
 
 
-def set_tma_walks(on: bool, wgrad: bool = False, a2_resident: bool = True):
+def set_tma_walks(on: bool, wgrad: bool = False, a2_resident: bool = False):
     """Engine option OGCP_OPT_TMA_WALKS: TMA-fed warp-specialised walks for merged 3-way sets
     (the K3 walk; `wgrad` also the weight-gradient walk; `a2_resident` keeps a small mode-2
     factor in shared memory)."""
-    check(lib().ogcp_ctx_set_option(ctx(), 7, int(bool(on)) | (2 if wgrad else 0) | (0 if a2_resident else 4)))
+    check(lib().ogcp_ctx_set_option(ctx(), 7, int(bool(on)) | (2 if wgrad else 0) | (4 if a2_resident else 0)))
 
 
 def set_walk_impl(impl: str):
     """Select the sample-walk kernels for merged 3-way sets: "tma" (default: TMA K3 walk,
-    generic weight walk), "tma-all" (both walks TMA-fed), "lean" or "generic"."""
-    set_tma_walks(impl in ("tma", "tma-all", "tma-noa2"), wgrad=impl == "tma-all", a2_resident=impl != "tma-noa2")
+    generic weight walk), "tma-a2" (mode-2 factor resident in shared memory), "tma-all" (both
+    walks TMA-fed), "lean" or "generic"."""
+    set_tma_walks(impl in ("tma", "tma-all", "tma-a2"), wgrad=impl == "tma-all", a2_resident=impl == "tma-a2")
     set_lean_walks(impl == "lean")
 
 

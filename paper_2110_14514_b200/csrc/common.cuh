@@ -170,7 +170,8 @@ struct Ctx {
                                 // off: c4 measured +0.5 ms per draw for -0.3 ms of k_sgrad
   bool lean_walks = false;      // walk3.cuh kernels for merged 3-way sets (register-pipelined)
   bool tma_walks = true;        // walk_tma.cuh K3 walk for merged 3-way sets (TMA gather4, warp-specialised)
-  bool tma_a2_resident = true;  // TMA walks: a mode-2 factor <= 128 KB resident in shared memory
+  bool tma_a2_resident = false; // TMA walks: a mode-2 factor <= 128 KB resident in shared memory (8 stages
+                                // then fit: c4 measured 7.55 -> 7.79 ms, fewer rows in flight)
   bool tma_wgrad = false;       // walk_tma.cuh weight-gradient walk (measured slower than the generic one)
   bool buckets = true;          // bucketed layout for merged sets of large slices (OGCP_OPT_BUCKETS)
   int buckets_force = 0;        // > 1: always bucket, with this many buckets (tests)

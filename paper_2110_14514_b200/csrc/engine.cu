@@ -1451,7 +1451,7 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   else if (option == OGCP_OPT_TMA_WALKS) {
     ctx->tma_walks = (value & 1) != 0;
     ctx->tma_wgrad = (value & 2) != 0;
-    ctx->tma_a2_resident = (value & 4) == 0;
+    ctx->tma_a2_resident = (value & 4) != 0;
   }
   else if (option == OGCP_OPT_SHARD_SIM) {
     if (ctx->comm) throw Error(OGCP_E_USAGE, "shard simulation needs a context without a communicator");

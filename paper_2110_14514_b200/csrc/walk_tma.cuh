@@ -15,11 +15,11 @@
 //   (four 128-byte factor rows per instruction, UTMALDG.2D.GATHER4), completing
 //   on the stage's mbarrier with an expect_tx byte count.  Mode-0 rows are
 //   gathered once per distinct row of the tile (the bucketed walk is sorted by
-//   mode-0 row, so runs of equal rows are the rule); a mode-2 factor of at most
-//   128 KB (the 1000-row mode at c4) is kept resident in shared memory instead
-//   of being gathered (8 stages then fit beside it).  At c4 this takes the
-//   walk's L2 traffic from ~800 to ~... B per sample: the K3 walk is bound by L2
-//   throughput (ncu: 9.3 TB/s of the ~12.4 TB/s LTS cap before these two cuts).
+//   mode-0 row, so runs of equal rows are the rule).  Optionally (A2S) a mode-2
+//   factor of at most 128 KB -- the 1000-row mode at c4 -- stays resident in
+//   shared memory instead of being gathered; only 8 stages then fit beside it,
+//   which measured slower (c4 K3 walk 7.55 -> 7.79 ms although its L2 bytes drop
+//   from 69 to 58 GB), so it is off by default.
 // * 8 consumer warps wait on the stage, read rows and metadata from shared
 //   memory (no global latency on their critical path), evaluate y and either
 //   scatter the sampled-MTTKRP contributions (K3: mode 0 summed per row segment

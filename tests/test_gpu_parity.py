@@ -208,7 +208,7 @@ def test_stream_fit_vs_reference(golden_dir, name):
                                                   (True, 4, 20, "tma"), (True, 32, 20, "tma"), (True, 4, 20, "lean"),
                                                   (True, 4, 20, "generic"), (True, 1, 12, "lean"),
                                                   (True, 4, 20, "tma-all"), (True, 1, 12, "tma-all"),
-                                                  (True, 4, 20, "tma-noa2")])
+                                                  (True, 4, 20, "tma-a2")])
 def test_dense_draw_solve_vs_oracle(merge, buckets, R, impl):
     """p = all nonzeros on a 1e5-nnz slice: the merged (count) form -- walked in
     ordinal order or in the slice's row-bucket order, by the TMA-fed or the

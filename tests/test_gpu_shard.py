@@ -163,7 +163,7 @@ def test_row_sharded_update_partitions_rows():
     assert accepted >= 1
 
 
-@pytest.mark.parametrize("impl", ["tma", "tma-all", "tma-noa2", "lean"])
+@pytest.mark.parametrize("impl", ["tma", "tma-all", "tma-a2", "lean"])
 @pytest.mark.parametrize("R", [12, 20])
 @pytest.mark.parametrize("buckets", [1, 4])
 def test_walk_kernels_gradient_match_generic(slice_1e5, impl, R, buckets):
