@@ -160,7 +160,12 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * the zero part of the walk meets the same L2-resident bucket rows and streams
  * mode 0 in order like the nonzero part; 0 keeps the draw order (lazy layout). */
 enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 3, OGCP_OPT_SHARD_SIM = 4,
-       OGCP_OPT_SORT_ZEROS = 5, OGCP_OPT_LEAN_WALKS = 6, OGCP_OPT_TMA_WALKS = 7 };
+       OGCP_OPT_SORT_ZEROS = 5, OGCP_OPT_LEAN_WALKS = 6, OGCP_OPT_TMA_WALKS = 7,
+       OGCP_OPT_BATCH_DRAWS = 8 };
+/* OGCP_OPT_BATCH_DRAWS (default 1): small per-draw sample sets (the c1 / c2
+ * shapes) -- all tau draws of a solver epoch are made at the epoch's start,
+ * one launch per sampler pass with one block per draw, instead of one draw
+ * per iteration on the side stream. */
 /* OGCP_OPT_TMA_WALKS (default 1): bit 0 -- the K3 walk of merged sample sets of
  * 3-way slices (ldr 16 / 32) runs in warp-specialised kernels whose factor-row
  * gathers are TMA tile::gather4 loads into a 16-stage shared-memory ring

@@ -289,6 +289,11 @@ def set_walk_impl(impl: str):
     set_lean_walks(impl == "lean")
 
 
+def set_batch_draws(on: bool):
+    """Engine option OGCP_OPT_BATCH_DRAWS: small draws of a solver epoch made at its start."""
+    check(lib().ogcp_ctx_set_option(ctx(), 8, int(bool(on))))
+
+
 def set_split_scatter(on: bool):
     """Engine option OGCP_OPT_SPLIT_SCATTER for the current device's context."""
     check(lib().ogcp_ctx_set_option(ctx(), 2, int(bool(on))))

@@ -873,22 +873,62 @@ __global__ void __launch_bounds__(kThreads, 1) k_gram_tc(const float* __restrict
 
 // Grams of every mode of a small model in one launch (blockIdx.y = mode), fp64
 // sums straight into the outputs: out1_k = B1_k' A_k, out2_k = B2_k' A_k (B2 nullable).
-__global__ void k_gram_small(SmallGrams g, int rank, int ldr, double* __restrict__ out1, double* __restrict__ out2) {
+// Rows are staged through shared memory 64 at a time (coalesced), and every
+// thread keeps two independent fp64 partial sums per entry, so the loop runs on
+// shared-memory latency instead of a dependent global load per row (c2: 41 us ->
+// a few us per launch; the Grams were the longest kernel of a c2 iteration).
+constexpr int kGramSmallRows = 64;
+__global__ void __launch_bounds__(kThreads) k_gram_small(SmallGrams g, int rank, int ldr, double* __restrict__ out1,
+                                                         double* __restrict__ out2) {
+  __shared__ float sA[kGramSmallRows * 32], sB1[kGramSmallRows * 32], sB2[kGramSmallRows * 32];
   const int k = blockIdx.y;
   const int RR = rank * rank;
   const float* A = g.A[k];
   const float* B1 = g.B1[k];
   const float* B2 = g.B2[k];
-  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
-    const int i = e / rank, j = e % rank;
-    double s1 = 0.0, s2 = 0.0;
-    for (int64_t r = 0; r < g.rows[k]; ++r) {
-      const double aj = A[r * ldr + j];
-      s1 += (double)B1[r * ldr + i] * aj;
-      if (B2) s2 += (double)B2[r * ldr + i] * aj;
+  const int64_t rows = g.rows[k];
+  // ldr <= 32 on this path (small models); entries e = threadIdx.x + kThreads * t
+  constexpr int kMaxPer = (32 * 32 + kThreads - 1) / kThreads;
+  double s1[kMaxPer][2], s2[kMaxPer][2];
+#pragma unroll
+  for (int t = 0; t < kMaxPer; ++t) s1[t][0] = s1[t][1] = s2[t][0] = s2[t][1] = 0.0;
+  for (int64_t r0 = 0; r0 < rows; r0 += kGramSmallRows) {
+    const int nr = (int)min((int64_t)kGramSmallRows, rows - r0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * ldr; e += blockDim.x) {
+      sA[e] = A[r0 * ldr + e];
+      sB1[e] = B1[r0 * ldr + e];
+      if (B2) sB2[e] = B2[r0 * ldr + e];
     }
-    out1[(int64_t)k * RR + e] = s1;
-    if (B2) out2[(int64_t)k * RR + e] = s2;
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < kMaxPer; ++t) {
+      const int e = threadIdx.x + kThreads * t;
+      if (e >= RR) continue;
+      const int i = e / rank, j = e % rank;
+      int r = 0;
+      for (; r + 1 < nr; r += 2) {
+        const double a0 = sA[r * ldr + j], a1 = sA[(r + 1) * ldr + j];
+        s1[t][0] += (double)sB1[r * ldr + i] * a0;
+        s1[t][1] += (double)sB1[(r + 1) * ldr + i] * a1;
+        if (B2) {
+          s2[t][0] += (double)sB2[r * ldr + i] * a0;
+          s2[t][1] += (double)sB2[(r + 1) * ldr + i] * a1;
+        }
+      }
+      if (r < nr) {
+        const double a0 = sA[r * ldr + j];
+        s1[t][0] += (double)sB1[r * ldr + i] * a0;
+        if (B2) s2[t][0] += (double)sB2[r * ldr + i] * a0;
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kMaxPer; ++t) {
+    const int e = threadIdx.x + kThreads * t;
+    if (e >= RR) continue;
+    out1[(int64_t)k * RR + e] = s1[t][0] + s1[t][1];
+    if (B2) out2[(int64_t)k * RR + e] = s2[t][0] + s2[t][1];
   }
 }
 

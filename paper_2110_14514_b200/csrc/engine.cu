@@ -345,7 +345,31 @@ struct DrawPipe {
     }
   }
   bool merged() const { return buf[0].merged; }
+  // Batched epochs (small draws): every draw of the epoch made at its start in one
+  // launch per pass (sampler.cu draw_batch_enqueue); issue() is then a no-op and
+  // take() hands out the epoch's draws in order.
+  DrawBatchSet batch;
+  bool batched = false;
+  int bnext = 0;
+  const Slice* bX = nullptr;
+  template <class KeyFn>
+  void begin_epoch(Ctx* ctx, const Slice* X, KeyFn key_of, int iters, int64_t budget, long long code0) {
+    batched = false;
+    const SampleBufs& b0 = buf[0];
+    if (!merged() && ctx->batch_draws && iters > 1 && ctx->world == 1 &&
+        draw_batch_eligible(ctx, X, b0.p, b0.q, budget, b0.semi)) {
+      std::vector<Pcg64> gens(iters);
+      for (int it = 0; it < iters; ++it) gens[it] = key_of(it);
+      draw_batch_enqueue(ctx, X, gens.data(), iters, b0.p, b0.q, budget, code0, 4, batch);
+      batched = true;
+      bnext = 0;
+      bX = X;
+      return;
+    }
+    issue(ctx, X, key_of(0), budget, code0, 0);
+  }
   void issue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t budget, long long code, int slot) {
+    if (batched) return;
     init();
     const cudaStream_t main = ctx->stream;
     OGCP_CUDA(cudaEventRecord(go, main));
@@ -361,6 +385,14 @@ struct DrawPipe {
     OGCP_CUDA(cudaEventRecord(done[slot], side));
   }
   SamplesP take(Ctx* ctx, int slot) {
+    if (batched) {
+      const int b = bnext++;
+      const int32_t* ord = batch.p ? batch.ord.as<int32_t>() + (int64_t)b * batch.p : nullptr;
+      const int32_t* zs = batch.q ? batch.cand.as<int32_t>() + (int64_t)b * batch.rows_max * bX->ndim : nullptr;
+      SamplesP Sb = semi_of(bX, samples_of(bX, ord, batch.p, zs, batch.q), buf[0].semi);
+      Sb.q_dev = batch.q ? batch.scal.as<long long>() + (int64_t)b * 16 + 8 : nullptr;  // lazy layout row count
+      return Sb;
+    }
     OGCP_CUDA(cudaStreamWaitEvent(ctx->stream, done[slot], 0));
     return S[slot];
   }
@@ -690,7 +722,9 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     for (int attempt = 0;; ++attempt) {
       reset_flags(ctx);
       const long long ev0 = ev;
-      if (!dense) grad.issue(ctx, X, keyed(seed, {t, 1, epoch, 0}), budget, code_of(ev0, 0), 0);
+      if (!dense)
+        grad.begin_epoch(ctx, X, [&](int it) { return keyed(seed, {t, 1, epoch, it}); }, cfg->iters_weights, budget,
+                         code_of(ev0, 0));
       for (int it = 0; it < cfg->iters_weights; ++it) {
         const long long e = ev++;
         const int64_t cnt = i + it + 1;
@@ -991,7 +1025,9 @@ static void solve_factors_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
     for (int attempt = 0;; ++attempt) {
       reset_flags(ctx);
       const long long ev0 = ev;
-      if (!dense) W.grad.issue(ctx, X, keyed(seed, {t, 3, epoch, 0}), budget, code_of(ev0, 0), 0);
+      if (!dense)
+        W.grad.begin_epoch(ctx, X, [&](int it) { return keyed(seed, {t, 3, epoch, it}); }, cfg->iters_factors,
+                           budget, code_of(ev0, 0));
       for (int it = 0; it < cfg->iters_factors; ++it) {
         const int64_t cnt = iter + it + 1;
         const double rate_i = ad->rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
@@ -1149,7 +1185,9 @@ static void solve_static_impl(Ctx* ctx, const Slice* X, const ogcp_solver_config
     for (int attempt = 0;; ++attempt) {
       reset_flags(ctx);
       const long long ev0 = ev;
-      if (!dense) W.grad.issue(ctx, X, keyed(seed, {seed_key, 7, epoch, 0}), budget, code_of(ev0, 0), 0);
+      if (!dense)
+        W.grad.begin_epoch(ctx, X, [&](int it) { return keyed(seed, {seed_key, 7, epoch, it}); }, iters, budget,
+                           code_of(ev0, 0));
       for (int it = 0; it < iters; ++it) {
         const long long e = ev++;
         const int64_t cnt = iter + it + 1;
@@ -1447,6 +1485,7 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   if (option == OGCP_OPT_MERGE_DRAWS) ctx->merge_draws = value != 0;
   else if (option == OGCP_OPT_SPLIT_SCATTER) ctx->split_scatter = value != 0;
   else if (option == OGCP_OPT_SORT_ZEROS) ctx->sort_zeros = value != 0;
+  else if (option == OGCP_OPT_BATCH_DRAWS) ctx->batch_draws = value != 0;
   else if (option == OGCP_OPT_LEAN_WALKS) ctx->lean_walks = value != 0;
   else if (option == OGCP_OPT_TMA_WALKS) {
     ctx->tma_walks = (value & 1) != 0;

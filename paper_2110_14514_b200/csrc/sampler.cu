@@ -457,6 +457,16 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_hits(ZeroSpec zs, const i
   }
 }
 
+// Batched small draws (DrawBatchSet): block b of a batch launch runs draw b --
+// its own StreamSpec, outputs, scalar block and event code offset by b strides.
+// A plain launch (gridDim 1, specs null) is a single draw.
+struct DrawBatch {
+  const StreamSpec* specs;  // nullable: the kernel's own StreamSpec
+  int64_t out_stride;       // output elements between consecutive draws
+  int64_t scal_stride;      // long longs between consecutive draws' scalar blocks
+  long long code_stride;    // event-code step between consecutive draws
+};
+
 // Small zero strata (lazy layout): hit test + flagging, the miss scan and the
 // q-th-miss search of passes A / B / locate in one block walking the rows in
 // order; it stops at the tile holding the q-th miss.
@@ -469,9 +479,20 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_fused(ZeroSpec zs, int32_
                                                              long long* __restrict__ hits_before,
                                                              long long* __restrict__ misses_out, int64_t p,
                                                              const long long* __restrict__ nz_avail, long long budget,
-                                                             long long code, DevFlags* flags) {
+                                                             long long code, DevFlags* flags, DrawBatch B) {
   __shared__ long long carry;
   __shared__ int found;
+  {
+    const int64_t bi = blockIdx.x;
+    cand += bi * B.out_stride;
+    const int64_t so = bi * B.scal_stride;
+    elems_avail += so;
+    rows_used += so;
+    hits_before += so;
+    misses_out += so;
+    if (nz_avail) nz_avail += so;
+    code += bi * B.code_stride;
+  }
   __shared__ int wsum[kScanThreads / 32];
   if (threadIdx.x == 0) {
     carry = 0;
@@ -890,8 +911,20 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_fused(StreamSpec sp, cons
                                                              int64_t target, int32_t* __restrict__ out,
                                                              long long* __restrict__ end_word,
                                                              long long* __restrict__ elems_total, DevFlags* report,
-                                                             long long code, long long* __restrict__ clear) {
+                                                             long long code, long long* __restrict__ clear,
+                                                             DrawBatch B) {
   __shared__ int32_t stage[kBlockWords];
+  {
+    const int64_t bi = blockIdx.x;
+    if (B.specs) sp = B.specs[bi];
+    out += bi * B.out_stride;
+    const int64_t so = bi * B.scal_stride;
+    if (w0p) w0p += so;
+    if (end_word) end_word += so;
+    elems_total += so;
+    if (clear) clear += so;
+    code += bi * B.code_stride;
+  }
   __shared__ long long carry_e;
   __shared__ int carry_c;
   if (threadIdx.x == 0) {
@@ -980,7 +1013,7 @@ static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int6
   if (fused) *fused = false;
   if (!hist && nblocks <= kFusedMaxTiles) {
     k_draw_fused<NCOL><<<1, kScanThreads, 0, ctx->stream>>>(sp, w0, nchunks, target, out, end_word, elems_total,
-                                                            report, code, clear);
+                                                            report, code, clear, DrawBatch{nullptr, 0, 0, 0});
     ctx->count();
     check_launch();
     if (fused) *fused = true;
@@ -1277,7 +1310,7 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
                                               X->filter_mask ? X->filter.as<unsigned int>() : nullptr,
                                               X->filter_mask, q, sc + 8, z_hits_before, z_misses,
                                               nz_stream ? p : 0, nz_avail, (long long)budget, code,
-                                              ctx->flags.as<DevFlags>());
+                                              ctx->flags.as<DevFlags>(), DrawBatch{nullptr, 0, 0, 0});
       ctx->count();
       check_launch();
       out.zsub = scr.cand.as<int32_t>();
@@ -1327,6 +1360,148 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
   ctx->count();
   check_launch();
   return out;
+}
+
+
+// ---------------------------------------------------------------------------
+// Batched small draws: every draw of a solver epoch (tau keyed generators,
+// rng_at(seed, t, phase, epoch, it) for it < tau) in one launch per pass, one
+// block per draw.  A draw depends only on the slice and its key (never on the
+// iterate), so the epoch's draws can all be made before its first iteration;
+// for the c1 / c2 shapes each draw is a chain of single-block kernels whose
+// latency (~40 us at c2) otherwise sits on every iteration's critical path.
+bool draw_batch_eligible(const Ctx* ctx, const Slice* X, int64_t p, int64_t q, int64_t budget, bool semi) {
+  if (semi || X->ndim > kMaxModes) return false;
+  if (p > 0 && X->nnz < 2) return false;
+  const double slack = ctx->slack;
+  if (p > 0) {
+    const double r = reject_rate((uint32_t)X->nnz);
+    const double w = ((double)p / (1.0 - r) + 10.0 * std::sqrt((double)p * r) / (1.0 - r) + 2048.0) * slack;
+    const int64_t nchunks = std::max<int64_t>(1, ((int64_t)w + kChunkWords - 1) / kChunkWords);
+    if ((nchunks + kScanThreads - 1) / kScanThreads > kFusedMaxTiles) return false;
+  }
+  if (q > 0) {
+    for (int k = 0; k < X->ndim; ++k)
+      if (X->dims[k] < 2) return false;  // the lazy in-place layout needs every mode to consume words
+    const double rho = X->omega_d > 0 ? (double)X->nnz / X->omega_d : 0.0;
+    if (rho >= 0.5) return false;
+    const double rows = ((double)q / (1.0 - rho) + 10.0 * std::sqrt((double)q * rho) / (1.0 - rho) + 64.0) * slack;
+    if (std::min(rows, (double)q + (double)budget + 1.0) > (double)kFusedMaxTiles * kRowsPerBlock) return false;
+    double rmax = 0.0;
+    for (int k = 0; k < X->ndim; ++k) rmax = std::max(rmax, reject_rate((uint32_t)X->dims[k]));
+    const double target = rows * X->ndim;
+    const double w = (target / (1.0 - rmax) + 10.0 * std::sqrt(target * rmax) / (1.0 - rmax) + 2048.0) * slack;
+    const int64_t nchunks = std::max<int64_t>(1, ((int64_t)w + kChunkWords - 1) / kChunkWords);
+    if ((nchunks + kScanThreads - 1) / kScanThreads > kFusedMaxTiles) return false;
+  }
+  return p > 0 || q > 0;
+}
+
+void draw_batch_enqueue(Ctx* ctx, const Slice* X, const Pcg64* gens, int n, int64_t p, int64_t q, int64_t budget,
+                        long long code0, long long code_stride, DrawBatchSet& B) {
+  init_jump_table();
+  ProfScope prof_scope(ctx, kProfDraw);
+  cudaStream_t s = ctx->stream;
+  const int d = X->ndim;
+  const double slack = ctx->slack;
+  B.n = n;
+  B.p = p;
+  B.q = q;
+  constexpr int64_t kScal = 16;
+  B.scal.ensure((size_t)n * kScal * 8);
+  OGCP_CUDA(cudaMemsetAsync(B.scal.ptr, 0, (size_t)n * kScal * 8, s));
+  long long* sc = B.scal.as<long long>();
+  std::vector<StreamSpec> hs(n);
+  for (int b = 0; b < n; ++b) {
+    hs[b].st_hi = (unsigned long long)(gens[b].state >> 64);
+    hs[b].st_lo = (unsigned long long)gens[b].state;
+    hs[b].inc_hi = (unsigned long long)(gens[b].inc >> 64);
+    hs[b].inc_lo = (unsigned long long)gens[b].inc;
+  }
+  // nonzero stratum: integers(0, eta, p) per draw
+  if (p > 0) {
+    StreamSpec sp = hs[0];
+    sp.ncol = 1;
+    sp.n[0] = (uint32_t)X->nnz;
+    sp.thr[0] = lemire_threshold((uint32_t)X->nnz);
+    for (auto& h : hs) {
+      h.ncol = sp.ncol;
+      h.n[0] = sp.n[0];
+      h.thr[0] = sp.thr[0];
+    }
+    B.specs.ensure((size_t)n * sizeof(StreamSpec));
+    OGCP_CUDA(cudaMemcpyAsync(B.specs.ptr, hs.data(), (size_t)n * sizeof(StreamSpec), cudaMemcpyHostToDevice, s));
+    const double r = reject_rate((uint32_t)X->nnz);
+    const double w = ((double)p / (1.0 - r) + 10.0 * std::sqrt((double)p * r) / (1.0 - r) + 2048.0) * slack;
+    const int64_t nchunks = std::max<int64_t>(1, ((int64_t)w + kChunkWords - 1) / kChunkWords);
+    B.ord.ensure((size_t)n * p * 4);
+    // q == 0: nothing follows, so the nonzero pass reports its own shortfall
+    k_draw_fused<1><<<n, kScanThreads, 0, s>>>(sp, nullptr, nchunks, p, B.ord.as<int32_t>(), sc + 0, sc + 1,
+                                               q == 0 ? ctx->flags.as<DevFlags>() : nullptr, code0, nullptr,
+                                               DrawBatch{B.specs.as<StreamSpec>(), p, kScal, code_stride});
+    ctx->count();
+  }
+  B.rows_max = 0;
+  if (q > 0) {
+    ZeroSpec zs;
+    zs.ndim = d;
+    StreamSpec sp;
+    int ncol = 0;
+    double rmax = 0.0;
+    for (int k = 0; k < kMaxModes; ++k) {
+      zs.colmap[k] = -1;
+      zs.st.s[k] = k < d ? X->strides[k] : 0;
+    }
+    for (int k = 0; k < d; ++k) {
+      sp.n[ncol] = (uint32_t)X->dims[k];
+      sp.thr[ncol] = lemire_threshold((uint32_t)X->dims[k]);
+      rmax = std::max(rmax, reject_rate((uint32_t)X->dims[k]));
+      zs.colmap[k] = ncol++;
+    }
+    zs.ncol = ncol;
+    sp.ncol = ncol;
+    for (auto& h : hs) {
+      h.ncol = sp.ncol;
+      for (int c = 0; c < ncol; ++c) {
+        h.n[c] = sp.n[c];
+        h.thr[c] = sp.thr[c];
+      }
+    }
+    B.zspecs.ensure((size_t)n * sizeof(StreamSpec));
+    OGCP_CUDA(cudaMemcpyAsync(B.zspecs.ptr, hs.data(), (size_t)n * sizeof(StreamSpec), cudaMemcpyHostToDevice, s));
+    const double rho = X->omega_d > 0 ? (double)X->nnz / X->omega_d : 0.0;
+    const double want = ((double)q / (1.0 - rho) + 10.0 * std::sqrt((double)q * rho) / (1.0 - rho) + 64.0) * slack;
+    int64_t rows_max = (int64_t)std::min(want, (double)q + (double)budget + 1.0);
+    if (rows_max < q) rows_max = q;
+    B.rows_max = rows_max;
+    const int64_t target = rows_max * ncol;
+    const double exp_words = (double)target / (1.0 - rmax);
+    const double sd = std::sqrt((double)target * rmax) / (1.0 - rmax);
+    const int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
+    const int64_t nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
+    B.cand.ensure((size_t)n * target * 4);
+    const DrawBatch zb{B.zspecs.as<StreamSpec>(), target, kScal, code_stride};
+    auto launch = [&](auto kern) {
+      kern<<<n, kScanThreads, 0, s>>>(sp, p > 0 ? sc + 0 : nullptr, nchunks, target, B.cand.as<int32_t>(), nullptr,
+                                      sc + 2, nullptr, code0, nullptr, zb);
+    };
+    switch (ncol) {
+      case 2: launch(k_draw_fused<2>); break;
+      case 3: launch(k_draw_fused<3>); break;
+      case 4: launch(k_draw_fused<4>); break;
+      case 5: launch(k_draw_fused<5>); break;
+      case 6: launch(k_draw_fused<6>); break;
+      case 7: launch(k_draw_fused<7>); break;
+      default: throw Error(OGCP_E_USAGE, "batched draws need 2..7 modes");
+    }
+    const unsigned long long* table = X->nnz > 0 ? X->hash.as<unsigned long long>() : nullptr;
+    k_zero_fused<<<n, kScanThreads, 0, s>>>(zs, B.cand.as<int32_t>(), sc + 2, rows_max, table, X->table_mask,
+                                            X->filter_mask ? X->filter.as<unsigned int>() : nullptr, X->filter_mask, q,
+                                            sc + 8, sc + 4, sc + 3, p, p > 0 ? sc + 1 : nullptr, (long long)budget,
+                                            code0, ctx->flags.as<DevFlags>(), zb);
+    ctx->count(2);
+  }
+  check_launch();
 }
 
 }  // namespace ogcp

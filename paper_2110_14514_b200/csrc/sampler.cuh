@@ -41,4 +41,17 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
                      int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr,
                      MergedDraw* merged = nullptr, bool lazy = false, bool semi = false);
 
+// Every draw of a solver epoch made up front (small draws only, see
+// draw_batch_eligible): draw b's nonzero ordinals at ord + b p, its zero stratum
+// in the lazy layout at cand + b rows_max ndim with the row count at
+// scal + 16 b + 8.
+struct DrawBatchSet {
+  DevBuf ord, cand, scal, specs, zspecs;
+  int n = 0;
+  int64_t p = 0, q = 0, rows_max = 0;
+};
+bool draw_batch_eligible(const Ctx* ctx, const Slice* X, int64_t p, int64_t q, int64_t budget, bool semi);
+void draw_batch_enqueue(Ctx* ctx, const Slice* X, const Pcg64* gens, int n, int64_t p, int64_t q, int64_t budget,
+                        long long code0, long long code_stride, DrawBatchSet& B);
+
 }  // namespace ogcp
