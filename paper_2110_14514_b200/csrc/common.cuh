@@ -166,6 +166,14 @@ struct Ctx {
   // c4 it measured 19.2 ms vs 10.2 ms for the fused pass (profiles/), the second
   // pass repeating the gather latency chain without saving enough traffic.
   bool split_scatter = false;
+  DevBuf wticket_buf;           // fused weight step: last-block ticket (0 between launches)
+  unsigned int* wticket() {
+    if (!wticket_buf.ptr) {
+      wticket_buf.ensure(64);
+      OGCP_CUDA(cudaMemset(wticket_buf.ptr, 0, 64));
+    }
+    return wticket_buf.as<unsigned int>();
+  }
   bool batch_draws = true;      // small draws: every draw of a solver epoch made at its start (one launch per pass)
   bool sort_zeros = false;      // bucketed merged draws: zero rows sorted by (bucket, mode-0 row);
                                 // off: c4 measured +0.5 ms per draw for -0.3 ms of k_sgrad

@@ -456,10 +456,38 @@ __global__ void __launch_bounds__(kThreads) k_sgrad_split(SamplesP S, ModelP M, 
   }
 }
 
+// Temporal-row Adam step body (adam.py:51-81 on the R-vector, fp64): thread r < ldr
+// sums column r of the nblk block partials in block order (deterministic).
+__device__ __forceinline__ void weight_step_body(const double* partials, int nblk, int rank, int ldr, double* ws,
+                                                 float* s_f, double mu, double rate_i, double b1, double b2,
+                                                 double eps, double lower, DevFlags* flags, long long code) {
+  const int r = threadIdx.x;
+  if (r >= ldr) return;
+  if (r >= rank) {
+    s_f[r] = 0.f;
+    return;
+  }
+  double g = 0.0;
+  for (int b = 0; b < nblk; ++b) g += partials[(int64_t)b * ldr + r];
+  double s = ws[r];
+  g += mu * s;
+  double u = b1 * ws[ldr + r] + (1.0 - b1) * g;
+  double v = b2 * ws[2 * ldr + r] + (1.0 - b2) * g * g;
+  double sn = s - rate_i * u / (sqrt(v) + eps);
+  if (sn < lower) sn = lower;
+  ws[r] = sn;
+  ws[ldr + r] = u;
+  ws[2 * ldr + r] = v;
+  s_f[r] = (float)sn;
+  // the sample kernels evaluate in fp32: an iterate beyond fp32 range has diverged for this engine
+  if (!isfinite(sn) || !isfinite((float)sn)) report(flags, kFlagDiverge, code, 0);
+}
+
 // ------------------------------------------------------------------ K2 (weights)
 template <int D, int G, int V, int U>
 __global__ void __launch_bounds__(kThreads, OGCP_WGRAD_MINB) k_wgrad(SamplesP S, ModelP M, const float* __restrict__ s_f, LossP L,
-                                                    double* __restrict__ partials, DevFlags* flags, long long code) {
+                                                    double* __restrict__ partials, DevFlags* flags, long long code,
+                                                    WStep step) {
   __shared__ double red[kThreads / 32][4 * V * G];
   constexpr int NDm = ND<D>::v;
   const int lane = threadIdx.x & 31;
@@ -530,6 +558,19 @@ __global__ void __launch_bounds__(kThreads, OGCP_WGRAD_MINB) k_wgrad(SamplesP S,
     double t = 0.0;
     for (int j = 0; j < kThreads / 32; ++j) t += red[j][c];
     partials[blockIdx.x * (int64_t)(4 * V * G) + c] = t;
+  }
+  if (step.ticket) {  // fused weight step: the last block to finish applies it
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(step.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      weight_step_body(partials, gridDim.x, step.rank, step.ldr, step.ws, step.s_f, step.mu, step.rate_i, step.b1,
+                       step.b2, step.eps, step.lower, flags, step.code);
+      if (threadIdx.x == 0) *step.ticket = 0u;
+    }
   }
 }
 
@@ -1368,26 +1409,7 @@ __global__ void __launch_bounds__(kThreads) k_factor_update_wide(int64_t rows, i
 __global__ void k_weight_step(const double* __restrict__ partials, int nblk, int rank, int ldr,
                               double* __restrict__ ws, float* __restrict__ s_f, double mu, double rate_i, double b1,
                               double b2, double eps, double lower, DevFlags* flags, long long code) {
-  const int r = threadIdx.x;
-  if (r >= ldr) return;
-  if (r >= rank) {
-    s_f[r] = 0.f;
-    return;
-  }
-  double g = 0.0;
-  for (int b = 0; b < nblk; ++b) g += partials[(int64_t)b * ldr + r];
-  double s = ws[r];
-  g += mu * s;
-  double u = b1 * ws[ldr + r] + (1.0 - b1) * g;
-  double v = b2 * ws[2 * ldr + r] + (1.0 - b2) * g * g;
-  double sn = s - rate_i * u / (sqrt(v) + eps);
-  if (sn < lower) sn = lower;
-  ws[r] = sn;
-  ws[ldr + r] = u;
-  ws[2 * ldr + r] = v;
-  s_f[r] = (float)sn;
-  // the sample kernels evaluate in fp32: an iterate beyond fp32 range has diverged for this engine
-  if (!isfinite(sn) || !isfinite((float)sn)) report(flags, kFlagDiverge, code, 0);
+  weight_step_body(partials, nblk, rank, ldr, ws, s_f, mu, rate_i, b1, b2, eps, lower, flags, code);
 }
 
 // ------------------------------------------------------------------ history penalty
@@ -1745,7 +1767,8 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
 }
 
 int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
-                  double* partials, long long code) {
+                  double* partials, long long code, const WStep* step, bool* stepped) {
+  if (stepped) *stepped = false;
   const int64_t total = S.p + S.q;
   int grid = 1;
   ProfScope prof_scope(ctx, kProfWgrad);
@@ -1764,7 +1787,12 @@ int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f
     constexpr int U = decltype(Uc)::value;
     auto kern = k_wgrad<D, G, V, U>;
     grid = sample_grid(kern, 0, std::max<int64_t>(total, 1), G, U);
-    kern<<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(), code);
+    WStep ws{};
+    if (step && step->ldr <= kThreads) {
+      ws = *step;
+      if (stepped) *stepped = true;
+    }
+    kern<<<grid, kThreads, 0, ctx->stream>>>(S, M, s_f, L, partials, ctx->flags.as<DevFlags>(), code, ws);
   });
   ctx->count();
   check_launch();

@@ -46,9 +46,23 @@ struct LossP {
 // (zeroed and written).  s_f: float [ldr] weights (padding zero).
 void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
                    float* const* grads, long long code);
+// Temporal-row Adam step (k_weight_step's arithmetic) fused into the tail of a
+// K2w launch: the last block to finish sums the block partials in block order
+// and updates the R-vector state.  ticket: a device counter that is 0 between
+// launches (the last block resets it).
+struct WStep {
+  int rank, ldr;
+  double* ws;
+  float* s_f;
+  double mu, rate_i, b1, b2, eps, lower;
+  long long code;
+  unsigned int* ticket;
+};
 // K2 (weight solve): per-block partial sums of Z'vec(Y) into partials [nblk x ldr] double.
+// With `step`, the walk kernel also applies the weight step when it can (*stepped
+// tells whether it did; otherwise the caller runs weight_step_enqueue).
 int wgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
-                  double* partials, long long code);
+                  double* partials, long long code, const WStep* step = nullptr, bool* stepped = nullptr);
 // K6: per-block partial sums of scale*f(x,m) into partials; returns the block count.
 int objective_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
                       double* partials, long long code);

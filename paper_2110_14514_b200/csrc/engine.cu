@@ -739,7 +739,12 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
         if (it + 1 < cfg->iters_weights)
           grad.issue(ctx, X, keyed(seed, {t, 1, epoch, it + 1}), budget, code_of(e + 1, 0), (it + 1) & 1);
         SamplesP Sg = sharded(ctx, grad.take(ctx, it & 1));
-        int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1));
+        // one GPU: the weight step runs in the tail of the K2w launch (last block)
+        WStep wstep{R, ldr, ws, s_f, cfg->reg_weights, rate_i, cfg->beta1, cfg->beta2, cfg->adam_eps,
+                    cfg->lower_bound, code_of(e, 2), ctx->wticket()};
+        bool stepped = false;
+        int nb = wgrad_enqueue(ctx, Sg, M, s_f, L, part, code_of(e, 1), ctx->world == 1 ? &wstep : nullptr, &stepped);
+        if (stepped) continue;
         const double* gparts = part;
         if (ctx->world > 1) {  // sum the shard gradients across ranks, then the replicated step
           sum_partials_enqueue(ctx, part, nb, ldr, gsum);
