@@ -165,8 +165,7 @@ enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 
 /* OGCP_OPT_BATCH_DRAWS (default 1): small per-draw sample sets (the c1 / c2
  * shapes) -- all tau draws of a solver epoch are made at the epoch's start,
  * one launch per sampler pass with one block per draw, instead of one draw
- * per iteration on the side stream.  Value bit 1 (2): do NOT fuse the small-model
- * factor step (history Grams + coefficients + K5 of every mode in one launch). */
+ * per iteration on the side stream. */
 /* OGCP_OPT_TMA_WALKS (default 1): bit 0 -- the K3 walk of merged sample sets of
  * 3-way slices (ldr 16 / 32) runs in warp-specialised kernels whose factor-row
  * gathers are TMA tile::gather4 loads into a 16-stage shared-memory ring

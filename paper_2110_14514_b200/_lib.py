@@ -289,10 +289,9 @@ def set_walk_impl(impl: str):
     set_lean_walks(impl == "lean")
 
 
-def set_batch_draws(on: bool, fused_small_step: bool = True):
-    """Engine option OGCP_OPT_BATCH_DRAWS: small draws of a solver epoch made at its start;
-    `fused_small_step`: small models' Grams + coefficients + K5 in one launch."""
-    check(lib().ogcp_ctx_set_option(ctx(), 8, int(bool(on)) | (0 if fused_small_step else 2)))
+def set_batch_draws(on: bool):
+    """Engine option OGCP_OPT_BATCH_DRAWS: small draws of a solver epoch made at its start."""
+    check(lib().ogcp_ctx_set_option(ctx(), 8, int(bool(on))))
 
 
 def set_split_scatter(on: bool):

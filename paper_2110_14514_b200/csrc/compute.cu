@@ -1240,69 +1240,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_factor_update_modes(K5Modes m, 
                          rate_i, b1, omb1, b2, omb2, eps, lower, flags, code);
 }
 
-// Small models (every mode <= kSmallRows rows, ldr <= 32, the c1 / c2 shapes): the
-// history Grams of every mode (P_m = A_m'A_m, C_m = Aold_m'A_m, fp64), their
-// Hadamard coefficients (k_hist_coeffs) and the K5 update of every mode in ONE
-// block -- three dependent launches of a few microseconds of latency each
-// become one (phases separated by __syncthreads; the Grams and coefficients pass
-// through global scratch written and read by this block only).
-template <int GR>
-__global__ void __launch_bounds__(kThreads) k_small_factor_step(K5Modes m, int ndim, int rank, int ldr,
-                                                                const double* __restrict__ S, double w,
-                                                                double* __restrict__ P, double* __restrict__ C,
-                                                                float* __restrict__ Mk, float* __restrict__ Nk,
-                                                                float reg, float rate_i, float b1, float omb1,
-                                                                float b2, float omb2, float eps, float lower,
-                                                                DevFlags* flags, long long code) {
-  const int RR = rank * rank;
-  // phase 1: Grams (two independent fp64 partial sums per entry)
-  for (int k = 0; k < ndim; ++k) {
-    const float* A = m.A[k];
-    const float* B = m.Aold[k];
-    for (int e = threadIdx.x; e < RR; e += blockDim.x) {
-      const int i = e / rank, j = e % rank;
-      double p0 = 0.0, p1 = 0.0, c0 = 0.0, c1 = 0.0;
-      int64_t r = 0;
-      for (; r + 1 < m.rows[k]; r += 2) {
-        const double a0 = A[r * ldr + j], a1 = A[(r + 1) * ldr + j];
-        p0 += (double)A[r * ldr + i] * a0;
-        p1 += (double)A[(r + 1) * ldr + i] * a1;
-        c0 += (double)B[r * ldr + i] * a0;
-        c1 += (double)B[(r + 1) * ldr + i] * a1;
-      }
-      if (r < m.rows[k]) {
-        const double a0 = A[r * ldr + j];
-        p0 += (double)A[r * ldr + i] * a0;
-        c0 += (double)B[r * ldr + i] * a0;
-      }
-      P[(int64_t)k * RR + e] = p0 + p1;
-      C[(int64_t)k * RR + e] = c0 + c1;
-    }
-  }
-  __syncthreads();
-  // phase 2: M_k = w (hadamard_{m != k} P_m) o S, N_k = w (hadamard_{m != k} C_m) o S
-  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
-    const double se = w * S[e];
-    for (int k = 0; k < ndim; ++k) {
-      double gp = 1.0, gc = 1.0;
-      for (int mm = 0; mm < ndim; ++mm) {
-        if (mm == k) continue;
-        gp *= P[(int64_t)mm * RR + e];
-        gc *= C[(int64_t)mm * RR + e];
-      }
-      Mk[(int64_t)k * RR + e] = (float)(gp * se);
-      Nk[(int64_t)k * RR + e] = (float)(gc * se);
-    }
-  }
-  __syncthreads();
-  // phase 3: K5 of every mode (factor_update_rows stages M_k / N_k itself)
-  for (int k = 0; k < ndim; ++k) {
-    factor_update_rows<GR>(m.rows[k], rank, ldr, m.A[k], m.Aold[k], m.G[k], m.u[k], m.v[k], Mk + (int64_t)k * RR,
-                           Nk + (int64_t)k * RR, reg, rate_i, b1, omb1, b2, omb2, eps, lower, flags, code);
-    __syncthreads();
-  }
-}
-
 // 32 < rank <= 128 with history / model terms: the apply H = A Mk - Aold Nk is
 // an [rows x R] x [R x R] product, so it is register-tiled: a CTA stages Mk, Nk
 // (R x R) once and a 32-row tile of A / Aold per pass in shared memory; thread
@@ -2026,30 +1963,6 @@ void factor_update_modes_enqueue(Ctx* ctx, const K5Modes& m, int ndim, int rank,
     case 8: launch(k_factor_update_modes<8>); break;
     case 16: launch(k_factor_update_modes<16>); break;
     default: launch(k_factor_update_modes<32>); break;
-  }
-  ctx->count();
-  check_launch();
-}
-
-void small_factor_step_enqueue(Ctx* ctx, const K5Modes& m, int ndim, int rank, int ldr, const double* S, double w,
-                               double* P, double* C, float* Mk, float* Nk, double reg, double rate_i, double beta1,
-                               double beta2, double eps, double lower, long long code) {
-  ProfScope prof_scope(ctx, kProfUpdate);
-  const float fb1 = (float)beta1, fomb1 = (float)(1.0 - beta1), fb2 = (float)beta2, fomb2 = (float)(1.0 - beta2);
-  int GR = 1;
-  while (GR < rank) GR <<= 1;
-  auto launch = [&](auto kern) {
-    kern<<<1, kThreads, 0, ctx->stream>>>(m, ndim, rank, ldr, S, w, P, C, Mk, Nk, (float)reg, (float)rate_i, fb1,
-                                          fomb1, fb2, fomb2, (float)eps, (float)lower, ctx->flags.as<DevFlags>(),
-                                          code);
-  };
-  switch (GR) {
-    case 1: launch(k_small_factor_step<1>); break;
-    case 2: launch(k_small_factor_step<2>); break;
-    case 4: launch(k_small_factor_step<4>); break;
-    case 8: launch(k_small_factor_step<8>); break;
-    case 16: launch(k_small_factor_step<16>); break;
-    default: launch(k_small_factor_step<32>); break;
   }
   ctx->count();
   check_launch();

@@ -102,11 +102,6 @@ struct K5Modes {
 };
 void factor_update_modes_enqueue(Ctx* ctx, const K5Modes& m, int ndim, int rank, int ldr, double reg, double rate_i,
                                  double beta1, double beta2, double eps, double lower, long long code);
-// Small models with history: Grams (P, C), coefficients (Mk, Nk) and K5 of every
-// mode in one single-block launch (m.Aold non-null, S = the window matrix).
-void small_factor_step_enqueue(Ctx* ctx, const K5Modes& m, int ndim, int rank, int ldr, const double* S, double w,
-                               double* P, double* C, float* Mk, float* Nk, double reg, double rate_i, double beta1,
-                               double beta2, double eps, double lower, long long code);
 // K5: g = G + lambda*A + (A Mk - Aold Nk) ; Adam ; clamp ; isfinite  (one mode).
 void factor_update_enqueue(Ctx* ctx, int64_t rows, int rank, int ldr, float* A, const float* Aold,
                            const float* G, float* u, float* v, const float* Mk, const float* Nk,

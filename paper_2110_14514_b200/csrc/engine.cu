@@ -927,23 +927,6 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
   if (rowshard) comm_reduce_rows(ctx, gp, M.dims, M.ndim, M.ldr);
   else comm_allreduce_sum(ctx, W.grads.as<float>(), off);
   const bool coeffs = hist || dense;
-  if (small_model(M) && hist && !dense && !rowshard && ctx->fused_small_step) {
-    // Grams + coefficients + K5 of every mode in one launch (latency-bound shapes)
-    K5Modes km{};
-    for (int k = 0; k < M.ndim; ++k) {
-      km.A[k] = A[k];
-      km.Aold[k] = old_factors[k];
-      km.G[k] = gp[k];
-      km.u[k] = ad->u[k];
-      km.v[k] = ad->v[k];
-      km.rows[k] = M.dims[k];
-    }
-    small_factor_step_enqueue(ctx, km, M.ndim, M.rank, M.ldr, W.hb.S.as<double>(), cfg->hist_weight,
-                              W.hb.P.as<double>(), W.hb.C.as<double>(), W.hb.Mk.as<float>(), W.hb.Nk.as<float>(),
-                              cfg->reg_factors, rate_i, cfg->beta1, cfg->beta2, cfg->adam_eps, cfg->lower_bound,
-                              code_of(ev, 2));
-    return;
-  }
   if (coeffs) {
     if (hist) grams_pc_enqueue(ctx, M, old_factors, W.hb, true);
     else grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true, true);
@@ -1507,10 +1490,7 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   if (option == OGCP_OPT_MERGE_DRAWS) ctx->merge_draws = value != 0;
   else if (option == OGCP_OPT_SPLIT_SCATTER) ctx->split_scatter = value != 0;
   else if (option == OGCP_OPT_SORT_ZEROS) ctx->sort_zeros = value != 0;
-  else if (option == OGCP_OPT_BATCH_DRAWS) {
-    ctx->batch_draws = (value & 1) != 0;
-    ctx->fused_small_step = (value & 2) == 0;
-  }
+  else if (option == OGCP_OPT_BATCH_DRAWS) ctx->batch_draws = value != 0;
   else if (option == OGCP_OPT_LEAN_WALKS) ctx->lean_walks = value != 0;
   else if (option == OGCP_OPT_TMA_WALKS) {
     ctx->tma_walks = (value & 1) != 0;
