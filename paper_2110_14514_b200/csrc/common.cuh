@@ -174,8 +174,7 @@ struct Ctx {
     }
     return wticket_buf.as<unsigned int>();
   }
-  bool batch_draws = true;
-  bool fused_small_step = true;  // small models: Grams + coefficients + K5 in one launch      // small draws: every draw of a solver epoch made at its start (one launch per pass)
+  bool batch_draws = true;      // small draws: every draw of a solver epoch made at its start (one launch per pass)
   bool sort_zeros = false;      // bucketed merged draws: zero rows sorted by (bucket, mode-0 row);
                                 // off: c4 measured +0.5 ms per draw for -0.3 ms of k_sgrad
   bool lean_walks = false;      // walk3.cuh kernels for merged 3-way sets (register-pipelined)
