@@ -294,6 +294,11 @@ def set_batch_draws(on: bool):
     check(lib().ogcp_ctx_set_option(ctx(), 8, int(bool(on))))
 
 
+def set_umma_gram(on: bool):
+    """Engine option OGCP_OPT_UMMA_GRAM: ldr 64 / 128 Grams on tcgen05 / TMEM."""
+    check(lib().ogcp_ctx_set_option(ctx(), 9, int(bool(on))))
+
+
 def set_split_scatter(on: bool):
     """Engine option OGCP_OPT_SPLIT_SCATTER for the current device's context."""
     check(lib().ogcp_ctx_set_option(ctx(), 2, int(bool(on))))

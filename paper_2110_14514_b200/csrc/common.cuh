@@ -174,6 +174,7 @@ struct Ctx {
     }
     return wticket_buf.as<unsigned int>();
   }
+  bool umma_gram = true;        // ldr 64 / 128 Grams on tcgen05 / TMEM (gram_umma.cuh)
   bool batch_draws = true;      // small draws: every draw of a solver epoch made at its start (one launch per pass)
   bool sort_zeros = false;      // bucketed merged draws: zero rows sorted by (bucket, mode-0 row);
                                 // off: c4 measured +0.5 ms per draw for -0.3 ms of k_sgrad

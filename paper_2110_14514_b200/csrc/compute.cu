@@ -1487,6 +1487,7 @@ using IC = std::integral_constant<int, N>;
 // pipelined gathers below ~130 registers.
 #include "walk3.cuh"
 #include "walk_tma.cuh"
+#include "gram_umma.cuh"
 
 enum class Layout { Scatter, Reduce };
 
@@ -1865,10 +1866,48 @@ void sum_partials_enqueue(Ctx* ctx, const double* partials, int nblk, int len, d
   check_launch();
 }
 
+// [rows x ldr] fp32, boxes of {32 floats, 32 rows} with the 128-byte swizzle: the
+// canonical MN-major SWIZZLE_128B operand tiles of the UMMA Gram (gram_umma.cuh).
+static CUtensorMap gram_tile_map(const float* A, int64_t rows, int ldr) {
+  CUtensorMap tm;
+  cuuint64_t gdim[2] = {(cuuint64_t)ldr, (cuuint64_t)std::max<int64_t>(rows, 1)};
+  cuuint64_t gstride[1] = {(cuuint64_t)ldr * 4};
+  cuuint32_t box[2] = {32, (cuuint32_t)umma::kRows};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), gdim, gstride, box,
+                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(OGCP_E_CUDA, "cuTensorMapEncodeTiled (Gram tiles) failed (" + std::to_string((int)r) + ")");
+  return tm;
+}
+
 void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* outP,
                    double* outC, DevBuf& scratch) {
   const int ngram = B ? 2 : 1;
-  if (ldr == 32 || ldr == 64 || ldr == 128) {  // tensor-core path
+  if ((ldr == 64 || ldr == 128) && ctx->umma_gram && rows > 0) {  // tcgen05 / TMEM path (gram_umma.cuh)
+    const int64_t nchunks = (rows + umma::kRows - 1) / umma::kRows;
+    const int nblk = (int)std::min<int64_t>(nchunks, kNumSMs);
+    scratch.ensure((size_t)nblk * ngram * ldr * ldr * 8);
+    umma::GramMaps maps;
+    maps.a = gram_tile_map(A, rows, ldr);
+    maps.b = B ? gram_tile_map(B, rows, ldr) : maps.a;
+    auto kern = ldr == 64 ? umma::k_gram_umma<64> : umma::k_gram_umma<128>;
+    static thread_local bool attr64 = false, attr128 = false;
+    bool& attr = ldr == 64 ? attr64 : attr128;
+    if (!attr) {
+      OGCP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, umma::kSmemG));
+      attr = true;
+    }
+    ProfScope prof_scope(ctx, kProfGram);
+    kern<<<nblk, umma::kThreadsG, umma::kSmemG, ctx->stream>>>(maps, rows, ngram, scratch.as<double>());
+    ctx->count();
+    k_gram_finalize<<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
+                      ctx->stream>>>(scratch.as<double>(), nblk, ngram, ldr, rank, outP, outC);
+    ctx->count();
+    check_launch();
+    return;
+  }
+  if (ldr == 32 || ldr == 64 || ldr == 128) {  // tensor-core path (mma.sync, split-TF32)
     // ldr 32: two CTAs per SM (80 KB of tiles each) to cover the load latency
     const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, kNumSMs * (ldr == 32 ? 2 : 1)));
     const int64_t rpb = (rows + nblk - 1) / nblk;

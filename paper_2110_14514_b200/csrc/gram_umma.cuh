@@ -1,0 +1,240 @@
+// K4 on the 5th-generation tensor cores (tcgen05 / TMEM, sm_100a): the history
+// Grams P = A'A and C = B'A (B = A_old) of a factor matrix with ldr 64 / 128
+// (reference gram kernels.py:75-98, _add_reg_and_history
+// solvers.py:159-179).  Included by compute.cu.
+//
+// Shape: D[M x N] += X[M x K] Y[K x N] with X = A' (or B'), Y = A, K = rows.  A
+// row of A is contiguous over both M (i) and N (j), so both UMMA operands are
+// MN-major views of the same shared-memory tile: no transpose.  M = 128 (ldr 64
+// pads X with two zero blocks), N = ldr; P and C accumulate in TMEM (fp32, 2 x
+// 128 columns) over all of a CTA's rows; CTAs write fp64 partials that
+// k_gram_finalize sums in block order (deterministic).
+//
+// Accuracy: fp32 inputs are split x = hi + lo (hi, lo TF32-rounded) and each
+// product is hi*hi + hi*lo + lo*hi (three kind::tf32 MMAs), which keeps fp32-level
+// accuracy like the mma.sync kernel it replaces.
+//
+// Pipeline (one CTA per SM, 3 stages of 32 rows):
+//   warp 0   TMA producer: 32-row boxes {32 floats, 32 rows} with SWIZZLE_128B into
+//            the hi tiles (one 4 KB box per 32 columns), mbarrier expect_tx;
+//   warps 2-5 converters: hi = rna_tf32(x) in place, lo = rna_tf32(x - hi),
+//            fence.proxy.async, arrive;  later the TMEM -> fp64 epilogue;
+//   warp 1   MMA issuer (one elected thread): 4 K-steps x (3 or 6) tcgen05.mma per
+//            stage, tcgen05.commit -> the stage's empty barrier.
+// Smem operand descriptor (canonical MN-major SWIZZLE_128B, uint128 units
+// ((8,n),(8,k)):((1,LBO),(8,SBO))): LBO = 4096 B between 32-column blocks,
+// SBO = 1024 B between 8-row groups; each K-step of 8 rows is one 1024 B atom.
+
+namespace umma {
+
+constexpr int kRows = 32;                    // rows (K) per stage
+constexpr int kStagesG = 3;
+constexpr int kTile = 4 * 4096;              // one operand tile: 4 column blocks x (32 rows x 128 B)
+constexpr int kStageBytes = 4 * kTile;       // A hi, A lo, B hi, B lo
+constexpr int kThreadsG = 192;               // 6 warps
+constexpr int kSmemG = kStagesG * kStageBytes + 1024 + 256;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* tm, int c0, int r0, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(tm), "r"(c0), "r"(r0), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// Canonical MN-major SWIZZLE_128B smem descriptor (version 1, layout type 2).
+__device__ __forceinline__ uint64_t mn_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(4096 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both MN-major, M = 128, N.
+__host__ __device__ constexpr uint32_t idesc_tf32(int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+
+struct GramMaps {
+  CUtensorMap a, b;
+};
+
+template <int LDR>
+__global__ void __launch_bounds__(kThreadsG, 1)
+    k_gram_umma(const __grid_constant__ GramMaps maps, int64_t rows, int ngram, double* __restrict__ partials) {
+  static_assert(LDR == 64 || LDR == 128, "UMMA Gram: ldr 64 or 128");
+  constexpr int NB = LDR / 32;  // 32-column (128 B) blocks per row
+  extern __shared__ __align__(1024) unsigned char g_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(g_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStagesG * kStageBytes);
+  uint64_t* conv = full + kStagesG;
+  uint64_t* empty = conv + kStagesG;
+  uint64_t* done = empty + kStagesG;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool two = ngram == 2;
+  const int64_t nchunks = (rows + kRows - 1) / kRows;
+  const int64_t G = gridDim.x, bi = blockIdx.x;
+  const int64_t my = nchunks > bi ? (nchunks - bi + G - 1) / G : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStagesG; ++s) {
+      bar_init(full + s, 1);
+      bar_init(conv + s, 4);
+      bar_init(empty + s, 1);
+    }
+    bar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // zero the column blocks TMA never writes (X is padded to M = 128 for ldr 64)
+  if (NB < 4) {
+    for (int s = 0; s < kStagesG; ++s)
+      for (int t = 0; t < 4; ++t) {
+        float4* z = reinterpret_cast<float4*>(sm + s * kStageBytes + t * kTile + NB * 4096);
+        for (int e = threadIdx.x; e < (4 - NB) * 4096 / 16; e += blockDim.x) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+  }
+  if (warp == 1) {  // TMEM: P in columns [0, 128), C in [128, 256)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      for (int64_t k = 0; k < my; ++k) {
+        const int s = (int)(k % kStagesG);
+        const int64_t u = k / kStagesG;
+        if (u > 0) bar_wait(empty + s, (unsigned)((u - 1) & 1));
+        unsigned char* st = sm + s * kStageBytes;
+        const int r0 = (int)((bi + k * G) * kRows);
+        bar_arrive_tx(full + s, (unsigned)(NB * 4096 * (two ? 2 : 1)));
+        for (int c = 0; c < NB; ++c) {
+          tma_box(st + c * 4096, &maps.a, 32 * c, r0, full + s);                  // A hi tile
+          if (two) tma_box(st + 2 * kTile + c * 4096, &maps.b, 32 * c, r0, full + s);  // B hi tile
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(LDR);
+      for (int64_t k = 0; k < my; ++k) {
+        const int s = (int)(k % kStagesG);
+        bar_wait(conv + s, (unsigned)((k / kStagesG) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t st = su32(sm + s * kStageBytes);
+        const uint32_t ahi = st, alo = st + kTile, bhi = st + 2 * kTile, blo = st + 3 * kTile;
+#pragma unroll
+        for (int g = 0; g < kRows / 8; ++g) {
+          const uint32_t o = g * 1024;
+          const uint32_t acc = (k > 0 || g > 0) ? 1u : 0u;
+          // P += Ahi'Ahi + Ahi'Alo + Alo'Ahi
+          mma_tf32(tmem, mn_desc(ahi + o), mn_desc(ahi + o), idesc, acc);
+          mma_tf32(tmem, mn_desc(ahi + o), mn_desc(alo + o), idesc, 1u);
+          mma_tf32(tmem, mn_desc(alo + o), mn_desc(ahi + o), idesc, 1u);
+          if (two) {  // C += Bhi'Ahi + Bhi'Alo + Blo'Ahi
+            mma_tf32(tmem + 128, mn_desc(bhi + o), mn_desc(ahi + o), idesc, acc);
+            mma_tf32(tmem + 128, mn_desc(bhi + o), mn_desc(alo + o), idesc, 1u);
+            mma_tf32(tmem + 128, mn_desc(blo + o), mn_desc(ahi + o), idesc, 1u);
+          }
+        }
+        mma_commit(empty + s);  // the stage's tiles may be refilled once these MMAs have read them
+      }
+      mma_commit(done);  // all accumulations complete
+    }
+  } else {
+    // ---------------------------------------------------------------- converters (warps 2-5)
+    const int ct = threadIdx.x - 64;  // 0 .. 127
+    for (int64_t k = 0; k < my; ++k) {
+      const int s = (int)(k % kStagesG);
+      bar_wait(full + s, (unsigned)((k / kStagesG) & 1));
+      unsigned char* st = sm + s * kStageBytes;
+      for (int t = 0; t < (two ? 2 : 1); ++t) {
+        float4* hi = reinterpret_cast<float4*>(st + 2 * t * kTile);
+        float4* lo = reinterpret_cast<float4*>(st + (2 * t + 1) * kTile);
+        for (int e = ct; e < NB * 4096 / 16; e += 128) {
+          const float4 x = hi[e];
+          float4 h, l;
+          h.x = rna_tf32(x.x); l.x = rna_tf32(x.x - h.x);
+          h.y = rna_tf32(x.y); l.y = rna_tf32(x.y - h.y);
+          h.z = rna_tf32(x.z); l.z = rna_tf32(x.z - h.z);
+          h.w = rna_tf32(x.w); l.w = rna_tf32(x.w - h.w);
+          hi[e] = h;
+          lo[e] = l;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
+      __syncwarp();
+      if (lane == 0) bar_arrive(conv + s);
+    }
+    // ---------------------------------------------------------------- epilogue: TMEM -> fp64 partials
+    bar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;              // TMEM lane quadrant this warp may read
+    const int m = 32 * q + lane;         // output row (i)
+    for (int gsel = 0; gsel < ngram; ++gsel) {
+      for (int c0 = 0; c0 < LDR; c0 += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(gsel * 128 + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+            "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (m < LDR) {
+          double* out = partials + ((int64_t)bi * ngram + gsel) * LDR * LDR + (int64_t)m * LDR + c0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) out[j] = my > 0 ? (double)__uint_as_float(r[j]) : 0.0;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
+}  // namespace umma

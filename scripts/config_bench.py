@@ -36,6 +36,8 @@ def main():
     args = ap.parse_args()
     if os.environ.get("OGCP_BUCKETS") == "0":
         _lib.set_buckets(False)
+    if os.environ.get("OGCP_UMMA") == "0":  # A/B knob: mma.sync Grams instead of tcgen05 / TMEM
+        _lib.set_umma_gram(False)
     kind = "bernoulli" if args.config == "c3" else "poisson"
     R = 16 if args.config == "c3" else args.rank
     H = 50 if args.config == "c3" else 500

@@ -261,17 +261,26 @@ def test_weight_solve_vs_oracle_large_ranks(R):
     np.testing.assert_allclose(res.trace.objective, tr, rtol=1e-4)
 
 
+@pytest.mark.parametrize("umma", [True, False])
 @pytest.mark.parametrize("R", [40, 64, 100, 128])
-def test_tensor_core_grams_vs_oracle(R):
-    """ldr 64 / 128 Grams run on tensor cores (split-TF32 mma): fp32-level accuracy,
-    checked norm-wise like the gradients (entries of a Hadamard of Grams of
-    random signs cancel, so elementwise relative error is meaningless near 0)."""
+def test_tensor_core_grams_vs_oracle(R, umma):
+    """ldr 64 / 128 Grams run on tensor cores -- tcgen05.mma kind::tf32 with TMEM
+    accumulators (csrc/gram_umma.cuh) or the mma.sync kernel -- with the split-TF32
+    3-product scheme: fp32-level accuracy, checked norm-wise like the gradients
+    (entries of a Hadamard of Grams of random signs cancel, so elementwise relative
+    error is meaningless near 0).  Mode sizes 3000 / 257 / 40 cover full chunks, a
+    ragged tail chunk and a single partial chunk."""
+    from paper_2110_14514_b200 import _lib
     rng = np.random.default_rng(R)
     dims = (3000, 257, 40)
     A = [rng.uniform(-1, 1, (d, R)) for d in dims]
     B = [a + 0.1 * rng.uniform(-1, 1, a.shape) for a in A]
-    for mode in (None, 1):
-        g, want = P.gram(A, mode), O.hadamard_gram(A, mode)
-        assert rel_err(g, want) < 1e-5
-        np.testing.assert_allclose(np.diag(g), np.diag(want), rtol=1e-5)
-        assert rel_err(P.gram(A, mode, other_factors=B), O.hadamard_gram(A, mode, B)) < 1e-5
+    _lib.set_umma_gram(umma)
+    try:
+        for mode in (None, 1):
+            g, want = P.gram(A, mode), O.hadamard_gram(A, mode)
+            assert rel_err(g, want) < 1e-5
+            np.testing.assert_allclose(np.diag(g), np.diag(want), rtol=1e-5)
+            assert rel_err(P.gram(A, mode, other_factors=B), O.hadamard_gram(A, mode, B)) < 1e-5
+    finally:
+        _lib.set_umma_gram(True)
