@@ -1866,16 +1866,16 @@ void sum_partials_enqueue(Ctx* ctx, const double* partials, int nblk, int len, d
   check_launch();
 }
 
-// [rows x ldr] fp32, boxes of {32 floats, 32 rows} with the 128-byte swizzle: the
-// canonical MN-major SWIZZLE_128B operand tiles of the UMMA Gram (gram_umma.cuh).
+// [rows x ldr] fp32 in raw row tiles of {ldr, 32 rows} (the UMMA Gram's converter
+// warps transpose them into its K-major operand tiles, gram_umma.cuh).
 static CUtensorMap gram_tile_map(const float* A, int64_t rows, int ldr) {
   CUtensorMap tm;
   cuuint64_t gdim[2] = {(cuuint64_t)ldr, (cuuint64_t)std::max<int64_t>(rows, 1)};
   cuuint64_t gstride[1] = {(cuuint64_t)ldr * 4};
-  cuuint32_t box[2] = {32, (cuuint32_t)umma::kRows};
+  cuuint32_t box[2] = {(cuuint32_t)ldr, (cuuint32_t)umma::kRows};
   cuuint32_t estr[2] = {1, 1};
   const CUresult r = tmap_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), gdim, gstride, box,
-                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(OGCP_E_CUDA, "cuTensorMapEncodeTiled (Gram tiles) failed (" + std::to_string((int)r) + ")");
   return tm;

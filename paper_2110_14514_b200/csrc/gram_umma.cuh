@@ -3,34 +3,35 @@
 // (reference gram kernels.py:75-98, _add_reg_and_history
 // solvers.py:159-179).  Included by compute.cu.
 //
-// Shape: D[M x N] += X[M x K] Y[K x N] with X = A' (or B'), Y = A, K = rows.  A
-// row of A is contiguous over both M (i) and N (j), so both UMMA operands are
-// MN-major views of the same shared-memory tile: no transpose.  M = 128 (ldr 64
-// pads X with two zero blocks), N = ldr; P and C accumulate in TMEM (fp32, 2 x
-// 128 columns) over all of a CTA's rows; CTAs write fp64 partials that
-// k_gram_finalize sums in block order (deterministic).
+// Shape: D[M x N] += X[M x K] Y[K x N] with X = A' (or B'), Y = A, K = rows.
+// kind::tf32 takes K-major shared-memory operands only (an MN-major tf32 operand
+// reads as zeros on this B200 -- measured, scripts/probes/probe_umma2.cu), so the
+// converter warps write each 32-row chunk transposed: T[i][k] = A[k][i], 128
+// rows i of 128 B (32 k's), in the canonical K-major SWIZZLE_128B layout (8-row
+// 1024 B atoms, 16-byte chunk index XOR row % 8).  T serves as both operands of
+// P (X = T_A as M x K, Y = T_A as N x K) and, with T_B, of C.  M = 128 (ldr 64
+// leaves rows 64..127 of T zero), N = ldr; P and C accumulate in TMEM (fp32,
+// columns [0,128) and [128,256)) over all of a CTA's rows; CTAs write fp64
+// partials that k_gram_finalize sums in block order (deterministic).
 //
-// Accuracy: fp32 inputs are split x = hi + lo (hi, lo TF32-rounded) and each
-// product is hi*hi + hi*lo + lo*hi (three kind::tf32 MMAs), which keeps fp32-level
-// accuracy like the mma.sync kernel it replaces.
+// Accuracy: x = hi + lo (hi, lo TF32-rounded, cvt.rna.tf32) and each product is
+// hi*hi + hi*lo + lo*hi (three MMAs), fp32-level like the mma.sync kernel.
 //
-// Pipeline (one CTA per SM, 3 stages of 32 rows):
-//   warp 0   TMA producer: 32-row boxes {32 floats, 32 rows} with SWIZZLE_128B into
-//            the hi tiles (one 4 KB box per 32 columns), mbarrier expect_tx;
-//   warps 2-5 converters: hi = rna_tf32(x) in place, lo = rna_tf32(x - hi),
-//            fence.proxy.async, arrive;  later the TMEM -> fp64 epilogue;
-//   warp 1   MMA issuer (one elected thread): 4 K-steps x (3 or 6) tcgen05.mma per
-//            stage, tcgen05.commit -> the stage's empty barrier.
-// Smem operand descriptor (canonical MN-major SWIZZLE_128B, uint128 units
-// ((8,n),(8,k)):((1,LBO),(8,SBO))): LBO = 4096 B between 32-column blocks,
-// SBO = 1024 B between 8-row groups; each K-step of 8 rows is one 1024 B atom.
+// Pipeline (one CTA per SM, 2 stages of 32 rows):
+//   warp 0    TMA producer: the raw [32 x ldr] row tiles of A (and B), expect_tx;
+//   warps 2-5 converters: split + transpose into T_hi / T_lo, fence.proxy.async,
+//             arrive; at the end the TMEM -> fp64 epilogue (tcgen05.ld 32x32b);
+//   warp 1    MMA issuer (one thread): 4 K-steps x 3 (or 6) tcgen05.mma per stage
+//             (the K-step advances the descriptor start by 32 B inside the atom),
+//             tcgen05.commit -> the stage's empty barrier.
 
 namespace umma {
 
 constexpr int kRows = 32;                    // rows (K) per stage
-constexpr int kStagesG = 3;
-constexpr int kTile = 4 * 4096;              // one operand tile: 4 column blocks x (32 rows x 128 B)
-constexpr int kStageBytes = 4 * kTile;       // A hi, A lo, B hi, B lo
+constexpr int kStagesG = 2;
+constexpr int kTile = 128 * 128;             // one transposed operand tile: 128 rows (i) x 128 B (32 k's)
+constexpr int kRaw = kRows * 128 * 4;        // one raw [32 x ldr] tile (ldr <= 128)
+constexpr int kStageBytes = 2 * kRaw + 4 * kTile;  // raw A, raw B, T_A hi, T_A lo, T_B hi, T_B lo
 constexpr int kThreadsG = 192;               // 6 warps
 constexpr int kSmemG = kStagesG * kStageBytes + 1024 + 256;
 
@@ -67,15 +68,19 @@ __device__ __forceinline__ float rna_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-// Canonical MN-major SWIZZLE_128B smem descriptor (version 1, layout type 2).
-__device__ __forceinline__ uint64_t mn_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(4096 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         (1ull << 46) | (2ull << 61);
+// Canonical K-major SWIZZLE_128B smem descriptor (version 1, layout type 2):
+// 8-row groups 1024 B apart (SBO); LBO unused for swizzled K-major.
+__device__ __forceinline__ uint64_t k_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+         (2ull << 61);
 }
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both MN-major, M = 128, N.
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N.
 __host__ __device__ constexpr uint32_t idesc_tf32(int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+// Byte offset of element (row i, k) in a K-major SWIZZLE_128B tile of 128-byte rows.
+__device__ __forceinline__ uint32_t swz(int i, int k) {
+  return (uint32_t)((i >> 3) * 1024 + (i & 7) * 128 + ((((k >> 2) ^ (i & 7)) & 7) << 4) + (k & 3) * 4);
 }
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -96,7 +101,6 @@ template <int LDR>
 __global__ void __launch_bounds__(kThreadsG, 1)
     k_gram_umma(const __grid_constant__ GramMaps maps, int64_t rows, int ngram, double* __restrict__ partials) {
   static_assert(LDR == 64 || LDR == 128, "UMMA Gram: ldr 64 or 128");
-  constexpr int NB = LDR / 32;  // 32-column (128 B) blocks per row
   extern __shared__ __align__(1024) unsigned char g_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(g_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStagesG * kStageBytes);
@@ -109,6 +113,9 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   const int64_t nchunks = (rows + kRows - 1) / kRows;
   const int64_t G = gridDim.x, bi = blockIdx.x;
   const int64_t my = nchunks > bi ? (nchunks - bi + G - 1) / G : 0;
+  // stage s: raw A | raw B | T_A hi | T_A lo | T_B hi | T_B lo
+  auto raw = [&](int s, int t) { return sm + s * kStageBytes + t * kRaw; };
+  auto tt = [&](int s, int t, int lo) { return sm + s * kStageBytes + 2 * kRaw + (2 * t + lo) * kTile; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesG; ++s) {
@@ -119,19 +126,20 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     bar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // zero the column blocks TMA never writes (X is padded to M = 128 for ldr 64)
-  if (NB < 4) {
+  if (LDR < 128) {  // rows i >= ldr of every T tile stay zero (M is padded to 128)
     for (int s = 0; s < kStagesG; ++s)
-      for (int t = 0; t < 4; ++t) {
-        float4* z = reinterpret_cast<float4*>(sm + s * kStageBytes + t * kTile + NB * 4096);
-        for (int e = threadIdx.x; e < (4 - NB) * 4096 / 16; e += blockDim.x) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      for (int t = 0; t < 2; ++t)
+        for (int lo = 0; lo < 2; ++lo) {
+          float4* z = reinterpret_cast<float4*>(tt(s, t, lo) + LDR * 128);
+          for (int e = threadIdx.x; e < (128 - LDR) * 128 / 16; e += blockDim.x) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
   }
   if (warp == 1) {  // TMEM: P in columns [0, 128), C in [128, 256)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the zeroed rows, for the tensor core
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -144,13 +152,10 @@ __global__ void __launch_bounds__(kThreadsG, 1)
         const int s = (int)(k % kStagesG);
         const int64_t u = k / kStagesG;
         if (u > 0) bar_wait(empty + s, (unsigned)((u - 1) & 1));
-        unsigned char* st = sm + s * kStageBytes;
         const int r0 = (int)((bi + k * G) * kRows);
-        bar_arrive_tx(full + s, (unsigned)(NB * 4096 * (two ? 2 : 1)));
-        for (int c = 0; c < NB; ++c) {
-          tma_box(st + c * 4096, &maps.a, 32 * c, r0, full + s);                  // A hi tile
-          if (two) tma_box(st + 2 * kTile + c * 4096, &maps.b, 32 * c, r0, full + s);  // B hi tile
-        }
+        bar_arrive_tx(full + s, (unsigned)(kRows * LDR * 4 * (two ? 2 : 1)));
+        tma_box(raw(s, 0), &maps.a, 0, r0, full + s);
+        if (two) tma_box(raw(s, 1), &maps.b, 0, r0, full + s);
       }
     }
   } else if (warp == 1) {
@@ -161,23 +166,23 @@ __global__ void __launch_bounds__(kThreadsG, 1)
         const int s = (int)(k % kStagesG);
         bar_wait(conv + s, (unsigned)((k / kStagesG) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t st = su32(sm + s * kStageBytes);
-        const uint32_t ahi = st, alo = st + kTile, bhi = st + 2 * kTile, blo = st + 3 * kTile;
+        const uint32_t ahi = su32(tt(s, 0, 0)), alo = su32(tt(s, 0, 1));
+        const uint32_t bhi = su32(tt(s, 1, 0)), blo = su32(tt(s, 1, 1));
 #pragma unroll
         for (int g = 0; g < kRows / 8; ++g) {
-          const uint32_t o = g * 1024;
+          const uint32_t o = g * 32;  // K-step of 8 tf32 = 32 bytes inside the 128-byte swizzle atom
           const uint32_t acc = (k > 0 || g > 0) ? 1u : 0u;
           // P += Ahi'Ahi + Ahi'Alo + Alo'Ahi
-          mma_tf32(tmem, mn_desc(ahi + o), mn_desc(ahi + o), idesc, acc);
-          mma_tf32(tmem, mn_desc(ahi + o), mn_desc(alo + o), idesc, 1u);
-          mma_tf32(tmem, mn_desc(alo + o), mn_desc(ahi + o), idesc, 1u);
+          mma_tf32(tmem, k_desc(ahi + o), k_desc(ahi + o), idesc, acc);
+          mma_tf32(tmem, k_desc(ahi + o), k_desc(alo + o), idesc, 1u);
+          mma_tf32(tmem, k_desc(alo + o), k_desc(ahi + o), idesc, 1u);
           if (two) {  // C += Bhi'Ahi + Bhi'Alo + Blo'Ahi
-            mma_tf32(tmem + 128, mn_desc(bhi + o), mn_desc(ahi + o), idesc, acc);
-            mma_tf32(tmem + 128, mn_desc(bhi + o), mn_desc(alo + o), idesc, 1u);
-            mma_tf32(tmem + 128, mn_desc(blo + o), mn_desc(ahi + o), idesc, 1u);
+            mma_tf32(tmem + 128, k_desc(bhi + o), k_desc(ahi + o), idesc, acc);
+            mma_tf32(tmem + 128, k_desc(bhi + o), k_desc(alo + o), idesc, 1u);
+            mma_tf32(tmem + 128, k_desc(blo + o), k_desc(ahi + o), idesc, 1u);
           }
         }
-        mma_commit(empty + s);  // the stage's tiles may be refilled once these MMAs have read them
+        mma_commit(empty + s);  // the stage may be refilled once these MMAs have read it
       }
       mma_commit(done);  // all accumulations complete
     }
@@ -187,19 +192,17 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     for (int64_t k = 0; k < my; ++k) {
       const int s = (int)(k % kStagesG);
       bar_wait(full + s, (unsigned)((k / kStagesG) & 1));
-      unsigned char* st = sm + s * kStageBytes;
       for (int t = 0; t < (two ? 2 : 1); ++t) {
-        float4* hi = reinterpret_cast<float4*>(st + 2 * t * kTile);
-        float4* lo = reinterpret_cast<float4*>(st + (2 * t + 1) * kTile);
-        for (int e = ct; e < NB * 4096 / 16; e += 128) {
-          const float4 x = hi[e];
-          float4 h, l;
-          h.x = rna_tf32(x.x); l.x = rna_tf32(x.x - h.x);
-          h.y = rna_tf32(x.y); l.y = rna_tf32(x.y - h.y);
-          h.z = rna_tf32(x.z); l.z = rna_tf32(x.z - h.z);
-          h.w = rna_tf32(x.w); l.w = rna_tf32(x.w - h.w);
-          hi[e] = h;
-          lo[e] = l;
+        const float* x = reinterpret_cast<const float*>(raw(s, t));
+        unsigned char* hi = tt(s, t, 0);
+        unsigned char* lo = tt(s, t, 1);
+        for (int e = ct; e < kRows * LDR; e += 128) {
+          const int kk = e / LDR, i = e - kk * LDR;
+          const float v = x[e];
+          const float h = rna_tf32(v);
+          const uint32_t off = swz(i, kk);
+          *reinterpret_cast<float*>(hi + off) = h;
+          *reinterpret_cast<float*>(lo + off) = rna_tf32(v - h);
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
@@ -209,8 +212,8 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     // ---------------------------------------------------------------- epilogue: TMEM -> fp64 partials
     bar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;              // TMEM lane quadrant this warp may read
-    const int m = 32 * q + lane;         // output row (i)
+    const int q = warp & 3;       // TMEM lane quadrant this warp may read
+    const int m = 32 * q + lane;  // output row (i)
     for (int gsel = 0; gsel < ngram; ++gsel) {
       for (int c0 = 0; c0 < LDR; c0 += 32) {
         uint32_t r[32];
