@@ -19,8 +19,9 @@
 //
 // Pipeline (one CTA per SM, 2 stages of 32 rows):
 //   warp 0    TMA producer: the raw [32 x ldr] row tiles of A (and B), expect_tx;
-//   warps 2-5 converters: split + transpose into T_hi / T_lo, fence.proxy.async,
-//             arrive; at the end the TMEM -> fp64 epilogue (tcgen05.ld 32x32b);
+//   warps 2-9 converters: split + transpose into T_hi / T_lo (16-byte chunks),
+//             fence.proxy.async, arrive; warps 2-5 then run the TMEM -> fp64
+//             epilogue (tcgen05.ld 32x32b, one TMEM lane quadrant each);
 //   warp 1    MMA issuer (one thread): 4 K-steps x 3 (or 6) tcgen05.mma per stage
 //             (the K-step advances the descriptor start by 32 B inside the atom),
 //             tcgen05.commit -> the stage's empty barrier.
@@ -32,7 +33,7 @@ constexpr int kStagesG = 2;
 constexpr int kTile = 128 * 128;             // one transposed operand tile: 128 rows (i) x 128 B (32 k's)
 constexpr int kRaw = kRows * 128 * 4;        // one raw [32 x ldr] tile (ldr <= 128)
 constexpr int kStageBytes = 2 * kRaw + 4 * kTile;  // raw A, raw B, T_A hi, T_A lo, T_B hi, T_B lo
-constexpr int kThreadsG = 192;               // 6 warps
+constexpr int kThreadsG = 320;               // 10 warps: TMA, MMA, 8 converters (4 of them run the epilogue)
 constexpr int kSmemG = kStagesG * kStageBytes + 1024 + 256;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStagesG; ++s) {
       bar_init(full + s, 1);
-      bar_init(conv + s, 4);
+      bar_init(conv + s, 8);
       bar_init(empty + s, 1);
     }
     bar_init(done, 1);
@@ -187,8 +188,10 @@ __global__ void __launch_bounds__(kThreadsG, 1)
       mma_commit(done);  // all accumulations complete
     }
   } else {
-    // ---------------------------------------------------------------- converters (warps 2-5)
-    const int ct = threadIdx.x - 64;  // 0 .. 127
+    // ---------------------------------------------------------------- converters (warps 2-9)
+    // thread -> (row i, 4 consecutive k): 4 raw loads down a column (lanes take
+    // consecutive i: conflict-free), one 16-byte swizzled chunk of T_hi and of T_lo
+    const int ct = threadIdx.x - 64;  // 0 .. 255
     for (int64_t k = 0; k < my; ++k) {
       const int s = (int)(k % kStagesG);
       bar_wait(full + s, (unsigned)((k / kStagesG) & 1));
@@ -196,41 +199,49 @@ __global__ void __launch_bounds__(kThreadsG, 1)
         const float* x = reinterpret_cast<const float*>(raw(s, t));
         unsigned char* hi = tt(s, t, 0);
         unsigned char* lo = tt(s, t, 1);
-        for (int e = ct; e < kRows * LDR; e += 128) {
-          const int kk = e / LDR, i = e - kk * LDR;
-          const float v = x[e];
-          const float h = rna_tf32(v);
-          const uint32_t off = swz(i, kk);
-          *reinterpret_cast<float*>(hi + off) = h;
-          *reinterpret_cast<float*>(lo + off) = rna_tf32(v - h);
+        for (int e = ct; e < (kRows / 4) * LDR; e += 256) {
+          const int k4 = e / LDR, i = e - k4 * LDR;
+          float v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[j] = x[(4 * k4 + j) * LDR + i];
+          float4 h, l;
+          h.x = rna_tf32(v[0]); l.x = rna_tf32(v[0] - h.x);
+          h.y = rna_tf32(v[1]); l.y = rna_tf32(v[1] - h.y);
+          h.z = rna_tf32(v[2]); l.z = rna_tf32(v[2] - h.z);
+          h.w = rna_tf32(v[3]); l.w = rna_tf32(v[3] - h.w);
+          const uint32_t off = swz(i, 4 * k4);
+          *reinterpret_cast<float4*>(hi + off) = h;
+          *reinterpret_cast<float4*>(lo + off) = l;
         }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
       __syncwarp();
       if (lane == 0) bar_arrive(conv + s);
     }
-    // ---------------------------------------------------------------- epilogue: TMEM -> fp64 partials
-    bar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;       // TMEM lane quadrant this warp may read
-    const int m = 32 * q + lane;  // output row (i)
-    for (int gsel = 0; gsel < ngram; ++gsel) {
-      for (int c0 = 0; c0 < LDR; c0 += 32) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(gsel * 128 + c0);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-            "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (m < LDR) {
-          double* out = partials + ((int64_t)bi * ngram + gsel) * LDR * LDR + (int64_t)m * LDR + c0;
+    if (warp < 6) {  // warps 2-5, one per TMEM lane quadrant, run the epilogue
+      // ---------------------------------------------------------------- epilogue: TMEM -> fp64 partials
+      bar_wait(done, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int q = warp & 3;       // TMEM lane quadrant this warp may read
+      const int m = 32 * q + lane;  // output row (i)
+      for (int gsel = 0; gsel < ngram; ++gsel) {
+        for (int c0 = 0; c0 < LDR; c0 += 32) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(gsel * 128 + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+              "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (m < LDR) {
+            double* out = partials + ((int64_t)bi * ngram + gsel) * LDR * LDR + (int64_t)m * LDR + c0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) out[j] = my > 0 ? (double)__uint_as_float(r[j]) : 0.0;
+            for (int j = 0; j < 32; ++j) out[j] = my > 0 ? (double)__uint_as_float(r[j]) : 0.0;
+          }
         }
       }
     }
