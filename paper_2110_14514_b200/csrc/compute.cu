@@ -1003,16 +1003,22 @@ void gram_small_enqueue(Ctx* ctx, const SmallGrams& g, int ndim, int rank, int l
 }
 
 // Sum block partials (fixed order) and extract the rank x rank blocks.
-__global__ void k_gram_finalize(const double* __restrict__ partials, int nblk, int ngram, int ldr, int rank,
+template <typename T>
+__global__ void k_gram_finalize(const T* __restrict__ partials, int nblk, int ngram, int ldr, int rank,
                                 double* __restrict__ outP, double* __restrict__ outC) {
   const int LL = ldr * ldr;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ngram * rank * rank; e += gridDim.x * blockDim.x) {
     const int g = e / (rank * rank);
     const int ij = e % (rank * rank);
     const int i = ij / rank, j = ij % rank;
-    double t = 0.0;
-    for (int b = 0; b < nblk; ++b) t += partials[((int64_t)b * ngram + g) * LL + i * ldr + j];
-    (g == 0 ? outP : outC)[ij] = t;
+    double t0 = 0.0, t1 = 0.0;  // fixed order: even / odd blocks, then combined
+    int b = 0;
+    for (; b + 1 < nblk; b += 2) {
+      t0 += (double)partials[((int64_t)b * ngram + g) * LL + i * ldr + j];
+      t1 += (double)partials[((int64_t)(b + 1) * ngram + g) * LL + i * ldr + j];
+    }
+    if (b < nblk) t0 += (double)partials[((int64_t)b * ngram + g) * LL + i * ldr + j];
+    (g == 0 ? outP : outC)[ij] = t0 + t1;
   }
 }
 
@@ -1887,7 +1893,7 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
   if ((ldr == 64 || ldr == 128) && ctx->umma_gram && rows > 0) {  // tcgen05 / TMEM path (gram_umma.cuh)
     const int64_t nchunks = (rows + umma::kRows - 1) / umma::kRows;
     const int nblk = (int)std::min<int64_t>(nchunks, kNumSMs);
-    scratch.ensure((size_t)nblk * ngram * ldr * ldr * 8);
+    scratch.ensure((size_t)nblk * ngram * ldr * ldr * 4);  // fp32 CTA partials (the TMEM accumulators)
     umma::GramMaps maps;
     maps.a = gram_tile_map(A, rows, ldr);
     maps.b = B ? gram_tile_map(B, rows, ldr) : maps.a;
@@ -1899,10 +1905,10 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
       attr = true;
     }
     ProfScope prof_scope(ctx, kProfGram);
-    kern<<<nblk, umma::kThreadsG, umma::kSmemG, ctx->stream>>>(maps, rows, ngram, scratch.as<double>());
+    kern<<<nblk, umma::kThreadsG, umma::kSmemG, ctx->stream>>>(maps, rows, ngram, scratch.as<float>());
     ctx->count();
-    k_gram_finalize<<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
-                      ctx->stream>>>(scratch.as<double>(), nblk, ngram, ldr, rank, outP, outC);
+    k_gram_finalize<float><<<std::max(1, ceil_div_i((int64_t)ngram * rank * rank, 256)), 256, 0, ctx->stream>>>(
+        scratch.as<float>(), nblk, ngram, ldr, rank, outP, outC);
     ctx->count();
     check_launch();
     return;
@@ -1918,7 +1924,7 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
       ProfScope prof_scope(ctx, kProfGram);
       kern<<<nblk, kThreads, smem, ctx->stream>>>(A, B ? B : A, rows, rpb, ngram, scratch.as<double>());
       ctx->count();
-      k_gram_finalize<<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
+      k_gram_finalize<double><<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
                         ctx->stream>>>(scratch.as<double>(), nblk, ngram, ldr, rank, outP, outC);
       ctx->count();
       check_launch();
@@ -1947,7 +1953,7 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
                                                    scratch.as<double>());
     ctx->count();
   }
-  k_gram_finalize<<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
+  k_gram_finalize<double><<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
                     ctx->stream>>>(scratch.as<double>(), nblk, ngram, ldr, rank, outP, outC);
   ctx->count();
   check_launch();

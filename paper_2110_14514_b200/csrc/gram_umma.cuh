@@ -11,8 +11,9 @@
 // 1024 B atoms, 16-byte chunk index XOR row % 8).  T serves as both operands of
 // P (X = T_A as M x K, Y = T_A as N x K) and, with T_B, of C.  M = 128 (ldr 64
 // leaves rows 64..127 of T zero), N = ldr; P and C accumulate in TMEM (fp32,
-// columns [0,128) and [128,256)) over all of a CTA's rows; CTAs write fp64
-// partials that k_gram_finalize sums in block order (deterministic).
+// columns [0,128) and [128,256)) over all of a CTA's rows; CTAs write their fp32
+// accumulators as partials that k_gram_finalize sums in fp64 in block order
+// (deterministic).
 //
 // Accuracy: x = hi + lo (hi, lo TF32-rounded, cvt.rna.tf32) and each product is
 // hi*hi + hi*lo + lo*hi (three MMAs), fp32-level like the mma.sync kernel.
@@ -100,7 +101,7 @@ struct GramMaps {
 
 template <int LDR>
 __global__ void __launch_bounds__(kThreadsG, 1)
-    k_gram_umma(const __grid_constant__ GramMaps maps, int64_t rows, int ngram, double* __restrict__ partials) {
+    k_gram_umma(const __grid_constant__ GramMaps maps, int64_t rows, int ngram, float* __restrict__ partials) {
   static_assert(LDR == 64 || LDR == 128, "UMMA Gram: ldr 64 or 128");
   extern __shared__ __align__(1024) unsigned char g_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(g_raw) + 1023) & ~(uintptr_t)1023);
@@ -238,9 +239,13 @@ __global__ void __launch_bounds__(kThreadsG, 1)
               : "r"(taddr));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           if (m < LDR) {
-            double* out = partials + ((int64_t)bi * ngram + gsel) * LDR * LDR + (int64_t)m * LDR + c0;
+            float4* out = reinterpret_cast<float4*>(partials + ((int64_t)bi * ngram + gsel) * LDR * LDR +
+                                                    (int64_t)m * LDR + c0);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) out[j] = my > 0 ? (double)__uint_as_float(r[j]) : 0.0;
+            for (int j = 0; j < 8; ++j)
+              out[j] = my > 0 ? make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                            __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
       }

@@ -26,12 +26,12 @@ int main() {
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   printf("encode %d\n", (int)r);
   maps.b = maps.a;
-  double* part; cudaMalloc(&part, 2 * LDR * LDR * 8); cudaMemset(part, 0xff, 2 * LDR * LDR * 8);
+  float* part; cudaMalloc(&part, 2 * LDR * LDR * 4); cudaMemset(part, 0xff, 2 * LDR * LDR * 4);
   cudaFuncSetAttribute(umma::k_gram_umma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, umma::kSmemG);
   umma::k_gram_umma<128><<<1, umma::kThreadsG, umma::kSmemG>>>(maps, rows, 1, part);
   printf("kernel: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
-  std::vector<double> o(LDR * LDR);
-  cudaMemcpy(o.data(), part, o.size() * 8, cudaMemcpyDeviceToHost);
+  std::vector<float> o(LDR * LDR);
+  cudaMemcpy(o.data(), part, o.size() * 4, cudaMemcpyDeviceToHost);
   double err = 0, nrm = 0;
   for (int i = 0; i < LDR; ++i) for (int j = 0; j < LDR; ++j) {
     double w = 0; for (int k = 0; k < rows; ++k) w += (double)h[k * LDR + i] * h[k * LDR + j];
