@@ -299,6 +299,11 @@ def set_umma_gram(on: bool):
     check(lib().ogcp_ctx_set_option(ctx(), 9, int(bool(on))))
 
 
+def set_deterministic(on: bool):
+    """Engine option OGCP_OPT_DETERMINISTIC: fixed-order (bitwise reproducible) K3 for small models."""
+    check(lib().ogcp_ctx_set_option(ctx(), 10, int(bool(on))))
+
+
 def set_split_scatter(on: bool):
     """Engine option OGCP_OPT_SPLIT_SCATTER for the current device's context."""
     check(lib().ogcp_ctx_set_option(ctx(), 2, int(bool(on))))

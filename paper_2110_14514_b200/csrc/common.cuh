@@ -174,6 +174,8 @@ struct Ctx {
     }
     return wticket_buf.as<unsigned int>();
   }
+  bool deterministic = false;   // small models: fixed-order (bitwise reproducible) K3 scatter
+  DevBuf det_partials;
   bool umma_gram = true;        // ldr 64 / 128 Grams on tcgen05 / TMEM (gram_umma.cuh)
   bool batch_draws = true;      // small draws: every draw of a solver epoch made at its start (one launch per pass)
   bool sort_zeros = false;      // bucketed merged draws: zero rows sorted by (bucket, mode-0 row);

@@ -1570,6 +1570,159 @@ static int sample_grid(K kern, size_t smem, int64_t total, int G, int U) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)kNumSMs * per_sm));
 }
 
+// ------------------------------------------------------------------ K3, deterministic (small models)
+// Bitwise run-to-run reproducible sampled MTTKRP for small models (every mode's
+// gradient fits a per-warp shared-memory copy): block b takes a fixed contiguous
+// range of the samples, warp w a fixed sub-range; a group of G lanes (one float4
+// each, G = ldr / 4) evaluates one sample, and the groups of a warp add their
+// contributions to the warp's private copy one group at a time (fixed order, no
+// atomics).  The block sums its warps' copies in warp order into a block partial;
+// the last block to finish (ticket) sums the partials in block order into G.
+// Every float addition has a fixed order, so the same sample set gives the same
+// bits -- the reference's same-seed bitwise trajectories (tests/test_streaming.py:
+// 222-238 there) hold for these shapes.  Reference: sampled_mttkrp kernels.py:33-56.
+constexpr int kDetThreads = 256;
+constexpr int64_t kDetMaxFloats = 4096;  // per-warp copy: sum_k dims[k] * ldr floats (16 KB)
+
+struct DetP {
+  int64_t off[kMaxModes];  // float offset of mode k inside a gradient copy
+  int64_t len;             // floats of one copy
+  unsigned int* ticket;
+  float* partials;         // [gridDim.x x len]
+};
+
+template <int G>
+__global__ void __launch_bounds__(kDetThreads) k_sgrad_det(SamplesP S, ModelP M, const float* __restrict__ s_f,
+                                                          LossP L, GradPtrs GP, DetP D, DevFlags* flags,
+                                                          long long code) {
+  extern __shared__ float wacc[];  // [8 warps][D.len]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / G, gl = lane % G;
+  constexpr int kGroups = 32 / G;
+  const int nd = M.ndim, ldr = M.ldr;
+  float* mine = wacc + (int64_t)warp * D.len;
+  for (int64_t e = lane; e < D.len; e += 32) mine[e] = 0.f;
+  __syncwarp();
+  const float4 s4 = gl * 4 < ldr ? __ldg(reinterpret_cast<const float4*>(s_f) + gl) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t p = S.p_dev ? (int64_t)*S.p_dev : S.p;
+  const int64_t total = p + (S.q_dev ? (int64_t)*S.q_dev : S.q);
+  const int64_t per_blk = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t blo = blockIdx.x * per_blk, bhi = min(total, blo + per_blk);
+  const int64_t per_w = (bhi - blo + (kDetThreads / 32) - 1) / (kDetThreads / 32);
+  const int64_t wlo = blo + warp * per_w, whi = min(bhi, wlo + per_w);
+  unsigned bits = 0;
+  for (int64_t base = wlo; base < whi; base += kGroups) {
+    const int64_t n = base + grp;
+    bool valid = n < whi;
+    int idx[kMaxModes];
+    float x = 0.f, scale = 0.f;
+    bool nz = false;
+    if (valid) {
+      if (n < p) {
+        nz = true;
+        const int o = __ldg(S.ord + n);
+        const int* r = S.rec + (int64_t)o * S.rec_ints;
+        for (int k = 0; k < nd; ++k) idx[k] = __ldg(r + k);
+        x = __int_as_float(__ldg(r + nd));
+        scale = (float)S.nz_scale * (S.cnt ? (float)__ldg(S.cnt + n) : 1.0f);
+      } else {
+        const int32_t* z = S.zsub + (n - p) * nd;
+        for (int k = 0; k < nd; ++k) idx[k] = __ldg(z + k);
+        valid = idx[0] >= 0;  // lazy layout: a rejected candidate
+        scale = (float)S.zero_scale;
+      }
+    }
+    float4 a[kMaxModes];
+    float4 pr = make_float4(1.f, 1.f, 1.f, 1.f);
+    for (int k = 0; k < nd; ++k) {
+      a[k] = (valid && gl * 4 < ldr) ? __ldg(reinterpret_cast<const float4*>(M.A[k] + (int64_t)idx[k] * ldr) + gl)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      pr = mul4(pr, a[k]);
+    }
+    float m = dot4(pr, s4);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) m += __shfl_xor_sync(kFull, m, o);
+    float y = 0.f;
+    if (valid) {
+      bits |= domain_bits(L.kind, m);
+      y = dloss(L.kind, nz ? x : 0.f, m, L.eps);
+      if (S.semi && nz) y -= dloss(L.kind, 0.0f, m, L.eps);
+      y *= scale;
+    }
+    // groups add in fixed order
+    for (int g2 = 0; g2 < kGroups; ++g2) {
+      if (grp == g2 && valid && gl * 4 < ldr) {
+        for (int k = 0; k < nd; ++k) {
+          float4 c = make_float4(y * s4.x, y * s4.y, y * s4.z, y * s4.w);
+          for (int j = 0; j < nd; ++j)
+            if (j != k) c = mul4(c, a[j]);
+          float* dst = mine + D.off[k] + (int64_t)idx[k] * ldr + gl * 4;
+          dst[0] += c.x;
+          dst[1] += c.y;
+          dst[2] += c.z;
+          dst[3] += c.w;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (bits) report(flags, kFlagData, code, bits);
+  __syncthreads();
+  float* part = D.partials + (int64_t)blockIdx.x * D.len;
+  for (int64_t e = threadIdx.x; e < D.len; e += blockDim.x) {
+    float t = 0.f;
+    for (int w = 0; w < kDetThreads / 32; ++w) t += wacc[(int64_t)w * D.len + e];
+    part[e] = t;
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(D.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int64_t e = threadIdx.x; e < D.len; e += blockDim.x) {
+    float t = 0.f;
+    for (int b = 0; b < (int)gridDim.x; ++b) t += D.partials[(int64_t)b * D.len + e];
+    int k = 0;
+    while (k + 1 < nd && e >= D.off[k + 1]) ++k;
+    GP.g[k][e - D.off[k]] = t;
+  }
+  if (threadIdx.x == 0) *D.ticket = 0u;
+}
+
+// Launch the deterministic scatter when the model is small enough; false otherwise.
+static bool sgrad_det_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_f, const LossP& L,
+                              const GradPtrs& GP, long long code) {
+  if (!ctx->deterministic || S.shard_world > 1 || M.ldr > 32 || M.ndim > kMaxModes) return false;
+  DetP D{};
+  int64_t len = 0;
+  for (int k = 0; k < M.ndim; ++k) {
+    D.off[k] = len;
+    len += M.dims[k] * M.ldr;
+  }
+  if (len > kDetMaxFloats) return false;
+  D.len = len;
+  const int64_t total = S.p + S.q;
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 64));
+  D.partials = static_cast<float*>(ctx->det_partials.ensure((size_t)nblk * len * 4));
+  D.ticket = ctx->wticket() + 1;  // second counter of the ticket buffer (0 between launches)
+  const size_t smem = (size_t)(kDetThreads / 32) * len * 4;
+  auto go = [&](auto kern) {
+    allow_smem(kern, smem);
+    kern<<<nblk, kDetThreads, smem, ctx->stream>>>(S, M, s_f, L, GP, D, ctx->flags.as<DevFlags>(), code);
+  };
+  switch (M.ldr) {
+    case 4: go(k_sgrad_det<1>); break;
+    case 8: go(k_sgrad_det<2>); break;
+    case 16: go(k_sgrad_det<4>); break;
+    default: go(k_sgrad_det<8>); break;
+  }
+  ctx->count();
+  check_launch();
+  return true;
+}
+
 // The lean 3-way walks (walk3.cuh) serve merged sets of 3-way slices at ldr 16 / 32
 // (at ldr 64 the double-buffered rows exceed the register budget).
 static bool lean_walk(const Ctx* ctx, const SamplesP& S, const ModelP& M) {
@@ -1726,6 +1879,10 @@ void sgrad_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, const float* s_
   }
   const int64_t total = S.p + S.q;
   if (total == 0) return;
+  {
+    ProfScope prof_scope(ctx, kProfSgrad);
+    if (sgrad_det_enqueue(ctx, S, M, s_f, L, GP, code)) return;
+  }
   // privatise small modes in shared memory when the per-CTA flush is cheap
   PrivP PV;
   PV.nmodes = 0;

@@ -1492,6 +1492,7 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   else if (option == OGCP_OPT_SORT_ZEROS) ctx->sort_zeros = value != 0;
   else if (option == OGCP_OPT_BATCH_DRAWS) ctx->batch_draws = value != 0;
   else if (option == OGCP_OPT_UMMA_GRAM) ctx->umma_gram = value != 0;
+  else if (option == OGCP_OPT_DETERMINISTIC) ctx->deterministic = value != 0;
   else if (option == OGCP_OPT_LEAN_WALKS) ctx->lean_walks = value != 0;
   else if (option == OGCP_OPT_TMA_WALKS) {
     ctx->tma_walks = (value & 1) != 0;
