@@ -36,6 +36,10 @@
 // gradient's summation order is fixed (deterministic); the K3 reductions into
 // modes 1 and 2 are float atomics (order-dependent in the last bits).
 
+#ifndef OGCP_TMA_STAGES
+#define OGCP_TMA_STAGES 16  // multiple of 8 (producer / consumer warps); fewer stages leave SM room for the draw
+#endif
+
 namespace walkt {
 
 constexpr int kT = 32;          // samples per stage (tile)
@@ -54,7 +58,7 @@ struct StageLayout {
   static constexpr int kRowsBytes = kModes * kT * kRowBytes;          // rows[mode][slot][ldr]
   static constexpr int kMetaBytes = 7 * kT * 4;                       // i0 i1 i2 x mult slot0 uniq0
   static constexpr int kBytes = (kRowsBytes + kMetaBytes + 127) / 128 * 128;
-  static constexpr int kStages = A2S ? 8 : 16;                        // smem ring depth
+  static constexpr int kStages = A2S ? 8 : OGCP_TMA_STAGES;           // smem ring depth
   static constexpr int kA2Off = kStages * kBytes;                     // resident mode-2 rows
   static constexpr int kSmemFixed = kStages * kBytes + 2 * kStages * 8 + 128;  // + barriers + alignment slack
 };

@@ -38,6 +38,8 @@ def main():
     import torch
     import paper_2110_14514_b200 as P
     from test_gpu_streams import stream_config, stream_data, ckpt_path
+    if os.environ.get("OGCP_DET") == "1":  # fixed-order (bitwise reproducible) factor-gradient scatter
+        P._lib.set_deterministic(True)
     golden = os.path.join(ROOT, "tests", "golden")
     g = np.load(os.path.join(golden, f"stream_{args.config}.npz"))
     cfg, loss = stream_config(args.config)
