@@ -346,8 +346,9 @@ def main():
         _lib.set_sort_zeros(os.environ["OGCP_SORT_ZEROS"] == "1")
     if os.environ.get("OGCP_LEAN"):  # A/B knob for the register-pipelined 3-way walk kernels
         _lib.set_lean_walks(os.environ["OGCP_LEAN"] == "1")
-    if os.environ.get("OGCP_TMA"):  # A/B knob for the TMA-fed 3-way walk kernels (0 off, 1 on, 2 + A2 residency)
-        _lib.set_tma_walks(os.environ["OGCP_TMA"] != "0", a2_resident=os.environ["OGCP_TMA"] == "2")
+    if os.environ.get("OGCP_TMA"):  # A/B knob for the TMA-fed 3-way walks (0 off, 1 on, 2 + A2 residency, 3 + weight walk)
+        _lib.set_tma_walks(os.environ["OGCP_TMA"] != "0", wgrad=os.environ["OGCP_TMA"] == "3",
+                           a2_resident=os.environ["OGCP_TMA"] == "2")
     if os.environ.get("OGCP_MERGE") == "0":  # A/B knob for the merged draws
         _lib.set_merge_draws(False)
     loss = P.make_loss("poisson")
