@@ -161,11 +161,7 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * mode 0 in order like the nonzero part; 0 keeps the draw order (lazy layout). */
 enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 3, OGCP_OPT_SHARD_SIM = 4,
        OGCP_OPT_SORT_ZEROS = 5, OGCP_OPT_LEAN_WALKS = 6, OGCP_OPT_TMA_WALKS = 7,
-       OGCP_OPT_BATCH_DRAWS = 8, OGCP_OPT_UMMA_GRAM = 9, OGCP_OPT_DETERMINISTIC = 10,
-       OGCP_OPT_PERSISTENT_SMALL = 11 };
-/* OGCP_OPT_PERSISTENT_SMALL (default 1): a temporal-row epoch whose draws were
- * batched (small draws, one GPU) runs as one cooperative launch: per iteration a
- * fixed-order grid sum and the fp64 Adam step, no host round trips. */
+       OGCP_OPT_BATCH_DRAWS = 8, OGCP_OPT_UMMA_GRAM = 9, OGCP_OPT_DETERMINISTIC = 10 };
 /* OGCP_OPT_DETERMINISTIC (default 0): for small models (sum of mode sizes x ldr
  * <= 4096, one GPU) the factor-gradient scatter adds in a fixed order (per-warp
  * shared-memory copies, groups in turn, fixed-order block and grid sums), so a

@@ -304,11 +304,6 @@ def set_deterministic(on: bool):
     check(lib().ogcp_ctx_set_option(ctx(), 10, int(bool(on))))
 
 
-def set_persistent_small(on: bool):
-    """Engine option OGCP_OPT_PERSISTENT_SMALL: one cooperative launch per small weight epoch."""
-    check(lib().ogcp_ctx_set_option(ctx(), 11, int(bool(on))))
-
-
 def set_split_scatter(on: bool):
     """Engine option OGCP_OPT_SPLIT_SCATTER for the current device's context."""
     check(lib().ogcp_ctx_set_option(ctx(), 2, int(bool(on))))

@@ -177,8 +177,6 @@ struct Ctx {
   bool deterministic = false;   // small models: fixed-order (bitwise reproducible) K3 scatter
   DevBuf det_partials;
   bool umma_gram = true;        // ldr 64 / 128 Grams on tcgen05 / TMEM (gram_umma.cuh)
-  bool persistent_small = true;  // small weight epochs: one cooperative launch per epoch
-  DevBuf wepoch_partials;
   bool batch_draws = true;      // small draws: every draw of a solver epoch made at its start (one launch per pass)
   bool sort_zeros = false;      // bucketed merged draws: zero rows sorted by (bucket, mode-0 row);
                                 // off: c4 measured +0.5 ms per draw for -0.3 ms of k_sgrad

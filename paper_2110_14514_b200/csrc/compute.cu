@@ -15,7 +15,6 @@
 // weight_gradient_mttkrp kernels.py:59-72; estimate_objective
 // sampling.py:177-206; gram kernels.py:75-98; _add_reg_and_history
 // solvers.py:159-179; Adam.step adam.py:51-81; _ensure_finite solvers.py:188-194.
-#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -1718,199 +1717,6 @@ static bool sgrad_det_enqueue(Ctx* ctx, const SamplesP& S, const ModelP& M, cons
     case 8: go(k_sgrad_det<2>); break;
     case 16: go(k_sgrad_det<4>); break;
     default: go(k_sgrad_det<8>); break;
-  }
-  ctx->count();
-  check_launch();
-  return true;
-}
-
-// ------------------------------------------------------------------ weight epoch, persistent (small draws)
-// A whole temporal-row epoch (tau iterations of K2w + the Adam step, solvers.py:
-// 240-262) in ONE cooperative launch for latency-bound shapes whose draws were made
-// at the epoch start (DrawBatchSet): per iteration every block sums its fixed share
-// of draw `it` into a fp64 partial, one grid-wide sync, then every block sums the
-// partials in block order and applies the identical Adam step to its shared-memory
-// copy of (s, u, v) -- no second sync (partials double-buffered by iteration
-// parity), no host round trip.  Replaces ~tau launch latencies per epoch.
-struct WEpoch {
-  const int32_t* ord;      // ordinals of draw b at ord + b p
-  int64_t p;
-  const int32_t* cand;     // zero rows of draw b at cand + b rows_max nd (lazy layout)
-  int64_t rows_max;
-  const long long* scal;   // draw b's scalar block (row count at + 8)
-  const int* rec;
-  int rec_ints;
-  double nz_scale, zero_scale;
-  int semi;
-  int iters;
-  int64_t i0;              // Adam iterations done before this epoch
-  double rate, b1, b2, eps, lower, mu;
-  long long ev0;           // event number of iteration 0 (error codes ev * 4 + k)
-  double* ws;              // s u v (s_o u_o v_o untouched)
-  float* s_f;
-  double* partials;        // [2][gridDim.x][ldr]
-};
-
-template <int G>
-__global__ void __launch_bounds__(kThreads) k_weight_epoch(WEpoch E, ModelP M, LossP L, DevFlags* flags) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double st_s[32], st_u[32], st_v[32];
-  __shared__ double red[kThreads / 32][32];
-  const int ldr = M.ldr, rank = M.rank, nd = M.ndim;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane / G, gl = lane % G;
-  constexpr int kGroups = 32 / G;
-  if (threadIdx.x < ldr) {
-    st_s[threadIdx.x] = E.ws[threadIdx.x];
-    st_u[threadIdx.x] = E.ws[ldr + threadIdx.x];
-    st_v[threadIdx.x] = E.ws[2 * ldr + threadIdx.x];
-  }
-  __syncthreads();
-  for (int it = 0; it < E.iters; ++it) {
-    const float4 s4 = make_float4((float)st_s[4 * gl], (float)st_s[4 * gl + 1], (float)st_s[4 * gl + 2],
-                                  (float)st_s[4 * gl + 3]);
-    const int32_t* ord = E.ord + (int64_t)it * E.p;
-    const int32_t* zs = E.cand + (int64_t)it * E.rows_max * nd;
-    const int64_t zrows = E.cand ? (int64_t)E.scal[16 * (int64_t)it + 8] : 0;
-    const int64_t total = E.p + zrows;
-    const int64_t per_blk = (total + gridDim.x - 1) / gridDim.x;
-    const int64_t blo = blockIdx.x * per_blk, bhi = min(total, blo + per_blk);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    unsigned bits = 0;
-    for (int64_t n0 = blo + (int64_t)warp * kGroups; n0 < bhi; n0 += (int64_t)(kThreads / 32) * kGroups) {
-      const int64_t n = n0 + grp;
-      bool valid = n < bhi;
-      bool nz = false;
-      int idx[kMaxModes];
-      float x = 0.f, scale = 0.f;
-      if (valid) {
-        if (n < E.p) {
-          nz = true;
-          const int* r = E.rec + (int64_t)__ldg(ord + n) * E.rec_ints;
-          for (int k = 0; k < nd; ++k) idx[k] = __ldg(r + k);
-          x = __int_as_float(__ldg(r + nd));
-          scale = (float)E.nz_scale;
-        } else {
-          const int32_t* z = zs + (n - E.p) * nd;
-          for (int k = 0; k < nd; ++k) idx[k] = __ldg(z + k);
-          valid = idx[0] >= 0;
-          scale = (float)E.zero_scale;
-        }
-      }
-      float4 pr = make_float4(1.f, 1.f, 1.f, 1.f);
-      for (int k = 0; k < nd; ++k) {
-        const float4 a = valid ? __ldg(reinterpret_cast<const float4*>(M.A[k] + (int64_t)idx[k] * ldr) + gl)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-        pr = mul4(pr, a);
-      }
-      float m = dot4(pr, s4);
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) m += __shfl_xor_sync(kFull, m, o);
-      if (valid) {
-        bits |= domain_bits(L.kind, m);
-        float y = dloss(L.kind, nz ? x : 0.f, m, L.eps);
-        if (E.semi && nz) y -= dloss(L.kind, 0.0f, m, L.eps);
-        y *= scale;
-        acc[0] += (double)(y * pr.x);
-        acc[1] += (double)(y * pr.y);
-        acc[2] += (double)(y * pr.z);
-        acc[3] += (double)(y * pr.w);
-      }
-    }
-    if (bits) report(flags, kFlagData, (E.ev0 + it) * 4 + 1, bits);
-    // groups of the warp (same columns) in fixed order, then warps in order
-#pragma unroll
-    for (int o = G; o < 32; o <<= 1)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[e] += __shfl_xor_sync(kFull, acc[e], o);
-    if (lane < G) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) red[warp][4 * lane + e] = acc[e];
-    }
-    __syncthreads();
-    double* part = E.partials + ((int64_t)(it & 1) * gridDim.x + blockIdx.x) * ldr;
-    if (threadIdx.x < ldr) {
-      double t = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) t += red[w][threadIdx.x];
-      part[threadIdx.x] = t;
-    }
-    grid.sync();
-    // every block: the same fixed-order sum and the same fp64 Adam step (adam.py:51-81)
-    if (threadIdx.x < ldr) {
-      const int r = threadIdx.x;
-      const double* pp = E.partials + (int64_t)(it & 1) * gridDim.x * ldr;
-      double g = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) g += pp[(int64_t)b * ldr + r];
-      if (r < rank) {
-        const double cnt = (double)(E.i0 + it + 1);
-        const double rate_i = E.rate * sqrt(1.0 - pow(E.b2, cnt)) / (1.0 - pow(E.b1, cnt));
-        const double s = st_s[r];
-        g += E.mu * s;
-        const double u = E.b1 * st_u[r] + (1.0 - E.b1) * g;
-        const double v = E.b2 * st_v[r] + (1.0 - E.b2) * g * g;
-        double sn = s - rate_i * u / (sqrt(v) + E.eps);
-        if (sn < E.lower) sn = E.lower;
-        st_s[r] = sn;
-        st_u[r] = u;
-        st_v[r] = v;
-        if (blockIdx.x == 0 && (!isfinite(sn) || !isfinite((float)sn)))
-          report(flags, kFlagDiverge, (E.ev0 + it) * 4 + 2, 0);
-      } else {
-        st_s[r] = 0.0;
-      }
-    }
-    __syncthreads();
-  }
-  if (blockIdx.x == 0 && threadIdx.x < ldr) {
-    const int r = threadIdx.x;
-    E.ws[r] = st_s[r];
-    E.ws[ldr + r] = st_u[r];
-    E.ws[2 * ldr + r] = st_v[r];
-    E.s_f[r] = r < rank ? (float)st_s[r] : 0.f;
-  }
-}
-
-bool weight_epoch_enqueue(Ctx* ctx, const WEpochArgs& a, const ModelP& M, const LossP& L) {
-  if (!ctx->persistent_small || M.ldr > 32 || M.ndim > kMaxModes || a.semi_unsupported) return false;
-  WEpoch E;
-  E.ord = a.ord;
-  E.p = a.p;
-  E.cand = a.cand;
-  E.rows_max = a.rows_max;
-  E.scal = a.scal;
-  E.rec = a.rec;
-  E.rec_ints = a.rec_ints;
-  E.nz_scale = a.nz_scale;
-  E.zero_scale = a.zero_scale;
-  E.semi = a.semi;
-  E.iters = a.iters;
-  E.i0 = a.i0;
-  E.rate = a.rate;
-  E.b1 = a.b1;
-  E.b2 = a.b2;
-  E.eps = a.eps;
-  E.lower = a.lower;
-  E.mu = a.mu;
-  E.ev0 = a.ev0;
-  E.ws = a.ws;
-  E.s_f = a.s_f;
-  DevFlags* fl = ctx->flags.as<DevFlags>();
-  void* args[] = {&E, const_cast<ModelP*>(&M), const_cast<LossP*>(&L), &fl};
-  auto go = [&](auto kern) {
-    int per_sm = 0;
-    OGCP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
-    const int64_t total = a.p + a.rows_max;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 511) / 512, (int64_t)kNumSMs * per_sm));
-    E.partials = static_cast<double*>(ctx->wepoch_partials.ensure((size_t)2 * grid * M.ldr * 8));
-    ProfScope prof_scope(ctx, kProfWgrad);
-    OGCP_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, kThreads, args, 0, ctx->stream));
-  };
-  switch (M.ldr) {
-    case 4: go(k_weight_epoch<1>); break;
-    case 8: go(k_weight_epoch<2>); break;
-    case 16: go(k_weight_epoch<4>); break;
-    default: go(k_weight_epoch<8>); break;
   }
   ctx->count();
   check_launch();

@@ -58,28 +58,6 @@ struct WStep {
   long long code;
   unsigned int* ticket;
 };
-// A whole temporal-row epoch on batched small draws in one cooperative launch
-// (compute.cu k_weight_epoch); false when not applicable (the caller then runs
-// the per-iteration launches).
-struct WEpochArgs {
-  const int32_t* ord;
-  int64_t p;
-  const int32_t* cand;
-  int64_t rows_max;
-  const long long* scal;
-  const int* rec;
-  int rec_ints;
-  double nz_scale, zero_scale;
-  int semi;
-  bool semi_unsupported;
-  int iters;
-  int64_t i0;
-  double rate, b1, b2, eps, lower, mu;
-  long long ev0;
-  double* ws;
-  float* s_f;
-};
-bool weight_epoch_enqueue(Ctx* ctx, const WEpochArgs& a, const ModelP& M, const LossP& L);
 // K2 (weight solve): per-block partial sums of Z'vec(Y) into partials [nblk x ldr] double.
 // With `step`, the walk kernel also applies the weight step when it can (*stepped
 // tells whether it did; otherwise the caller runs weight_step_enqueue).

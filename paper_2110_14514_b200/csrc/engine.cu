@@ -384,13 +384,6 @@ struct DrawPipe {
     ctx->stream = main;
     OGCP_CUDA(cudaEventRecord(done[slot], side));
   }
-  SamplesP batch_set(int b) const {
-    const int32_t* ord = batch.p ? batch.ord.as<int32_t>() + (int64_t)b * batch.p : nullptr;
-    const int32_t* zs = batch.q ? batch.cand.as<int32_t>() + (int64_t)b * batch.rows_max * bX->ndim : nullptr;
-    SamplesP Sb = semi_of(bX, samples_of(bX, ord, batch.p, zs, batch.q), buf[0].semi);
-    Sb.q_dev = batch.q ? batch.scal.as<long long>() + (int64_t)b * 16 + 8 : nullptr;
-    return Sb;
-  }
   SamplesP take(Ctx* ctx, int slot) {
     if (batched) {
       const int b = bnext++;
@@ -732,36 +725,7 @@ static void solve_weights_impl(Ctx* ctx, const Slice* X, const ogcp_solver_confi
       if (!dense)
         grad.begin_epoch(ctx, X, [&](int it) { return keyed(seed, {t, 1, epoch, it}); }, cfg->iters_weights, budget,
                          code_of(ev0, 0));
-      bool persistent = false;
-      if (!dense && grad.batched && ctx->world == 1) {  // the whole epoch in one cooperative launch
-        const SamplesP S0 = grad.batch_set(0);
-        WEpochArgs a{};
-        a.ord = S0.ord;
-        a.p = grad.batch.p;
-        a.cand = grad.batch.q ? grad.batch.cand.as<int32_t>() : nullptr;
-        a.rows_max = grad.batch.rows_max;
-        a.scal = grad.batch.scal.as<long long>();
-        a.rec = S0.rec;
-        a.rec_ints = S0.rec_ints;
-        a.nz_scale = S0.nz_scale;
-        a.zero_scale = S0.zero_scale;
-        a.semi = S0.semi;
-        a.semi_unsupported = false;
-        a.iters = cfg->iters_weights;
-        a.i0 = i;
-        a.rate = rate;
-        a.b1 = cfg->beta1;
-        a.b2 = cfg->beta2;
-        a.eps = cfg->adam_eps;
-        a.lower = cfg->lower_bound;
-        a.mu = cfg->reg_weights;
-        a.ev0 = ev0;
-        a.ws = ws;
-        a.s_f = s_f;
-        persistent = weight_epoch_enqueue(ctx, a, M, L);
-        if (persistent) ev += cfg->iters_weights;
-      }
-      for (int it = 0; it < (persistent ? 0 : cfg->iters_weights); ++it) {
+      for (int it = 0; it < cfg->iters_weights; ++it) {
         const long long e = ev++;
         const int64_t cnt = i + it + 1;
         const double rate_i = rate * std::sqrt(1.0 - std::pow(cfg->beta2, (double)cnt)) /
@@ -1529,7 +1493,6 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   else if (option == OGCP_OPT_BATCH_DRAWS) ctx->batch_draws = value != 0;
   else if (option == OGCP_OPT_UMMA_GRAM) ctx->umma_gram = value != 0;
   else if (option == OGCP_OPT_DETERMINISTIC) ctx->deterministic = value != 0;
-  else if (option == OGCP_OPT_PERSISTENT_SMALL) ctx->persistent_small = value != 0;
   else if (option == OGCP_OPT_LEAN_WALKS) ctx->lean_walks = value != 0;
   else if (option == OGCP_OPT_TMA_WALKS) {
     ctx->tma_walks = (value & 1) != 0;
