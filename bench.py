@@ -342,8 +342,8 @@ def main():
         _lib.set_split_scatter(True)
     if os.environ.get("OGCP_BUCKETS"):  # A/B knob for the bucketed merged walk: 0 off, k > 1 forces k buckets
         _lib.set_buckets(int(os.environ["OGCP_BUCKETS"]))
-    if os.environ.get("OGCP_SORT_ZEROS"):  # A/B knob for the sorted zero rows
-        _lib.set_sort_zeros(os.environ["OGCP_SORT_ZEROS"] == "1")
+    if os.environ.get("OGCP_SORT_ZEROS"):  # A/B knob for the sorted zero rows (0, 1, 2 = bucket only)
+        _lib.set_sort_zeros(int(os.environ["OGCP_SORT_ZEROS"]))
     if os.environ.get("OGCP_LEAN"):  # A/B knob for the register-pipelined 3-way walk kernels
         _lib.set_lean_walks(os.environ["OGCP_LEAN"] == "1")
     if os.environ.get("OGCP_TMA"):  # A/B knob for the TMA-fed 3-way walks (0 off, 1 on, 2 + A2 residency, 3 + weight walk)

@@ -264,9 +264,10 @@ def debug_solve_draw(X, seed: int, key, p, q: int, ldr: int, max_rejects=None):
     return ords[:nn.value].astype(np.int64), cnts[:nn.value].astype(np.int64), zeros[:nz.value].astype(np.int64)
 
 
-def set_sort_zeros(on: bool):
-    """Engine option OGCP_OPT_SORT_ZEROS: zero rows of bucketed merged draws in walk order."""
-    check(lib().ogcp_ctx_set_option(ctx(), 5, int(bool(on))))
+def set_sort_zeros(mode):
+    """Engine option OGCP_OPT_SORT_ZEROS: zero rows of bucketed merged draws in walk order
+    (0 off, 1 / True by (bucket, mode-0 row), 2 by bucket only)."""
+    check(lib().ogcp_ctx_set_option(ctx(), 5, int(mode)))
 
 
 def set_lean_walks(on: bool):

@@ -178,7 +178,8 @@ struct Ctx {
   DevBuf det_partials;
   bool umma_gram = true;        // ldr 64 / 128 Grams on tcgen05 / TMEM (gram_umma.cuh)
   bool batch_draws = true;      // small draws: every draw of a solver epoch made at its start (one launch per pass)
-  bool sort_zeros = false;      // bucketed merged draws: zero rows sorted by (bucket, mode-0 row);
+  int sort_zeros = 0;           // bucketed merged draws: zero rows sorted by (bucket, mode-0 row) [1] or
+                                // by bucket only [2];
                                 // off: c4 measured +0.5 ms per draw for -0.3 ms of k_sgrad
   bool lean_walks = false;      // walk3.cuh kernels for merged 3-way sets (register-pipelined)
   bool tma_walks = true;        // walk_tma.cuh K3 walk for merged 3-way sets (TMA gather4, warp-specialised)

@@ -1489,7 +1489,7 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   OGCP_API_BEGIN
   if (option == OGCP_OPT_MERGE_DRAWS) ctx->merge_draws = value != 0;
   else if (option == OGCP_OPT_SPLIT_SCATTER) ctx->split_scatter = value != 0;
-  else if (option == OGCP_OPT_SORT_ZEROS) ctx->sort_zeros = value != 0;
+  else if (option == OGCP_OPT_SORT_ZEROS) ctx->sort_zeros = (int)std::min<int64_t>(std::max<int64_t>(value, 0), 2);
   else if (option == OGCP_OPT_BATCH_DRAWS) ctx->batch_draws = value != 0;
   else if (option == OGCP_OPT_UMMA_GRAM) ctx->umma_gram = value != 0;
   else if (option == OGCP_OPT_DETERMINISTIC) ctx->deterministic = value != 0;

@@ -1098,7 +1098,8 @@ static const int32_t* sort_zero_rows(Ctx* ctx, const Slice* X, DrawScratch& scr,
   const int d = X->ndim;
   const int nbb = bits_for(X->nbuckets);
   const int i0b = bits_for(X->dims[0]);
-  const int b0 = std::min(i0b, 30 - nbb);
+  // sort_zeros 2: bucket only (a one-digit radix pass); 1: bucket, then mode-0 row
+  const int b0 = ctx->sort_zeros == 2 ? 0 : std::min(i0b, 30 - nbb);
   const int s0 = i0b - b0;
   const int kb = nbb + b0;
   scr.zkey.ensure((size_t)rows * 4);
@@ -1331,7 +1332,7 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
       k_zero_locate<<<1, kScanThreads, 0, s>>>(scr.zcount.as<uint32_t>(), scr.zoff.as<long long>(), zblocks,
                                                scr.miss.as<uint8_t>(), rows_max, q, sc + 8, z_hits_before);
       ctx->count();
-      if (merged && merged->perm && ctx->sort_zeros && X->bucket_mode > 0 && q >= 65536 && rows_max < INT32_MAX) {
+      if (merged && merged->perm && ctx->sort_zeros > 0 && X->bucket_mode > 0 && q >= 65536 && rows_max < INT32_MAX) {
         out.zsub = sort_zero_rows(ctx, X, scr, rows_max, q, sc + 8);  // exactly q rows, walk order
         out.q_dev = nullptr;
       } else {
