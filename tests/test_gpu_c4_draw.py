@@ -91,3 +91,37 @@ def test_c4_merged_counts_equal_bincount(c4, buckets, sort_zeros):
         key = (zeros[:, 1] * buckets // DIMS[1]) * DIMS[0] + zeros[:, 0]
         zeros = zeros[np.argsort(key, kind="stable")]
     assert np.array_equal(z, zeros)
+
+
+def test_c4_factor_gradient_tma_walk_matches_generic(c4):
+    """The bench-scale K3 walk: one factor iteration at rate ~0 (u = (1 - b1) g) on the c4
+    slice (p = all, q = 2^24, R = 32, row-bucketed merged set) with the TMA-fed
+    warp-specialised walk (csrc/walk_tma.cuh) and with the generic sample kernels gives
+    the same factor gradients (fp32 reduction order only), and the weight gradient of the
+    same draw matches too."""
+    from paper_2110_14514_b200.solvers import solve_factors_device, solve_weights_device
+    X, _ = c4
+    R = 32
+    rng = np.random.default_rng(3)
+    init = [rng.uniform(0.5, 1.5, (d, R)) / np.sqrt(d) for d in DIMS]
+    w = np.full(R, 2.0)
+    cfg = P.SolverConfig(max_epochs_factors=1, iters_factors=1, rate_factors=1e-30,
+                         samples=P.SamplerConfig(None, Q, 1 << 20, 1 << 20, seed=9))
+    loss = P.make_loss("poisson")
+
+    def u_of(impl):
+        _lib.set_walk_impl(impl)
+        try:
+            model = P.DeviceModel.from_numpy(init)
+            adam = cfg.make_adam(cfg.rate_factors, loss)
+            adam.init_device(model.dims, model.rank)
+            solve_factors_device(X, model, w, None, [], cfg, loss, adam, 0, 1)
+            out = [t[:, :R].double().cpu().numpy() for t in adam._buf["u"]]
+            del model, adam
+            return out
+        finally:
+            _lib.set_walk_impl("tma")
+
+    a, b = u_of("tma"), u_of("generic")
+    for k in range(3):
+        assert np.linalg.norm(a[k] - b[k]) <= 1e-5 * np.linalg.norm(b[k]), k

@@ -284,3 +284,24 @@ def test_tensor_core_grams_vs_oracle(R, umma):
             assert rel_err(P.gram(A, mode, other_factors=B), O.hadamard_gram(A, mode, B)) < 1e-5
     finally:
         _lib.set_umma_gram(True)
+
+
+
+def test_tcgen05_gram_at_c5_scale():
+    """The tcgen05 / TMEM Gram at the c5 shape (100K rows, ldr 128: 3125 32-row chunks over
+    148 CTAs) against the mma.sync kernel and fp64 numpy (norm-wise 1e-5)."""
+    from paper_2110_14514_b200 import _lib
+    rng = np.random.default_rng(128)
+    A = rng.uniform(-1, 1, (100_000, 128))
+    B = A + 0.05 * rng.uniform(-1, 1, A.shape)
+    want_p, want_c = A.T @ A, B.T @ A
+    out = {}
+    for umma in (True, False):
+        _lib.set_umma_gram(umma)
+        try:
+            out[umma] = (P.gram([A], None), P.gram([A], None, other_factors=[B]))
+        finally:
+            _lib.set_umma_gram(True)
+    for umma in (True, False):
+        assert rel_err(out[umma][0], want_p) < 1e-5
+        assert rel_err(out[umma][1], want_c) < 1e-5
