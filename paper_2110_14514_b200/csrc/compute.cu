@@ -941,8 +941,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_gram_tc(const float* __restrict
 // shared-memory latency instead of a dependent global load per row (c2: 41 us ->
 // a few us per launch; the Grams were the longest kernel of a c2 iteration).
 constexpr int kGramSmallRows = 64;
+__device__ __forceinline__ void hist_coeffs_body(int ndim, int rank, const double* P, const double* C,
+                                                 const double* S, double w, const double* s, double extra, float* Mk,
+                                                 float* Nk) {
+  const int RR = rank * rank;
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+    const double se = S ? w * S[e] : 0.0;
+    const double me = se + (s ? extra * s[e / rank] * s[e % rank] : 0.0);
+    for (int k = 0; k < ndim; ++k) {
+      double gp = 1.0, gc = 1.0;
+      for (int m = 0; m < ndim; ++m) {
+        if (m == k) continue;
+        gp *= P[(int64_t)m * RR + e];
+        if (C) gc *= C[(int64_t)m * RR + e];
+      }
+      Mk[(int64_t)k * RR + e] = (float)(gp * me);
+      Nk[(int64_t)k * RR + e] = C ? (float)(gc * se) : 0.f;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_gram_small(SmallGrams g, int rank, int ldr, double* __restrict__ out1,
-                                                         double* __restrict__ out2) {
+                                                         double* __restrict__ out2, CoeffTail tail) {
   __shared__ float sA[kGramSmallRows * 32], sB1[kGramSmallRows * 32], sB2[kGramSmallRows * 32];
   const int k = blockIdx.y;
   const int RR = rank * rank;
@@ -993,11 +1013,25 @@ __global__ void __launch_bounds__(kThreads) k_gram_small(SmallGrams g, int rank,
     out1[(int64_t)k * RR + e] = s1[t][0] + s1[t][1];
     if (B2) out2[(int64_t)k * RR + e] = s2[t][0] + s2[t][1];
   }
+  if (tail.ticket) {  // the last mode-block also computes every mode's history coefficients
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(tail.ticket, 1u) == gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    hist_coeffs_body(gridDim.y, rank, out1, out2, tail.S, tail.w, tail.s, tail.extra, tail.Mk, tail.Nk);
+    if (threadIdx.x == 0) *tail.ticket = 0u;
+  }
 }
 
-void gram_small_enqueue(Ctx* ctx, const SmallGrams& g, int ndim, int rank, int ldr, double* out1, double* out2) {
+void gram_small_enqueue(Ctx* ctx, const SmallGrams& g, int ndim, int rank, int ldr, double* out1, double* out2,
+                        const CoeffTail* tail) {
   ProfScope prof_scope(ctx, kProfGram);
-  k_gram_small<<<dim3(1, ndim), kThreads, 0, ctx->stream>>>(g, rank, ldr, out1, out2);
+  CoeffTail t{};
+  if (tail) t = *tail;
+  k_gram_small<<<dim3(1, ndim), kThreads, 0, ctx->stream>>>(g, rank, ldr, out1, out2, t);
   ctx->count();
   check_launch();
 }
@@ -1029,21 +1063,7 @@ __global__ void k_gram_finalize(const T* __restrict__ partials, int nblk, int ng
 __global__ void k_hist_coeffs(int ndim, int rank, const double* __restrict__ P, const double* __restrict__ C,
                               const double* __restrict__ S, double w, const double* __restrict__ s, double extra,
                               float* __restrict__ Mk, float* __restrict__ Nk) {
-  const int RR = rank * rank;
-  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
-    const double se = S ? w * S[e] : 0.0;
-    const double me = se + (s ? extra * s[e / rank] * s[e % rank] : 0.0);
-    for (int k = 0; k < ndim; ++k) {
-      double gp = 1.0, gc = 1.0;
-      for (int m = 0; m < ndim; ++m) {
-        if (m == k) continue;
-        gp *= P[(int64_t)m * RR + e];
-        if (C) gc *= C[(int64_t)m * RR + e];
-      }
-      Mk[(int64_t)k * RR + e] = (float)(gp * me);
-      Nk[(int64_t)k * RR + e] = C ? (float)(gc * se) : 0.f;
-    }
-  }
+  hist_coeffs_body(ndim, rank, P, C, S, w, s, extra, Mk, Nk);
 }
 
 // Dense-Gaussian weight gradient without the mu term (solvers.py:182-185):

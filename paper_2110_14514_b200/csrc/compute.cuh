@@ -89,7 +89,19 @@ struct SmallGrams {
   const float* B2[kMaxModes];  // nullable
   int64_t rows[kMaxModes];
 };
-void gram_small_enqueue(Ctx* ctx, const SmallGrams& g, int ndim, int rank, int ldr, double* out1, double* out2);
+// Optional tail of the small-model Gram launch: the last mode-block to finish
+// also computes the history coefficients of every mode (k_hist_coeffs' arithmetic).
+struct CoeffTail {
+  const double* S;   // nullable
+  double w;
+  const double* s;   // nullable (dense-Gaussian model term)
+  double extra;
+  float* Mk;
+  float* Nk;
+  unsigned int* ticket;  // nullptr: no tail
+};
+void gram_small_enqueue(Ctx* ctx, const SmallGrams& g, int ndim, int rank, int ldr, double* out1, double* out2,
+                        const CoeffTail* tail = nullptr);
 struct K5Modes {
   float* A[kMaxModes];
   const float* Aold[kMaxModes];

@@ -927,7 +927,19 @@ static void factor_iteration(Ctx* ctx, const Slice* X, const ModelP& M, float* c
   if (rowshard) comm_reduce_rows(ctx, gp, M.dims, M.ndim, M.ldr);
   else comm_allreduce_sum(ctx, W.grads.as<float>(), off);
   const bool coeffs = hist || dense;
-  if (coeffs) {
+  if (coeffs && hist && small_model(M) && !rowshard) {
+    // small models: the history coefficients run in the tail of the Gram launch
+    SmallGrams g{};
+    for (int k = 0; k < M.ndim; ++k) {
+      g.A[k] = M.A[k];
+      g.B1[k] = M.A[k];
+      g.B2[k] = old_factors[k];
+      g.rows[k] = M.dims[k];
+    }
+    CoeffTail tail{W.hb.S.as<double>(), cfg->hist_weight, dense_s, 2.0, W.hb.Mk.as<float>(), W.hb.Nk.as<float>(),
+                   ctx->wticket() + 2};
+    gram_small_enqueue(ctx, g, M.ndim, M.rank, M.ldr, W.hb.P.as<double>(), W.hb.C.as<double>(), &tail);
+  } else if (coeffs) {
     if (hist) grams_pc_enqueue(ctx, M, old_factors, W.hb, true);
     else grams_enqueue(ctx, M, nullptr, W.hb.P.as<double>(), W.hb, true, true);
     hist_coeffs_enqueue(ctx, M.ndim, M.rank, W.hb.P.as<double>(), hist ? W.hb.C.as<double>() : nullptr,
