@@ -403,7 +403,10 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6553.3))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6553.3 GB/s"
     sg = prof["sgrad"]
-    sg_ms = sg["ms"] / max(sg["launches"], 1)  # one K3 walk per factor iteration (its launches bracketed together)
+    # one K3 walk per factor iteration; a walk is two launches (merged nonzeros, zero stratum),
+    # each bracketed on its own, so the per-walk time is the bracket total over the iterations
+    walks = sum(m.epochs_factors * cfg.iters_factors for m in st.metrics if m.t > t_first)
+    sg_ms = sg["ms"] / max(walks, 1)
     # Algorithmic bytes per walk = B_f x |Y|, |Y| = entries of the merged sampled gradient tensor
     # (sampling.py:233-239): distinct nonzero ordinals among p draws with replacement (expected
     # eta*(1-(1-1/eta)^p), sd ~ 5e3 at c4) plus the q zero draws (distinct w.p. ~1 at omega = 1e15).
@@ -479,6 +482,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "K3 walk (k_walk_tma: merged nonzeros + zero stratum, TMA-fed)",
                          "algorithmic_bytes_per_launch": sg_bytes, "avg_launch_ms": sg_ms,
+                         "launch_unit": "one K3 walk = its two launches (k_walk_tma nonzero + zero stratum)",
                          "bytes_model": "B_f = 8dR+4d+4 = 784 B per entry of the merged gradient tensor Y; "
                                         f"|Y| = {y_entries:.4g} (distinct nonzero draws + zero draws)",
                          # three honest denominators: the SURVEY 8(d) byte model counts row gathers
