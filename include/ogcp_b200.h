@@ -161,7 +161,16 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * mode 0 in order like the nonzero part; 0 keeps the draw order (lazy layout). */
 enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 3, OGCP_OPT_SHARD_SIM = 4,
        OGCP_OPT_SORT_ZEROS = 5, OGCP_OPT_LEAN_WALKS = 6, OGCP_OPT_TMA_WALKS = 7,
-       OGCP_OPT_BATCH_DRAWS = 8, OGCP_OPT_UMMA_GRAM = 9, OGCP_OPT_DETERMINISTIC = 10 };
+       OGCP_OPT_BATCH_DRAWS = 8, OGCP_OPT_UMMA_GRAM = 9, OGCP_OPT_DETERMINISTIC = 10,
+       OGCP_OPT_SHARD_DRAWS = 11 };
+/* OGCP_OPT_SHARD_DRAWS (default 1): in a multi-GPU solve (2..8 ranks) the merged
+ * gradient draws of slices whose modes all exceed 1 are sharded by RNG word
+ * range -- each rank generates 1/world of the words; tile maps, per-rank zero-row
+ * records and the nibble counters (reduce-scattered to the ordinal owners) are
+ * exchanged on a second communicator -- so no rank replays the whole stream; 0
+ * keeps every rank generating every word.  In shard simulation (OGCP_OPT_SHARD_SIM)
+ * 1 runs every rank's part on this GPU with exact device-side exchanges; 2 runs
+ * only this rank's part, its own slots standing in for the others' (timing). */
 /* OGCP_OPT_DETERMINISTIC (default 0): for small models (sum of mode sizes x ldr
  * <= 4096, one GPU) the factor-gradient scatter adds in a fixed order (per-warp
  * shared-memory copies, groups in turn, fixed-order block and grid sums), so a

@@ -264,6 +264,13 @@ def debug_solve_draw(X, seed: int, key, p, q: int, ldr: int, max_rejects=None):
     return ords[:nn.value].astype(np.int64), cnts[:nn.value].astype(np.int64), zeros[:nz.value].astype(np.int64)
 
 
+def set_shard_draws(mode):
+    """Engine option OGCP_OPT_SHARD_DRAWS: multi-GPU merged draws sharded by RNG word range
+    (0 off: every rank replays the whole stream; 1 on; 2 on, shard simulation runs only this
+    rank's part -- timing)."""
+    check(lib().ogcp_ctx_set_option(ctx(), 11, int(mode)))
+
+
 def set_sort_zeros(mode):
     """Engine option OGCP_OPT_SORT_ZEROS: zero rows of bucketed merged draws in walk order
     (0 off, 1 / True by (bucket, mode-0 row), 2 by bucket only)."""

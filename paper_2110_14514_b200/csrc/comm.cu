@@ -38,6 +38,7 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -61,6 +62,7 @@ NcclApi& api() {
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.lib, "ncclGroupStart"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.lib, "ncclGroupEnd"));
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.lib, "ncclCommDestroy"));
+    a.CommSplit = reinterpret_cast<decltype(a.CommSplit)>(dlsym(a.lib, "ncclCommSplit"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(a.lib, "ncclGetErrorString"));
   });
   if (!a.lib || !a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.Reduce || !a.Broadcast || !a.GroupStart ||
@@ -164,6 +166,34 @@ void comm_sync_flags(Ctx* ctx) {
   check_launch();
 }
 
+// ---- sharded draws (sampler.cu shard_draw_enqueue): a second communicator, so the
+// draw's collectives on the side stream never interleave with the solve's on the
+// context stream within one communicator
+void comm_draw_group(Ctx* ctx, bool begin) {
+  if (!ctx->comm_draw) return;
+  nccl_check(begin ? api().GroupStart() : api().GroupEnd(), "ncclGroup");
+}
+
+void comm_draw_allgather(Ctx* ctx, void* buf, size_t bytes) {
+  if (!ctx->comm_draw || bytes == 0) return;
+  char* b = static_cast<char*>(buf);
+  nccl_check(api().AllGather(b + bytes * ctx->rank, b, bytes, ncclUint8, (ncclComm_t)ctx->comm_draw, ctx->stream),
+             "ncclAllGather");
+}
+
+void comm_draw_reduce_scatter_u32(Ctx* ctx, uint32_t* buf, size_t words) {
+  if (!ctx->comm_draw || words == 0) return;
+  nccl_check(api().ReduceScatter(buf, buf + words * ctx->rank, words, ncclUint32, ncclSum,
+                                 (ncclComm_t)ctx->comm_draw, ctx->stream),
+             "ncclReduceScatter");
+}
+
+void comm_draw_allreduce_u64(Ctx* ctx, unsigned long long* buf, size_t n) {
+  if (!ctx->comm_draw || n == 0) return;
+  nccl_check(api().AllReduce(buf, buf, n, ncclUint64, ncclSum, (ncclComm_t)ctx->comm_draw, ctx->stream),
+             "ncclAllReduce");
+}
+
 void comm_init(Ctx* ctx, const uint8_t* id, int rank, int world) {
   if (world < 1 || rank < 0 || rank >= world) throw Error(OGCP_E_USAGE, "bad rank / world size");
   if (world == 1) {
@@ -178,6 +208,12 @@ void comm_init(Ctx* ctx, const uint8_t* id, int rank, int world) {
   OGCP_CUDA(cudaSetDevice(ctx->device));
   nccl_check(api().CommInitRank(&comm, world, uid, rank), "ncclCommInitRank");
   ctx->comm = comm;
+  ctx->comm_draw = nullptr;  // without ncclCommSplit (NCCL < 2.18) the draws stay replicated
+  if (api().CommSplit) {
+    ncclComm_t dc = nullptr;
+    nccl_check(api().CommSplit(comm, 0, rank, &dc, nullptr), "ncclCommSplit");
+    ctx->comm_draw = dc;
+  }
   ctx->rank = rank;
   ctx->world = world;
 }
@@ -199,7 +235,7 @@ int comm_selftest(Ctx* ctx) {
   ncclComm_t comm;
   nccl_check(api().CommInitRank(&comm, 1, uid, 0), "ncclCommInitRank");
   DevBuf buf;
-  char* d = static_cast<char*>(buf.ensure(256));
+  char* d = static_cast<char*>(buf.ensure(512));
   const float hf[4] = {1.5f, -2.f, 3.25f, 0.f};
   const double hd[2] = {1e300, -7.5};
   const long long hl[4] = {5, -3, 1LL << 40, 0};
@@ -217,7 +253,27 @@ int comm_selftest(Ctx* ctx) {
   nccl_check(api().ReduceScatter(d, d, 2, ncclFloat32, ncclSum, comm, st), "ncclReduceScatter");
   nccl_check(api().AllGather(d + 8, d + 8, 2, ncclFloat32, comm, st), "ncclAllGather");
   nccl_check(api().GroupEnd(), "ncclGroupEnd");
+  // the sharded draws' collectives on a split communicator: uint8 all-gather,
+  // uint32 reduce-scatter and uint64 all-reduce (one group)
+  ncclComm_t dc = nullptr;
+  const uint32_t hu[2] = {0x12345678u, 7u};
+  const unsigned long long hq[2] = {1ull << 40, 3ull};
+  OGCP_CUDA(cudaMemcpy(d + 192, hu, sizeof(hu), cudaMemcpyHostToDevice));
+  OGCP_CUDA(cudaMemcpy(d + 208, hq, sizeof(hq), cudaMemcpyHostToDevice));
+  if (api().CommSplit) {
+    nccl_check(api().CommSplit(comm, 0, 0, &dc, nullptr), "ncclCommSplit");
+    nccl_check(api().GroupStart(), "ncclGroupStart");
+    nccl_check(api().AllGather(d + 192, d + 192, 4, ncclUint8, dc, st), "ncclAllGather");
+    nccl_check(api().ReduceScatter(d + 192, d + 192, 2, ncclUint32, ncclSum, dc, st), "ncclReduceScatter");
+    nccl_check(api().AllReduce(d + 208, d + 208, 2, ncclUint64, ncclSum, dc, st), "ncclAllReduce");
+    nccl_check(api().GroupEnd(), "ncclGroupEnd");
+  }
   OGCP_CUDA(cudaStreamSynchronize(st));
+  uint32_t ru[2];
+  unsigned long long rq[2];
+  OGCP_CUDA(cudaMemcpy(ru, d + 192, sizeof(ru), cudaMemcpyDeviceToHost));
+  OGCP_CUDA(cudaMemcpy(rq, d + 208, sizeof(rq), cudaMemcpyDeviceToHost));
+  if (dc && api().CommDestroy) api().CommDestroy(dc);
   float rf[4];
   double rd[2];
   long long rl[4];
@@ -229,10 +285,15 @@ int comm_selftest(Ctx* ctx) {
   for (int i = 0; i < 4; ++i) bad += rf[i] != hf[i];
   for (int i = 0; i < 2; ++i) bad += rd[i] != hd[i];
   for (int i = 0; i < 4; ++i) bad += rl[i] != hl[i];
+  for (int i = 0; i < 2; ++i) bad += ru[i] != hu[i];
+  for (int i = 0; i < 2; ++i) bad += rq[i] != hq[i];
+  bad += api().CommSplit ? 0 : 1;  // the sharded draws need a second communicator
   return bad;
 }
 
 void comm_destroy(Ctx* ctx) {
+  if (ctx->comm_draw && api().CommDestroy) api().CommDestroy((ncclComm_t)ctx->comm_draw);
+  ctx->comm_draw = nullptr;
   if (ctx->comm && api().CommDestroy) api().CommDestroy((ncclComm_t)ctx->comm);
   ctx->comm = nullptr;
   ctx->world = 1;

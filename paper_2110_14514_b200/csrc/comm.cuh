@@ -17,6 +17,14 @@ void comm_gather_rows(Ctx* ctx, float* const* bufs, const int64_t* rows, int nbu
 // Make the device error word identical on every rank (min of first codes, OR of bits),
 // so every rank takes the same accept / reject / raise decision.
 void comm_sync_flags(Ctx* ctx);
+// Sharded-draw exchanges on the draw communicator (ctx->comm_draw) and ctx->stream:
+// in-place all-gather of per-rank slots of `bytes` each; in-place reduce-scatter of
+// uint32 sums (chunk r of `words` words lands on rank r); uint64 sum all-reduce.
+// begin/end bracket one NCCL group.
+void comm_draw_group(Ctx* ctx, bool begin);
+void comm_draw_allgather(Ctx* ctx, void* buf, size_t bytes);
+void comm_draw_reduce_scatter_u32(Ctx* ctx, uint32_t* buf, size_t words);
+void comm_draw_allreduce_u64(Ctx* ctx, unsigned long long* buf, size_t n);
 void comm_init(Ctx* ctx, const uint8_t* id, int rank, int world);
 void comm_unique_id(uint8_t* out128);
 void comm_destroy(Ctx* ctx);

@@ -191,6 +191,9 @@ struct Ctx {
   DevBuf ybuf;                  // per-sample y of the split scatter
   // multi-GPU: NCCL communicator over the ranks that share one stream of slices
   void* comm = nullptr;         // ncclComm_t
+  void* comm_draw = nullptr;    // ncclComm_t split from comm: the sharded draws' exchanges (side stream)
+  bool shard_draws = true;      // multi-GPU merged draws sharded by word range (sampler.cu shard_draw_enqueue)
+  bool shard_sim_timing = false;  // shard simulation of sharded draws: this rank's part only (timing)
   int rank = 0, world = 1;
   DevBuf flagpack;
   // scratch

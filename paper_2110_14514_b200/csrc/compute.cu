@@ -175,7 +175,9 @@ struct SampleStream {
     nd = D > 0 ? D : M_.ndim;
     int64_t lo = 0, hi = total;
     zoff = 0;
-    if (S.shard_world > 1 && S.zshard) {  // rank-owned merged nonzeros + a contiguous share of the zero rows
+    if (S.shard_world > 1 && S.zshard == 2) {
+      // word-sharded draw: rank-owned merged nonzeros and rank-local zero rows, all of them
+    } else if (S.shard_world > 1 && S.zshard == 1) {  // rank-owned merged nonzeros + a contiguous share of the zero rows
       const int64_t zrows = total - p;
       const int64_t zlo = zrows * S.shard_rank / S.shard_world, zhi = zrows * (S.shard_rank + 1) / S.shard_world;
       hi = p + (zhi - zlo);
@@ -1760,7 +1762,7 @@ static walk3::Walk<ZERO> walk_of(const SamplesP& S) {
   W.n_dev = ZERO ? S.q_dev : S.p_dev;
   W.n_host = ZERO ? S.q : S.p;
   W.shard_rank = S.shard_rank;
-  W.shard_world = ZERO && S.zshard ? S.shard_world : 1;
+  W.shard_world = ZERO && S.zshard == 1 ? S.shard_world : 1;
   return W;
 }
 

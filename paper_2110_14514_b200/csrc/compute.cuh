@@ -23,7 +23,8 @@ struct SamplesP {
   int shard_rank, shard_world;  // multi-GPU: this rank evaluates its contiguous 1/world of the samples
   int semi;                 // semi-stratified estimator: nonzero draws use g(x,m) - g(0,m); zero_scale = omega/q
   int chunk_shift;          // bucketed merged set: warps walk chunks of 2^chunk_shift batches round-robin
-  int zshard;               // multi-GPU merged set: the nonzero part is rank-owned; only zero rows are split
+  int zshard;               // multi-GPU merged set: the nonzero part is rank-owned; zero rows split
+                            // (1: a contiguous 1/world of [0, *q_dev)) or already rank-local (2: all of them)
 };
 
 struct GradPtrs {

@@ -199,11 +199,16 @@ static SamplesP semi_of(const Slice* X, SamplesP S, bool semi) {
   return S;
 }
 
-// Multi-GPU merged draws: rank r owns the nonzero ordinals [eta r / N, eta (r+1) / N)
-// and evaluates every merged sample there, plus a contiguous 1/N of the zero rows.
+// Multi-GPU merged draws: rank r owns the r-th chunk of whole nibble words of the
+// nonzero ordinals (shard_owner_range: [8 cw r, 8 cw (r+1)), cw = ceil(eta / 8 / N))
+// and evaluates every merged sample there, plus its share of the zero rows.
 static void owned_range(const Ctx* ctx, const Slice* X, int64_t* olo, int64_t* ohi) {
-  *olo = X->nnz * ctx->rank / ctx->world;
-  *ohi = X->nnz * (ctx->rank + 1) / ctx->world;
+  if (ctx->world <= 1) {
+    *olo = 0;
+    *ohi = X->nnz;
+    return;
+  }
+  shard_owner_range(X->nnz, ctx->rank, ctx->world, olo, ohi);
 }
 
 // Solve-time sample sets are evaluated sharded across the context's ranks.
@@ -270,6 +275,8 @@ struct SampleBufs {
   MergedDraw md;
   bool merged = false;
   bool owned = false;  // multi-GPU: the merged nonzero part is this rank's own ordinal range
+  bool word_sharded = false;  // multi-GPU: drawn by word range (shard_draw_enqueue); zero rows rank-local
+  ShardScratch sh;
   bool semi = false;  // semi-stratified extension
   const int32_t* zsub = nullptr;   // where the last draw left the zero coordinates
   const long long* q_dev = nullptr;  // lazy zero layout row count (device)
@@ -291,8 +298,11 @@ struct SampleBufs {
     md.olo = ctx->world > 1 ? (uint32_t)olo : 0u;
     md.ohi = ctx->world > 1 ? (uint32_t)ohi : 0u;
     owned = merged && ctx->world > 1;
-    const DrawOut o = draw_enqueue(ctx, X, g, p, q, budget, merged ? nullptr : ord.as<int32_t>(),
-                                   zero.as<int32_t>(), code, scr, merged ? &md : nullptr, /*lazy=*/true, semi);
+    word_sharded = owned && shard_draw_eligible(ctx, X, p, q, semi);
+    const DrawOut o = word_sharded ? shard_draw_enqueue(ctx, X, g, p, q, budget, code, md, sh)
+                                   : draw_enqueue(ctx, X, g, p, q, budget, merged ? nullptr : ord.as<int32_t>(),
+                                                  zero.as<int32_t>(), code, scr, merged ? &md : nullptr,
+                                                  /*lazy=*/true, semi);
     zsub = o.zsub;
     q_dev = o.q_dev;
     return sample_set(X);
@@ -308,7 +318,7 @@ SamplesP SampleBufs::sample_set(const Slice* X) const {
   }
   SamplesP S = semi_of(X, samples_of(X, md.ord.as<int32_t>(), p, zsub, q), semi);
   S.q_dev = q_dev;
-  S.zshard = owned ? 1 : 0;
+  S.zshard = word_sharded ? 2 : (owned ? 1 : 0);
   if (md.perm) {  // positions into the bucketed copy, walked in round-robin chunks
     S.rec = X->rec_b.as<int>();
     S.chunk_shift = 3;  // 8 batches per chunk (measured flat for shifts 2..6 on c4)
@@ -1506,6 +1516,10 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   else if (option == OGCP_OPT_UMMA_GRAM) ctx->umma_gram = value != 0;
   else if (option == OGCP_OPT_DETERMINISTIC) ctx->deterministic = value != 0;
   else if (option == OGCP_OPT_LEAN_WALKS) ctx->lean_walks = value != 0;
+  else if (option == OGCP_OPT_SHARD_DRAWS) {
+    ctx->shard_draws = value != 0;
+    ctx->shard_sim_timing = value == 2;
+  }
   else if (option == OGCP_OPT_TMA_WALKS) {
     ctx->tma_walks = (value & 1) != 0;
     ctx->tma_wgrad = (value & 2) != 0;
@@ -1945,7 +1959,9 @@ int ogcp_debug_solve_draw(ogcp_ctx* ctx, const ogcp_slice* s, uint64_t seed, con
   if (S.q_dev) OGCP_CUDA(cudaMemcpy(&zrows, S.q_dev, 8, cudaMemcpyDeviceToHost));
   const int64_t total = pn + zrows;
   int64_t nlo = 0, nhi = pn, zlo = 0, zhi = zrows;
-  if (S.shard_world > 1 && S.zshard) {
+  if (S.shard_world > 1 && S.zshard == 2) {
+    // rank-local zero rows (word-sharded draw): all of them
+  } else if (S.shard_world > 1 && S.zshard) {
     zlo = zrows * S.shard_rank / S.shard_world;
     zhi = zrows * (S.shard_rank + 1) / S.shard_world;
   } else if (S.shard_world > 1) {

@@ -24,12 +24,15 @@
 // "rejected > budget" fires iff more than `budget` hits precede the q-th miss.
 #include <algorithm>
 #include <cmath>
+#include <memory>
+#include <vector>
 
 #include <cub/cub.cuh>
 
 #include "common.cuh"
 #include "hash.cuh"
 #include "sampler.cuh"
+#include "comm.cuh"
 
 namespace ogcp {
 
@@ -231,13 +234,17 @@ __device__ __forceinline__ uint32_t map_at(const Map<NCOL>& m, int c) {
   return v;
 }
 
-// Pass 1: per-chunk maps + per-block aggregate maps.
+// Pass 1: per-chunk maps + per-block aggregate maps.  Block b covers tile b0 + b
+// of the stream (b0 > 0: a word-range shard); tmaps are indexed by the launch's
+// own chunks, bagg by tile.
 template <int NCOL>
 __global__ void __launch_bounds__(kScanThreads) k_draw_count(StreamSpec sp, const long long* w0p, int64_t nchunks,
                                                              uint8_t* __restrict__ tmaps,
-                                                             uint32_t* __restrict__ bagg) {
-  const int64_t chunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
-  WordGen g = block_wordgen(sp, w0p);
+                                                             uint32_t* __restrict__ bagg, int64_t b0 = 0) {
+  const int64_t tile = b0 + blockIdx.x;
+  const int64_t chunk = tile * kScanThreads + threadIdx.x;
+  const int64_t lchunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
+  WordGen g = tile_wordgen(sp, w0p, tile);
   Map<NCOL> m = identity_map<NCOL>();
   if (chunk < nchunks) {
     int col[NCOL];
@@ -261,13 +268,13 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_count(StreamSpec sp, cons
       }
     }
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) tmaps[chunk * NCOL + c] = (uint8_t)m.c[c];
+    for (int c = 0; c < NCOL; ++c) tmaps[lchunk * NCOL + c] = (uint8_t)m.c[c];
   }
   Map<NCOL> excl, agg;
   block_scan_maps<NCOL>(m, excl, agg);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) bagg[blockIdx.x * (int64_t)NCOL + c] = agg.c[c];
+    for (int c = 0; c < NCOL; ++c) bagg[tile * NCOL + c] = agg.c[c];
   }
 }
 
@@ -312,6 +319,13 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_scan_blocks(const uint32_
 // write the block's contiguous output range with coalesced stores.
 // NCOL == 1 (nonzero stratum): out[e] = value; records the end word of element target-1.
 // NCOL  > 1 (zero candidates):  out[e] = value (row-major [row][NCOL]).
+//
+// Word-range shards (sharded draws, below): b0 is the first tile of this rank's
+// range; lim_dev (nullable) lowers the element limit to *lim_dev and shift_dev
+// (nullable) writes element e at out[e - *shift_dev], dropping e < *shift_dev;
+// ocnt (nullable, merged form) counts the accepted draws per owner rank
+// (ordinal / ospan, at most kMaxDrawOwners owners) instead of `owned`.
+constexpr int kMaxDrawOwners = 8;
 template <int NCOL>
 __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, const long long* w0p, int64_t nchunks,
                                                              const uint8_t* __restrict__ tmaps,
@@ -320,27 +334,38 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
                                                              long long* __restrict__ end_word,
                                                              uint32_t* __restrict__ hist, DevFlags* flags,
                                                              uint32_t olo, uint32_t ohi,
-                                                             unsigned long long* __restrict__ owned) {
+                                                             unsigned long long* __restrict__ owned,
+                                                             int64_t b0 = 0, const long long* lim_dev = nullptr,
+                                                             const long long* shift_dev = nullptr,
+                                                             unsigned long long* __restrict__ ocnt = nullptr,
+                                                             uint32_t ospan = 1) {
   __shared__ int32_t stage[kBlockWords];
   uint32_t mine = 0;  // merged form: accepted draws landing in this rank's ordinal range [olo, ohi)
-  const int64_t chunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
-  WordGen g = block_wordgen(sp, w0p);
+  uint32_t oc[kMaxDrawOwners];
+#pragma unroll
+  for (int j = 0; j < kMaxDrawOwners; ++j) oc[j] = 0;
+  const int64_t tile = b0 + blockIdx.x;
+  const int64_t chunk = tile * kScanThreads + threadIdx.x;
+  const int64_t lchunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
+  WordGen g = tile_wordgen(sp, w0p, tile);
+  if (lim_dev) target = min((long long)target, *lim_dev);
+  const long long shift = shift_dev ? *shift_dev : 0;
   Map<NCOL> m = identity_map<NCOL>();
   if (chunk < nchunks) {
 #pragma unroll
-    for (int c = 0; c < NCOL; ++c) m.c[c] = tmaps[chunk * NCOL + c];
+    for (int c = 0; c < NCOL; ++c) m.c[c] = tmaps[lchunk * NCOL + c];
   }
   Map<NCOL> excl, agg;
   block_scan_maps<NCOL>(m, excl, agg);
-  const int bcol = (int)bstart[blockIdx.x * 2 + 0];
-  const long long eb = bstart[blockIdx.x * 2 + 1];
+  const int bcol = (int)bstart[tile * 2 + 0];
+  const long long eb = bstart[tile * 2 + 1];
   const uint32_t adv = map_at<NCOL>(excl, bcol);
   const long long nblk = map_at<NCOL>(agg, bcol);
   int col = (int)((bcol + adv) % NCOL);
   long long e = eb + adv;
   int rel = (int)adv;
   if (chunk < nchunks && e < target) {
-    uint64_t w = block_word0(w0p) + (uint64_t)threadIdx.x * kChunkWords;
+    uint64_t w = tile_word0(w0p, tile) + (uint64_t)threadIdx.x * kChunkWords;
     for (int i = 0; i < kChunkWords && e < target; ++i, ++w) {
       const uint32_t word = g.next();
       uint32_t n = sp.n[0], thr = sp.thr[0];
@@ -354,7 +379,13 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
           if (val >= olo && val < ohi) {
             const uint32_t o = val - olo;
             atomicAdd(hist + (o >> 3), 1u << ((o & 7u) << 2));
-            ++mine;
+            if (ocnt) {
+              const uint32_t own = val / ospan;
+#pragma unroll
+              for (int j = 0; j < kMaxDrawOwners; ++j) oc[j] += own == (uint32_t)j;
+            } else {
+              ++mine;
+            }
           }
         } else {
           stage[rel++] = (int32_t)val;
@@ -366,6 +397,16 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
     }
   }
   if (hist) {
+    if (ocnt) {
+#pragma unroll
+      for (int j = 0; j < kMaxDrawOwners; ++j) {
+        uint32_t v = oc[j];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(ocnt + j, (unsigned long long)v);
+      }
+      return;
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(owned, (unsigned long long)mine);
@@ -373,7 +414,8 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
   }
   __syncthreads();
   const long long lim = min((long long)nblk, (long long)target - eb);
-  for (long long i = threadIdx.x; i < lim; i += kScanThreads) out[eb + i] = stage[i];
+  for (long long i = threadIdx.x; i < lim; i += kScanThreads)
+    if (eb + i >= shift) out[eb + i - shift] = stage[i];
 }
 
 struct ZeroSpec {
@@ -660,11 +702,12 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_compact(ZeroSpec zs, cons
 // Lazy layout: locate the q-th miss.  The accepted zeros are then candidate rows
 // [0, R) minus the rows flagged -1, R = row of the q-th miss + 1, and the
 // reference's rejection count at its last round is R - q (sampling.py:137-150).
-__global__ void __launch_bounds__(kScanThreads) k_zero_locate(const uint32_t* __restrict__ bcount,
-                                                              const long long* __restrict__ boff, int64_t nblocks,
-                                                              const uint8_t* __restrict__ miss, int64_t rows_max,
-                                                              int64_t q, long long* __restrict__ rows_used,
-                                                              long long* __restrict__ hits_before) {
+// (a __device__ body: the sharded draw's cut runs it with a device-side q; all
+// threads of the block call it, row_base shifts the reported hit count)
+__device__ void zero_locate_body(const uint32_t* __restrict__ bcount, const long long* __restrict__ boff,
+                                 int64_t nblocks, const uint8_t* __restrict__ miss, int64_t rows_max, int64_t q,
+                                 long long* __restrict__ rows_used, long long* __restrict__ hits_before,
+                                 long long row_base, long long q_global) {
   __shared__ int64_t sb;
   __shared__ int wsum[kScanThreads / 32];
   if (threadIdx.x == 0) {
@@ -701,10 +744,18 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_locate(const uint32_t* __
     if (!(bits & (1u << j))) continue;
     if (rank == target) {
       *rows_used = r0 + j + 1;
-      *hits_before = (r0 + j) - (q - 1);
+      *hits_before = (row_base + r0 + j) - (q_global - 1);
     }
     ++rank;
   }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_zero_locate(const uint32_t* __restrict__ bcount,
+                                                              const long long* __restrict__ boff, int64_t nblocks,
+                                                              const uint8_t* __restrict__ miss, int64_t rows_max,
+                                                              int64_t q, long long* __restrict__ rows_used,
+                                                              long long* __restrict__ hits_before) {
+  zero_locate_body(bcount, boff, nblocks, miss, rows_max, q, rows_used, hits_before, 0, q);
 }
 
 // Semi-stratified uniform stratum with size-1 modes: [row][ncol] -> [row][d] (zeros inserted).
@@ -1126,6 +1177,39 @@ static const int32_t* sort_zero_rows(Ctx* ctx, const Slice* X, DrawScratch& scr,
   return scr.zsorted.as<int32_t>();
 }
 
+// Merged form, second half: the 4-bit counters of ordinals [olo, olo + own) ->
+// (ordinal or bucketed position, multiplicity) in ascending order, certified by
+// Σ counters = *owned (the draws that landed in the range); the distinct count
+// lands in sc[5] (merged->count), the counter sum in sc[7].
+static void merged_compact(Ctx* ctx, MergedDraw* merged, const uint32_t* counters, uint32_t olo, int64_t own,
+                           const unsigned long long* owned, long long* sc) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nwords = (own + 7) / 8;
+  // (the caller sized merged->ord / cnt for min(p, own) entries)
+  if (merged->perm) {  // emit in the slice's bucketed position order
+    merged->pnib.ensure((size_t)std::max<int64_t>(nwords, 1) * 4);
+    k_hist_permute<<<std::max<int64_t>(1, std::min<int64_t>((nwords + 255) / 256, kNumSMs * 16)), 256, 0, s>>>(
+        counters, merged->perm, own, nwords, merged->pnib.as<uint32_t>(), (int32_t)olo);
+    ctx->count();
+    counters = merged->pnib.as<uint32_t>();
+  }
+  const int64_t hblocks = std::max<int64_t>(1, (nwords + (int64_t)kHistWordsPerThread * kScanThreads - 1) /
+                                                   ((int64_t)kHistWordsPerThread * kScanThreads));
+  merged->bcount.ensure((size_t)hblocks * 4);
+  merged->boff.ensure((size_t)hblocks * 8);
+  unsigned long long* cnt_sum = reinterpret_cast<unsigned long long*>(sc + 7);
+  k_hist_count<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, merged->bcount.as<uint32_t>(), cnt_sum);
+  k_hist_verify<<<1, 32, 0, s>>>(cnt_sum, owned, ctx->flags.as<DevFlags>());
+  ctx->count();
+  k_zero_scan<<<1, 1024, 0, s>>>(merged->bcount.as<uint32_t>(), hblocks, merged->boff.as<long long>(), sc + 5);
+  // positions (bucketed copy) are local; unbucketed ordinals are global
+  k_hist_write<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, own, merged->boff.as<long long>(),
+                                                          merged->ord.as<int32_t>(), merged->cnt.as<uint8_t>(),
+                                                          merged->perm ? 0 : (int32_t)olo);
+  ctx->count(3);
+  merged->count = sc + 5;
+}
+
 // Enqueue one stratified draw.  ordinals: int32 [p]; zero_subs: int32 [q x ndim].
 // code: event code (event*4) recorded on sampling errors / shortfall.
 DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
@@ -1191,31 +1275,7 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
         unsigned long long* owned = reinterpret_cast<unsigned long long*>(sc + 9);
         run_stream<1>(ctx, sp, nullptr, p, words, nullptr, nz_end, nz_avail, scr, merged->hist.as<uint32_t>(), olo,
                       ohi, owned);
-        const uint32_t* counters = merged->hist.as<uint32_t>();
-        if (merged->perm) {  // emit in the slice's bucketed position order
-          merged->pnib.ensure((size_t)std::max<int64_t>(nwords, 1) * 4);
-          k_hist_permute<<<std::max<int64_t>(1, std::min<int64_t>((nwords + 255) / 256, kNumSMs * 16)), 256, 0, s>>>(
-              counters, merged->perm, own, nwords, merged->pnib.as<uint32_t>(), (int32_t)olo);
-          ctx->count();
-          counters = merged->pnib.as<uint32_t>();
-        }
-        const int64_t hblocks = std::max<int64_t>(1, (nwords + (int64_t)kHistWordsPerThread * kScanThreads - 1) /
-                                                         ((int64_t)kHistWordsPerThread * kScanThreads));
-        merged->bcount.ensure((size_t)hblocks * 4);
-        merged->boff.ensure((size_t)hblocks * 8);
-        unsigned long long* cnt_sum = reinterpret_cast<unsigned long long*>(sc + 7);
-        k_hist_count<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, merged->bcount.as<uint32_t>(),
-                                                                cnt_sum);
-        k_hist_verify<<<1, 32, 0, s>>>(cnt_sum, owned, ctx->flags.as<DevFlags>());
-        ctx->count();
-        k_zero_scan<<<1, 1024, 0, s>>>(merged->bcount.as<uint32_t>(), hblocks, merged->boff.as<long long>(),
-                                       sc + 5);
-        // positions (bucketed copy) are local; unbucketed ordinals are global
-        k_hist_write<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, own, merged->boff.as<long long>(),
-                                                                merged->ord.as<int32_t>(), merged->cnt.as<uint8_t>(),
-                                                                merged->perm ? 0 : (int32_t)olo);
-        ctx->count(3);
-        merged->count = sc + 5;
+        merged_compact(ctx, merged, merged->hist.as<uint32_t>(), olo, own, owned, sc);
       } else {
         // q == 0: nothing follows, so the fused pass reports its own shortfall
         run_stream<1>(ctx, sp, nullptr, p, words, ordinals, nz_end, nz_avail, scr, nullptr, 0, 0, nullptr,
@@ -1360,6 +1420,497 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
                                 (long long)budget, code, ctx->flags.as<DevFlags>());
   ctx->count();
   check_launch();
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Word-range sharded merged draws (multi-GPU; sampler.cuh ShardScratch).  Rank r
+// of N generates the stream tiles [r S, (r + 1) S), S = ceil(tiles / N), of both
+// strata; everything a rank needs from the others is small (per-tile aggregate
+// maps, per-rank zero-row records) except the nibble counters, which are
+// reduce-scattered to the ordinal owners (eta / 2 bytes in total).
+
+// Per-chunk map of the words of one thread's chunk (the counting loop of k_draw_count).
+template <int NCOL>
+__device__ __forceinline__ Map<NCOL> chunk_map(WordGen& g, const StreamSpec& sp) {
+  Map<NCOL> m = identity_map<NCOL>();
+  int col[NCOL];
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) col[c] = c;
+#pragma unroll 4
+  for (int i = 0; i < kChunkWords; ++i) {
+    const uint32_t w = g.next();
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) {
+      const int cc = col[c];
+      uint32_t n = sp.n[0], thr = sp.thr[0];
+#pragma unroll
+      for (int j = 1; j < NCOL; ++j)
+        if (j == cc) { n = sp.n[j]; thr = sp.thr[j]; }
+      if ((uint32_t)((uint64_t)w * n) >= thr) {
+        m.c[c] += 1;
+        col[c] = cc + 1 == NCOL ? 0 : cc + 1;
+      }
+    }
+  }
+  return m;
+}
+
+// The word after element target-1 of the stream (what k_draw_write records as
+// end_word), found by re-generating the one tile that holds it.
+template <int NCOL>
+__global__ void __launch_bounds__(kScanThreads) k_draw_locate_end(StreamSpec sp, const long long* w0p, int64_t nchunks,
+                                                                  const long long* __restrict__ bstart,
+                                                                  int64_t nblocks, const long long* __restrict__ total,
+                                                                  int64_t target, long long* __restrict__ end_word) {
+  __shared__ long long tb;
+  if (threadIdx.x == 0) {
+    tb = -1;
+    if (target > 0 && *total >= target) {
+      int64_t lo = 0, hi = nblocks - 1;  // last tile whose first element is <= target-1
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (bstart[mid * 2 + 1] <= target - 1) lo = mid;
+        else hi = mid - 1;
+      }
+      tb = lo;
+    }
+  }
+  __syncthreads();
+  if (tb < 0) return;
+  const int64_t tile = tb;
+  const int64_t chunk = tile * kScanThreads + threadIdx.x;
+  WordGen g = tile_wordgen(sp, w0p, tile);
+  WordGen g0 = g;
+  Map<NCOL> m = identity_map<NCOL>();
+  if (chunk < nchunks) m = chunk_map<NCOL>(g, sp);
+  Map<NCOL> excl, agg;
+  block_scan_maps<NCOL>(m, excl, agg);
+  const int bcol = (int)bstart[tile * 2 + 0];
+  const uint32_t adv = map_at<NCOL>(excl, bcol);
+  int col = (int)((bcol + adv) % NCOL);
+  long long e = bstart[tile * 2 + 1] + adv;
+  if (chunk >= nchunks || e > target - 1) return;
+  uint64_t w = tile_word0(w0p, tile) + (uint64_t)threadIdx.x * kChunkWords;
+  for (int i = 0; i < kChunkWords && e < target; ++i, ++w) {
+    const uint32_t word = g0.next();
+    uint32_t n = sp.n[0], thr = sp.thr[0];
+#pragma unroll
+    for (int j = 1; j < NCOL; ++j)
+      if (j == col) { n = sp.n[j]; thr = sp.thr[j]; }
+    if ((uint32_t)((uint64_t)word * n) >= thr) {
+      if (e == target - 1) *end_word = (long long)(w + 1);
+      ++e;
+      col = col + 1 == NCOL ? 0 : col + 1;
+    }
+  }
+}
+
+// This rank's zero candidate rows: the rows whose first element lies in its
+// element range [E(r S), E((r + 1) S)) (complete rows only, clipped to the
+// provisioned target).  zr: [0] first row, [1] end row, [2] local elements,
+// [3] element shift (ncol x first row), [4] element limit (ncol x end row),
+// [5] end of its own element range, [6] first tile after its range.
+__global__ void k_zshard_range(const long long* __restrict__ bst, int64_t nblocks, const long long* __restrict__ total,
+                               int64_t target, int64_t slot, int rank, int world, int ncol, long long* __restrict__ zr,
+                               long long* __restrict__ rec_rows) {
+  if (threadIdx.x || blockIdx.x) return;
+  const long long tlim = min(*total, (long long)target);
+  const int64_t blo = (int64_t)rank * slot, bhi = min((int64_t)(rank + 1) * slot, nblocks);
+  const long long elo = blo < nblocks ? min(bst[blo * 2 + 1], tlim) : tlim;
+  const long long ehi = (rank == world - 1 || bhi >= nblocks) ? tlim : min(bst[bhi * 2 + 1], tlim);
+  const long long rows_all = tlim / ncol;
+  long long rhi = rank == world - 1 ? rows_all : min((ehi + ncol - 1) / ncol, rows_all);
+  long long rlo = min(min((elo + ncol - 1) / ncol, rows_all), rhi);
+  zr[0] = rlo;
+  zr[1] = rhi;
+  zr[2] = (rhi - rlo) * ncol;
+  zr[3] = rlo * ncol;
+  zr[4] = rhi * ncol;
+  zr[5] = ehi;
+  zr[6] = bhi;
+  *rec_rows = rhi - rlo;
+}
+
+// The elements of this rank's last row past its own tiles (< ncol of them, the
+// first accepted words of the next tile).
+template <int NCOL>
+__global__ void k_zshard_tail(StreamSpec sp, const long long* w0p, const long long* __restrict__ bst, int64_t nblocks,
+                              const long long* __restrict__ zr, int32_t* __restrict__ out) {
+  const long long lim = zr[4], ehi = zr[5], shift = zr[3];
+  const int64_t tile = zr[6];
+  if (zr[1] <= zr[0] || lim <= ehi || tile >= nblocks) return;
+  WordGen g = tile_wordgen(sp, w0p, tile);  // thread 0's chunk starts at the tile's first word
+  if (threadIdx.x != 0) return;
+  int col = (int)bst[tile * 2 + 0];
+  long long e = bst[tile * 2 + 1];
+  while (e < lim) {
+    const uint32_t word = g.next();
+    uint32_t n = sp.n[0], thr = sp.thr[0];
+#pragma unroll
+    for (int j = 1; j < NCOL; ++j)
+      if (j == col) { n = sp.n[j]; thr = sp.thr[j]; }
+    const uint64_t prod = (uint64_t)word * n;
+    if ((uint32_t)prod >= thr) {
+      if (e >= shift) out[e - shift] = (int32_t)(prod >> 32);
+      ++e;
+      col = col + 1 == NCOL ? 0 : col + 1;
+    }
+  }
+}
+
+// Locate the q-th miss from the all-gathered (misses, rows) records: the rank
+// holding it finds its local row (rows_used = local row + 1, hits_before = the
+// reference's rejection count); ranks before it use all their rows, ranks after
+// it none.  Status as k_draw_status: a nonzero shortfall asks for a retry; with
+// fewer than q misses in all ranks' rows, more than `budget` hits is the
+// reference's SamplingError, else a shortfall.
+__global__ void __launch_bounds__(kScanThreads) k_zshard_cut(
+    const long long* __restrict__ rec, int world, int rank, int64_t q, long long budget,
+    const long long* __restrict__ zr, const uint32_t* __restrict__ bcount, const long long* __restrict__ boff,
+    int64_t nblocks, const uint8_t* __restrict__ miss, int64_t lrows_max, long long* __restrict__ rows_used,
+    long long* __restrict__ hits_before, const long long* __restrict__ nz_avail, int64_t p, long long code,
+    DevFlags* flags) {
+  __shared__ long long t_loc;
+  __shared__ int holds;
+  const bool nz_short = p > 0 && *nz_avail < p;
+  if (threadIdx.x == 0) {
+    long long before = 0, mt = 0, nt = 0;
+    for (int s = 0; s < world; ++s) {
+      if (s < rank) before += rec[2 * s];
+      mt += rec[2 * s];
+      nt += rec[2 * s + 1];
+    }
+    const long long mine = rec[2 * rank], rows = rec[2 * rank + 1];
+    const long long t = q - before;
+    *hits_before = 0;
+    holds = 0;
+    if (t <= 0) *rows_used = 0;
+    else if (t > mine) *rows_used = rows;
+    else holds = 1;
+    t_loc = t;
+    bool exhausted = false, shortfall = nz_short;
+    if (!nz_short && mt < q) {
+      if (nt - mt > budget) exhausted = true;
+      else shortfall = true;
+    }
+    if (exhausted) atomicMin(&flags->first_code[kFlagSampling], code);
+    else if (shortfall) atomicMin(&flags->first_code[kFlagShortfall], code);
+  }
+  __syncthreads();
+  if (!holds) return;
+  zero_locate_body(bcount, boff, nblocks, miss, lrows_max, t_loc, rows_used, hits_before, zr[0], q);
+  __syncthreads();
+  if (threadIdx.x == 0 && !nz_short && *hits_before > budget) atomicMin(&flags->first_code[kFlagSampling], code);
+}
+
+template <typename T>
+__global__ void k_add_into(T* __restrict__ dst, const T* __restrict__ src, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+
+void shard_owner_range(int64_t eta, int rank, int world, int64_t* olo, int64_t* ohi) {
+  const int64_t cw = ((eta + 7) / 8 + world - 1) / world;
+  *olo = std::min<int64_t>(8 * cw * rank, eta);
+  *ohi = std::min<int64_t>(8 * cw * (rank + 1), eta);
+}
+
+bool shard_draw_eligible(const Ctx* ctx, const Slice* X, int64_t p, int64_t q, bool semi) {
+  if (!ctx->shard_draws || ctx->world < 2 || ctx->world > kMaxDrawOwners) return false;
+  if (!ctx->comm_draw && !ctx->shard_sim) return false;
+  if (semi || p <= 0 || q <= 0 || X->nnz < 2 || X->ndim > kMaxCols) return false;
+  for (int k = 0; k < X->ndim; ++k)
+    if (X->dims[k] < 2) return false;  // the in-place lazy layout (every mode consumes words)
+  return true;
+}
+
+namespace {
+
+struct ShardPlan {
+  int world = 1, ncol = 0;
+  int64_t eta = 0, p = 0, q = 0, budget = 0;
+  StreamSpec spn, spz;
+  ZeroSpec zs;
+  int64_t n_nchunks = 0, n_nblocks = 0, n_slot = 0;
+  int64_t z_nchunks = 0, z_nblocks = 0, z_slot = 0, z_target = 0;
+  int64_t lrows_max = 0, lzblocks = 0, cw = 0;
+};
+
+ShardPlan shard_plan(const Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget) {
+  ShardPlan pl;
+  const int W = ctx->world;
+  const int d = X->ndim;
+  pl.world = W;
+  pl.eta = X->nnz;
+  pl.p = p;
+  pl.q = q;
+  pl.budget = budget;
+  StreamSpec sp;
+  sp.st_hi = (unsigned long long)(g.state >> 64);
+  sp.st_lo = (unsigned long long)g.state;
+  sp.inc_hi = (unsigned long long)(g.inc >> 64);
+  sp.inc_lo = (unsigned long long)g.inc;
+  const double slack = ctx->slack;
+  // nonzero stratum: integers(0, eta, size=p), words provisioned as draw_enqueue does
+  pl.spn = sp;
+  pl.spn.ncol = 1;
+  pl.spn.n[0] = (uint32_t)pl.eta;
+  pl.spn.thr[0] = lemire_threshold((uint32_t)pl.eta);
+  {
+    const double r = reject_rate((uint32_t)pl.eta);
+    const int64_t words = (int64_t)(((double)p / (1.0 - r) + 10.0 * std::sqrt((double)p * r) / (1.0 - r) + 2048.0) *
+                                    slack);
+    pl.n_nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
+    pl.n_nblocks = (pl.n_nchunks + kScanThreads - 1) / kScanThreads;
+    pl.n_slot = (pl.n_nblocks + W - 1) / W;
+  }
+  pl.cw = ((pl.eta + 7) / 8 + W - 1) / W;
+  // zero stratum: candidate rows as draw_enqueue provisions them (every mode consumes words)
+  pl.spz = sp;
+  pl.ncol = d;
+  pl.spz.ncol = d;
+  pl.zs.ndim = d;
+  pl.zs.ncol = d;
+  double rmax = 0.0;
+  for (int k = 0; k < kMaxModes; ++k) {
+    pl.zs.colmap[k] = k < d ? k : -1;
+    pl.zs.st.s[k] = k < d ? X->strides[k] : 0;
+  }
+  for (int k = 0; k < d; ++k) {
+    pl.spz.n[k] = (uint32_t)X->dims[k];
+    pl.spz.thr[k] = lemire_threshold((uint32_t)X->dims[k]);
+    rmax = std::max(rmax, reject_rate((uint32_t)X->dims[k]));
+  }
+  const double rho = X->omega_d > 0 ? (double)pl.eta / X->omega_d : 0.0;
+  const double exp_rows = rho < 1.0 ? (double)q / (1.0 - rho) : 1e30;
+  const double sd_rows = rho < 1.0 ? std::sqrt((double)q * rho) / (1.0 - rho) : 1e30;
+  const double want = (exp_rows + 10.0 * sd_rows + 64.0) * slack;
+  const double cap = (double)q + (double)budget + 1.0;
+  int64_t rows_max = (int64_t)std::min(want, cap);
+  if (rows_max < q) rows_max = q;
+  pl.z_target = rows_max * d;
+  {
+    const double exp_words = (double)pl.z_target / (1.0 - rmax);
+    const double sd = std::sqrt((double)pl.z_target * rmax) / (1.0 - rmax);
+    const int64_t words = (int64_t)((exp_words + 10.0 * sd + 2048.0) * slack);
+    pl.z_nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
+    pl.z_nblocks = (pl.z_nchunks + kScanThreads - 1) / kScanThreads;
+    pl.z_slot = (pl.z_nblocks + W - 1) / W;
+  }
+  // a rank's rows start in its own elements: at most (its words) / d + 1 of them
+  pl.lrows_max = std::min<int64_t>(rows_max, pl.z_slot * (int64_t)kBlockWords / d + 1);
+  pl.lzblocks = ((pl.lrows_max + kRowsPerThread - 1) / kRowsPerThread + kScanThreads - 1) / kScanThreads;
+  return pl;
+}
+
+void shard_alloc(const ShardPlan& pl, ShardScratch& sh, int d) {
+  const int W = pl.world;
+  sh.tm_nz.ensure((size_t)pl.n_slot * kScanThreads);
+  sh.tm_z.ensure((size_t)pl.z_slot * kScanThreads * pl.ncol);
+  sh.bagg_nz.ensure((size_t)W * pl.n_slot * 4);
+  sh.bagg_z.ensure((size_t)W * pl.z_slot * pl.ncol * 4);
+  sh.bst_nz.ensure((size_t)pl.n_nblocks * 16);
+  sh.bst_z.ensure((size_t)pl.z_nblocks * 16);
+  sh.hist.ensure((size_t)W * pl.cw * 4);
+  sh.ocnt.ensure((size_t)kMaxDrawOwners * 8);
+  sh.zrec.ensure((size_t)W * 16);
+  sh.scal.ensure(16 * 8);
+  sh.cand.ensure((size_t)std::max<int64_t>(pl.lrows_max, 1) * d * 4);
+  sh.miss.ensure((size_t)pl.lzblocks * kScanThreads);
+  sh.zcount.ensure((size_t)pl.lzblocks * 4);
+  sh.zoff.ensure((size_t)pl.lzblocks * 8);
+}
+
+template <int NCOL>
+void zero_tiles(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r, bool count) {
+  cudaStream_t s = ctx->stream;
+  const int64_t b0 = (int64_t)r * pl.z_slot;
+  const int64_t nt = std::max<int64_t>(0, std::min(pl.z_slot, pl.z_nblocks - b0));
+  long long* sc = sh.scal.as<long long>();
+  if (count) {
+    if (nt > 0) {
+      k_draw_count<NCOL><<<(unsigned)nt, kScanThreads, 0, s>>>(pl.spz, sc + 0, pl.z_nchunks, sh.tm_z.as<uint8_t>(),
+                                                              sh.bagg_z.as<uint32_t>(), b0);
+      ctx->count();
+    }
+    return;
+  }
+  k_draw_scan_blocks<NCOL><<<1, kScanThreads, 0, s>>>(sh.bagg_z.as<uint32_t>(), pl.z_nblocks, sh.bst_z.as<long long>(),
+                                                      sc + 2);
+  k_zshard_range<<<1, 1, 0, s>>>(sh.bst_z.as<long long>(), pl.z_nblocks, sc + 2, pl.z_target, pl.z_slot, r, pl.world,
+                                 NCOL, sc + 9, sh.zrec.as<long long>() + 2 * r + 1);
+  ctx->count(2);
+  if (nt > 0) {
+    k_draw_write<NCOL><<<(unsigned)nt, kScanThreads, 0, s>>>(
+        pl.spz, sc + 0, pl.z_nchunks, sh.tm_z.as<uint8_t>(), sh.bst_z.as<long long>(), pl.z_target,
+        sh.cand.as<int32_t>(), nullptr, nullptr, ctx->flags.as<DevFlags>(), 0u, 0u, nullptr, b0, sc + 13, sc + 12);
+    ctx->count();
+  }
+  k_zshard_tail<NCOL><<<1, 32, 0, s>>>(pl.spz, sc + 0, sh.bst_z.as<long long>(), pl.z_nblocks, sc + 9,
+                                       sh.cand.as<int32_t>());
+  ctx->count();
+}
+
+void zero_tiles_any(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r, bool count) {
+  switch (pl.ncol) {
+    case 2: zero_tiles<2>(ctx, pl, sh, r, count); break;
+    case 3: zero_tiles<3>(ctx, pl, sh, r, count); break;
+    case 4: zero_tiles<4>(ctx, pl, sh, r, count); break;
+    case 5: zero_tiles<5>(ctx, pl, sh, r, count); break;
+    case 6: zero_tiles<6>(ctx, pl, sh, r, count); break;
+    case 7: zero_tiles<7>(ctx, pl, sh, r, count); break;
+    default: throw Error(OGCP_E_INTERNAL, "sharded draw: unsupported mode count");
+  }
+}
+
+// Rank r's part before the first exchange: the nonzero tiles' maps.
+void phase_count(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r) {
+  cudaStream_t s = ctx->stream;
+  OGCP_CUDA(cudaMemsetAsync(sh.scal.ptr, 0, 16 * 8, s));
+  OGCP_CUDA(cudaMemsetAsync(sh.ocnt.ptr, 0, (size_t)kMaxDrawOwners * 8, s));
+  const int64_t b0 = (int64_t)r * pl.n_slot;
+  const int64_t nt = std::max<int64_t>(0, std::min(pl.n_slot, pl.n_nblocks - b0));
+  if (nt > 0) {
+    k_draw_count<1><<<(unsigned)nt, kScanThreads, 0, s>>>(pl.spn, nullptr, pl.n_nchunks, sh.tm_nz.as<uint8_t>(),
+                                                          sh.bagg_nz.as<uint32_t>(), b0);
+    ctx->count();
+  }
+}
+
+// After the map all-gather: the stream scan, the nonzero end word, this rank's
+// counters over all ordinals, and the zero stream's tile maps.
+void phase_write(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r) {
+  cudaStream_t s = ctx->stream;
+  long long* sc = sh.scal.as<long long>();
+  k_draw_scan_blocks<1><<<1, kScanThreads, 0, s>>>(sh.bagg_nz.as<uint32_t>(), pl.n_nblocks, sh.bst_nz.as<long long>(),
+                                                   sc + 1);
+  k_draw_locate_end<1><<<1, kScanThreads, 0, s>>>(pl.spn, nullptr, pl.n_nchunks, sh.bst_nz.as<long long>(),
+                                                  pl.n_nblocks, sc + 1, pl.p, sc + 0);
+  ctx->count(2);
+  OGCP_CUDA(cudaMemsetAsync(sh.hist.ptr, 0, (size_t)pl.world * pl.cw * 4, s));
+  const int64_t b0 = (int64_t)r * pl.n_slot;
+  const int64_t nt = std::max<int64_t>(0, std::min(pl.n_slot, pl.n_nblocks - b0));
+  if (nt > 0) {
+    k_draw_write<1><<<(unsigned)nt, kScanThreads, 0, s>>>(
+        pl.spn, nullptr, pl.n_nchunks, sh.tm_nz.as<uint8_t>(), sh.bst_nz.as<long long>(), pl.p, nullptr, nullptr,
+        sh.hist.as<uint32_t>(), ctx->flags.as<DevFlags>(), 0u, (uint32_t)pl.eta, nullptr, b0, nullptr, nullptr,
+        sh.ocnt.as<unsigned long long>(), (uint32_t)(8 * pl.cw));
+    ctx->count();
+  }
+  zero_tiles_any(ctx, pl, sh, r, /*count=*/true);
+  check_launch();
+}
+
+// After the counter reduce-scatter and the zero maps' all-gather: this rank's zero
+// candidate rows and their hit test (and, for the calling rank, the compaction of
+// its merged nonzeros).
+void phase_zero(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r, const Slice* X) {
+  cudaStream_t s = ctx->stream;
+  long long* sc = sh.scal.as<long long>();
+  zero_tiles_any(ctx, pl, sh, r, /*count=*/false);
+  k_zero_hits<<<(unsigned)pl.lzblocks, kScanThreads, 0, s>>>(
+      pl.zs, sh.cand.as<int32_t>(), sc + 11, pl.lrows_max, X->hash.as<unsigned long long>(), X->table_mask,
+      sh.miss.as<uint8_t>(), sh.zcount.as<uint32_t>(), 0, nullptr, 1,
+      X->filter_mask ? X->filter.as<unsigned int>() : nullptr, X->filter_mask);
+  k_zero_scan<<<1, 1024, 0, s>>>(sh.zcount.as<uint32_t>(), pl.lzblocks, sh.zoff.as<long long>(),
+                                 sh.zrec.as<long long>() + 2 * r);
+  ctx->count(2);
+  check_launch();
+}
+
+enum class XMode { nccl, emulate, replicate };
+
+// All-gather of per-rank slots of `bytes`: NCCL, the other ranks' buffers (exact
+// simulation), or this rank's own slot standing in for the others (timing simulation).
+void xchg_allgather(Ctx* ctx, XMode xm, std::vector<ShardScratch*>& st, DevBuf ShardScratch::*mb, size_t bytes) {
+  const int W = ctx->world, R = ctx->rank;
+  if (xm == XMode::nccl) {
+    comm_draw_allgather(ctx, (st[R]->*mb).ptr, bytes);
+    return;
+  }
+  for (int s = 0; s < W; ++s) {
+    if (!st[s]) continue;
+    char* dst = static_cast<char*>((st[s]->*mb).ptr);
+    for (int o = 0; o < W; ++o) {
+      if (o == s) continue;
+      const char* src = st[o] ? static_cast<const char*>((st[o]->*mb).ptr) + o * bytes : dst + s * bytes;
+      OGCP_CUDA(cudaMemcpyAsync(dst + o * bytes, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  }
+}
+
+}  // namespace
+
+DrawOut shard_draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
+                           long long code, MergedDraw& md, ShardScratch& sh) {
+  init_jump_table();
+  ProfScope prof_scope(ctx, kProfDraw);
+  const ShardPlan pl = shard_plan(ctx, X, g, p, q, budget);
+  const int W = ctx->world, R = ctx->rank, d = X->ndim;
+  cudaStream_t s = ctx->stream;
+  const XMode xm = ctx->comm_draw ? XMode::nccl : (ctx->shard_sim_timing ? XMode::replicate : XMode::emulate);
+  static thread_local std::vector<std::unique_ptr<ShardScratch>> emu;  // the other ranks' state (exact simulation)
+  std::vector<ShardScratch*> st(W, nullptr);
+  st[R] = &sh;
+  if (xm == XMode::emulate) {
+    if ((int)emu.size() < W) emu.resize(W);
+    for (int r = 0; r < W; ++r)
+      if (r != R) {
+        if (!emu[r]) emu[r].reset(new ShardScratch);
+        st[r] = emu[r].get();
+      }
+  }
+  for (int r = 0; r < W; ++r)
+    if (st[r]) shard_alloc(pl, *st[r], d);
+  // 1. nonzero tile maps -> all-gather
+  for (int r = 0; r < W; ++r)
+    if (st[r]) phase_count(ctx, pl, *st[r], r);
+  xchg_allgather(ctx, xm, st, &ShardScratch::bagg_nz, (size_t)pl.n_slot * 4);
+  // 2. scan, end word, counters over all ordinals, zero tile maps -> reduce-scatter the
+  //    counters, all-reduce the per-owner draw counts, all-gather the zero maps (one group)
+  for (int r = 0; r < W; ++r)
+    if (st[r]) phase_write(ctx, pl, *st[r], r);
+  if (xm == XMode::nccl) {
+    comm_draw_group(ctx, true);
+    comm_draw_reduce_scatter_u32(ctx, sh.hist.as<uint32_t>(), (size_t)pl.cw);
+    comm_draw_allreduce_u64(ctx, sh.ocnt.as<unsigned long long>(), (size_t)W);
+    comm_draw_allgather(ctx, sh.bagg_z.ptr, (size_t)pl.z_slot * pl.ncol * 4);
+    comm_draw_group(ctx, false);
+  } else {
+    if (xm == XMode::emulate)
+      for (int o = 0; o < W; ++o) {
+        if (o == R) continue;
+        k_add_into<uint32_t><<<kNumSMs * 4, 256, 0, s>>>(sh.hist.as<uint32_t>() + (size_t)R * pl.cw,
+                                                         st[o]->hist.as<uint32_t>() + (size_t)R * pl.cw, pl.cw);
+        k_add_into<unsigned long long><<<1, 32, 0, s>>>(sh.ocnt.as<unsigned long long>(),
+                                                        st[o]->ocnt.as<unsigned long long>(), W);
+        ctx->count(2);
+      }
+    xchg_allgather(ctx, xm, st, &ShardScratch::bagg_z, (size_t)pl.z_slot * pl.ncol * 4);
+  }
+  // 3. this rank's merged nonzeros (owner range) from the summed counters
+  int64_t olo, ohi;
+  shard_owner_range(pl.eta, R, W, &olo, &ohi);
+  const int64_t own = ohi - olo;
+  md.ord.ensure((size_t)std::max<int64_t>(std::min(p, own), 1) * 4);
+  md.cnt.ensure((size_t)std::max<int64_t>(std::min(p, own), 1));
+  long long* sc = sh.scal.as<long long>();
+  merged_compact(ctx, &md, sh.hist.as<uint32_t>() + (size_t)R * pl.cw, (uint32_t)olo, own,
+                 sh.ocnt.as<unsigned long long>() + R, sc);
+  // 4. zero rows -> all-gather the (misses, rows) records -> the cut
+  for (int r = 0; r < W; ++r)
+    if (st[r]) phase_zero(ctx, pl, *st[r], r, X);
+  xchg_allgather(ctx, xm, st, &ShardScratch::zrec, 16);
+  k_zshard_cut<<<1, kScanThreads, 0, s>>>(sh.zrec.as<long long>(), W, R, q, (long long)budget, sc + 9,
+                                          sh.zcount.as<uint32_t>(), sh.zoff.as<long long>(), pl.lzblocks,
+                                          sh.miss.as<uint8_t>(), pl.lrows_max, sc + 8, sc + 4, sc + 1, p, code,
+                                          ctx->flags.as<DevFlags>());
+  ctx->count();
+  check_launch();
+  DrawOut out;
+  out.zsub = sh.cand.as<int32_t>();
+  out.q_dev = sc + 8;
   return out;
 }
 

@@ -41,6 +41,39 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
                      int32_t* ordinals, int32_t* zero_subs, long long code, DrawScratch& scr,
                      MergedDraw* merged = nullptr, bool lazy = false, bool semi = false);
 
+// Word-range sharded merged draw (multi-GPU).  Rank r
+// generates only its 1/N of the stream's 32-bit words: the per-tile aggregate
+// maps are all-gathered so every rank scans the whole stream (tile start column
+// and element offset, the nonzero stratum's end word), its draws are histogrammed
+// into nibble counters over all ordinals that are reduce-scattered to the
+// ordinal owners (uint32 sums of packed nibbles are nibble sums while no counter
+// wraps, which the count check certifies), and its zero candidate rows (the rows
+// that start in its element range) are probed locally; an all-gather of the
+// per-rank (misses, rows) locates the q-th miss.  One rank's device state:
+struct ShardScratch {
+  DevBuf tm_nz, tm_z;      // own tiles' chunk maps
+  DevBuf bagg_nz, bagg_z;  // per-tile aggregate maps, world x slot tiles (all-gathered)
+  DevBuf bst_nz, bst_z;    // per-tile start (column, element) of every tile
+  DevBuf hist;             // world x cw nibble words (chunk r: owner r's ordinals after the reduce-scatter)
+  DevBuf ocnt;             // world uint64: this rank's draws per owner range (all-reduced)
+  DevBuf zrec;             // world x 2 int64: (misses, rows) of every rank's zero rows (all-gathered)
+  DevBuf scal;             // 16 int64 scalars
+  DevBuf cand, miss, zcount, zoff;  // this rank's zero candidate rows [rows x ndim], hit bits, miss scan
+};
+// Owner ranges of a sharded merged draw: chunks of 8 * ceil(ceil(eta / 8) / world)
+// ordinals (whole nibble words).
+void shard_owner_range(int64_t eta, int rank, int world, int64_t* olo, int64_t* ohi);
+bool shard_draw_eligible(const Ctx* ctx, const Slice* X, int64_t p, int64_t q, bool semi);
+// The draw as rank ctx->rank of ctx->world: md receives this rank's merged nonzeros
+// (ordinals [olo, ohi) of shard_owner_range), the result's zsub / q_dev this rank's
+// zero rows in the lazy layout (local rows [0, *q_dev), -1-flagged hits skipped).
+// With a draw communicator the exchanges are NCCL collectives on ctx->stream; in
+// shard simulation (no communicator) every rank's part runs on this GPU in lock
+// step with device-side exchanges -- exact -- or, with ctx->shard_sim_timing, only
+// this rank's part with its own slots standing in for the others' (timing only).
+DrawOut shard_draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_t q, int64_t budget,
+                           long long code, MergedDraw& md, ShardScratch& sh);
+
 // Every draw of a solver epoch made up front (small draws only, see
 // draw_batch_eligible): draw b's nonzero ordinals at ord + b p, its zero stratum
 // in the lazy layout at cand + b rows_max ndim with the row count at

@@ -2,17 +2,20 @@
 
 1. Measured: the context runs in shard-simulation mode (OGCP_OPT_SHARD_SIM) and
    executes exactly rank 0's share of a world-N solve -- its own ordinal range of the
-   merged draws, its share of the zero rows, its owned rows of K5 / the Grams, and
-   the draw words / probes every rank repeats -- with the NCCL collectives skipped.
+   merged draws, its zero rows, its owned rows of K5 / the Grams -- with the NCCL
+   collectives skipped.  Two draw designs, both measured:
+   * replicated: every rank generates every RNG word and probes every zero candidate
+     (OGCP_OPT_SHARD_DRAWS 0);
+   * word-range sharded (the default, OGCP_OPT_SHARD_DRAWS 1): rank 0 generates its
+     1/N of the words (timing simulation, value 2: its own slots stand in for the
+     other ranks' in the all-gathers).
 2. Modeled: the per-step collectives of the real run, from their bytes at a stated
    NVLink bus bandwidth: per factor iteration one in-place reduce-scatter + one
    all-gather of every mode's factor rows (sum_k I_k * ldr * 4 bytes, (N-1)/N of it
    per rank each way) and a 2 d R^2 fp64 Gram all-reduce; per weight iteration an
-   R-vector all-reduce; per objective one fp64 -- latency-bound ones at LAT_US.
-3. Modeled: the same with the draw sharded by word range:
-   the write and probe passes (measured per launch at N = 1 from the launch list,
-   SHARDABLE_MS) divided by N, plus a reduce-scatter of 8-bit ordinal counters
-   (eta bytes) and a tiny all-gather of miss counts per draw.
+   R-vector all-reduce; per objective one fp64; per sharded draw the counter
+   reduce-scatter (eta / 2 bytes) and two small all-gathers -- latency-bound ones at
+   LAT_US.
 
     python scripts/shard_projection.py [N ...]  > profiles/r02_shard_projection.txt
 """
@@ -30,40 +33,27 @@ from paper_2110_14514_b200.synthetic import gen_slice  # noqa: E402
 
 BUS_GBS = 700.0   # assumed NCCL ring/NVLS bus bandwidth per GPU on NVSwitch (NVLink 5: 900 GB/s per direction)
 LAT_US = 15.0     # small-collective latency
-# per-draw c4 kernel time that word-range sharding divides by N (r02 launch list, ms):
-# k_draw_write<1> 0.483 + k_draw_write<3> 0.218 + k_zero_hits 0.320
-SHARDABLE_MS = 1.021
 
 
-def collectives_ms(world, ldr=32):
+def collectives_ms(world, sharded_draw, ldr=32):
     if world == 1:
         return 0.0
     rows = sum(bench.DIMS)
     grad = rows * ldr * 4 * (world - 1) / world / (BUS_GBS * 1e9) * 1e3  # one RS or AG, ms
     per_factor = 2 * grad + LAT_US / 1e3  # RS + AG of the rows + Gram all-reduce
     per_weight = LAT_US / 1e3
-    return 100 * per_factor + 100 * per_weight + 4 * LAT_US / 1e3
+    per_draw = 0.0
+    if sharded_draw:  # counters RS (eta / 2 bytes) + map / record all-gathers
+        per_draw = bench.NNZ / 2 * (world - 1) / world / (BUS_GBS * 1e9) * 1e3 + 3 * LAT_US / 1e3
+    return 100 * per_factor + 100 * per_weight + 200 * per_draw + 4 * LAT_US / 1e3
 
 
-def sharded_draw_saving_ms(world):
-    if world == 1:
-        return 0.0
-    eta = bench.NNZ
-    rs = eta * (world - 1) / world / (BUS_GBS * 1e9) * 1e3  # 8-bit counters to the ordinal owners
-    per_draw = SHARDABLE_MS * (1 - 1 / world) - rs - LAT_US / 1e3
-    return 200 * per_draw  # one draw per weight and per factor iteration
-
-
-def main(worlds):
-    X, factors, mix, total = gen_slice(bench.DIMS, bench.NNZ, bench.RANK, "poisson", seed=42)
-    cfg = bench.make_cfg(P)
-    loss = P.make_loss("poisson")
+def measure(P, X, factors, mix, total, cfg, loss, world, shard_draws):
     L, ctx = _lib.lib(), _lib.ctx()
-    base = None
-    rows = []
-    for world in worlds:
-        st = bench.make_state(P, X, factors, mix, total, cfg, loss, seed=11)
-        _lib.set_shard_sim(0, world)
+    st = bench.make_state(P, X, factors, mix, total, cfg, loss, seed=11)
+    _lib.set_shard_sim(0, world)
+    _lib.set_shard_draws(shard_draws)
+    try:
         for _ in range(2):
             P.process_slice(st, X, loss, cfg, exact_loss=False)
         torch.cuda.synchronize()
@@ -81,22 +71,35 @@ def main(worlds):
             L.ogcp_ctx_profile_read(ctx, cls, C.byref(n), C.byref(tms))
             prof[name] = round(tms.value / 2, 1)
         L.ogcp_ctx_profile_enable(ctx, 0)
+    finally:
         _lib.set_shard_sim(0, 1)
-        step = e0.elapsed_time(e1) / 2
-        coll = collectives_ms(world)
-        now = step + coll
-        sharded = max(now - sharded_draw_saving_ms(world), 0.0)
-        base = base or now
-        row = {"N": world, "rank0_step_ms_measured": round(step, 1), "collectives_ms_modeled": round(coll, 1),
-               "step_ms_current_design": round(now, 1), "speedup_current": round(base / now, 2),
-               "step_ms_with_sharded_draw": round(sharded, 1), "speedup_with_sharded_draw": round(base / sharded, 2),
-               "per_step_bracket_ms": prof}
-        rows.append(row)
+        _lib.set_shard_draws(1)
+    del st
+    torch.cuda.empty_cache()
+    return e0.elapsed_time(e1) / 2, prof
+
+
+def main(worlds):
+    X, factors, mix, total = gen_slice(bench.DIMS, bench.NNZ, bench.RANK, "poisson", seed=42)
+    cfg = bench.make_cfg(P)
+    loss = P.make_loss("poisson")
+    base = None
+    for world in worlds:
+        row = {"N": world}
+        for tag, mode in (("replicated_draw", 0), ("sharded_draw", 2)):
+            if world == 1 and mode:
+                continue
+            step, prof = measure(P, X, factors, mix, total, cfg, loss, world, mode)
+            coll = collectives_ms(world, mode != 0)
+            now = step + coll
+            base = base or now
+            row[tag] = {"rank0_step_ms_measured": round(step, 1), "collectives_ms_modeled": round(coll, 1),
+                        "step_ms": round(now, 1), "speedup": round(base / now, 2), "per_step_bracket_ms": prof}
         print(json.dumps(row), flush=True)
     print(json.dumps({"assumptions": {"bus_gbs": BUS_GBS, "small_collective_latency_us": LAT_US,
-                                      "shardable_draw_ms_per_draw": SHARDABLE_MS,
                                       "note": "projection: rank-0 kernels measured on one B200 in shard-simulation "
-                                              "mode; collectives and the sharded draw modeled from bytes"}}))
+                                              "mode (draw collectives' data stood in by rank 0's own slots); "
+                                              "collectives modeled from bytes"}}))
 
 
 if __name__ == "__main__":

@@ -93,6 +93,42 @@ def test_c4_merged_counts_equal_bincount(c4, buckets, sort_zeros):
     assert np.array_equal(z, zeros)
 
 
+@pytest.mark.parametrize("world", [4, 8])
+def test_c4_word_sharded_draw_partitions_bincount(c4, world):
+    """The multi-GPU draw sharded by RNG word range (OGCP_OPT_SHARD_DRAWS), at the bench
+    scale: each of `world` simulated ranks generates its 1/world of the words, the tile
+    maps / zero-row records are all-gathered and the nibble counters reduce-scattered
+    (exact device-side stand-ins on this GPU).  Rank r's merged set holds exactly the
+    np.bincount entries of its own ordinal chunk, and the ranks' zero rows, in rank
+    order, are the reference's accepted zero rows in draw order."""
+    X, lin = c4
+    ords, zeros = numpy_draw(lin, NNZ, Q, 7, KEY)
+    counts = np.bincount(ords, minlength=NNZ)
+    del ords
+    cw = (-(-NNZ // 8) + world - 1) // world
+    zparts = []
+    _lib.set_buckets(4)
+    try:
+        for r in range(world):
+            _lib.set_shard_sim(r, world)
+            o, c, z = _lib.debug_solve_draw(X, 7, KEY, None, Q, ldr=32)
+            lo, hi = min(8 * cw * r, NNZ), min(8 * cw * (r + 1), NNZ)
+            order = np.argsort(o, kind="stable")
+            o, c = o[order], c[order]
+            nzr = lo + np.flatnonzero(counts[lo:hi])
+            assert np.array_equal(o, nzr), r
+            assert np.array_equal(c, counts[nzr]), r
+            zparts.append(z)
+    finally:
+        _lib.set_shard_sim(0, 1)
+        _lib.set_buckets(1)
+    z = np.concatenate(zparts)
+    assert np.array_equal(z, zeros)
+    # the rows are split roughly evenly (word ranges of equal length)
+    sizes = np.array([len(p_) for p_ in zparts])
+    assert sizes.min() > 0.8 * Q / world and sizes.max() < 1.2 * Q / world
+
+
 def test_c4_factor_gradient_tma_walk_matches_generic(c4):
     """The bench-scale K3 walk: one factor iteration at rate ~0 (u = (1 - b1) g) on the c4
     slice (p = all, q = 2^24, R = 32, row-bucketed merged set) with the TMA-fed

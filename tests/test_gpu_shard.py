@@ -1,9 +1,12 @@
 """The multi-GPU shard partition, checked in one process: a context put in
 shard-simulation mode (OGCP_OPT_SHARD_SIM, no communicator) runs exactly the
 share of rank r of a world-N solve.  For merged (count-form) gradient draws --
-with and without the row-bucketed layout -- the ranks' nonzero shares (their
-own ordinal ranges) and zero-row shares must partition the single-GPU set
-exactly; for plain draws the contiguous split must too."""
+with and without the row-bucketed layout, replicated or sharded by RNG word
+range (OGCP_OPT_SHARD_DRAWS: the simulation then runs every rank's part in lock
+step with exact device-side stand-ins for the all-gathers / reduce-scatter) --
+the ranks' nonzero shares (their own ordinal ranges) and zero-row shares must
+partition the single-GPU set exactly; for plain draws the contiguous split must
+too."""
 
 import numpy as np
 import pytest
@@ -33,24 +36,33 @@ def _draw(X, p, q, world=1, rank=0):
         _lib.set_shard_sim(0, 1)
 
 
+def owner_range(eta, r, world):
+    """shard_owner_range: chunks of whole nibble words (8 ordinals) per rank."""
+    cw = (-(-eta // 8) + world - 1) // world
+    return min(8 * cw * r, eta), min(8 * cw * (r + 1), eta)
+
+
+@pytest.mark.parametrize("shard_draws", [0, 1])
 @pytest.mark.parametrize("buckets", [1, 4])
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_merged_draw_shards_partition(slice_1e5, buckets, world):
+def test_merged_draw_shards_partition(slice_1e5, buckets, world, shard_draws):
     X = slice_1e5
     _lib.set_buckets(buckets)
+    _lib.set_shard_draws(shard_draws)
     try:
         o, c, z = _draw(X, None, 4000)  # p = all: merged form
         assert c.sum() == X.nnz and len(z) == 4000
         parts = [_draw(X, None, 4000, world, r) for r in range(world)]
     finally:
         _lib.set_buckets(1)
+        _lib.set_shard_draws(1)
     po = np.concatenate([q[0] for q in parts])
     pc = np.concatenate([q[1] for q in parts])
     a, b = np.argsort(o, kind="stable"), np.argsort(po, kind="stable")
     np.testing.assert_array_equal(po[b], o[a])
     np.testing.assert_array_equal(pc[b], c[a])
     for r, (ro, _, _) in enumerate(parts):  # each rank holds its own ordinal range
-        lo, hi = X.nnz * r // world, X.nnz * (r + 1) // world
+        lo, hi = owner_range(X.nnz, r, world)
         assert ro.size == 0 or (ro.min() >= lo and ro.max() < hi)
     np.testing.assert_array_equal(np.concatenate([q[2] for q in parts]), z)
 
@@ -63,8 +75,9 @@ def test_plain_draw_shards_partition(slice_1e5):
     np.testing.assert_array_equal(np.concatenate([q[2] for q in parts]), z)
 
 
+@pytest.mark.parametrize("shard_draws", [0, 1])
 @pytest.mark.parametrize("R", [6, 20])
-def test_sharded_gradients_sum_to_single_gpu(slice_1e5, R):
+def test_sharded_gradients_sum_to_single_gpu(slice_1e5, R, shard_draws):
     """Shard-simulated factor solves of one iteration with rate ~0: every rank's
     K3 output is its partial gradient, so the per-rank first Adam moments
     (u = (1-b1) g) must sum to the single-GPU one (R = 20: the lean 3-way walks)."""
@@ -78,6 +91,7 @@ def test_sharded_gradients_sum_to_single_gpu(slice_1e5, R):
 
     def u_of(world, rank):
         _lib.set_shard_sim(rank, world)
+        _lib.set_shard_draws(shard_draws)
         try:
             model = P.DeviceModel.from_numpy(init)
             adam = cfg.make_adam(cfg.rate_factors, loss)
@@ -87,6 +101,7 @@ def test_sharded_gradients_sum_to_single_gpu(slice_1e5, R):
             return [t[:, :R].double().cpu().numpy() for t in adam._buf["u"]]
         finally:
             _lib.set_shard_sim(0, 1)
+            _lib.set_shard_draws(1)
 
     full = u_of(1, 0)
     for world in (2, 4):
