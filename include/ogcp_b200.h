@@ -151,10 +151,14 @@ int ogcp_ctx_profile_reset(ogcp_ctx* ctx);
  * random-access mode in row-bucket order (Slice bucketed copy, built once per
  * slice) so the bucket's factor/gradient rows stay L2-resident; a value k > 1
  * forces k buckets on every merged solve (tests). */
-/* OGCP_OPT_SHARD_SIM: value = rank | world << 16 on a context without a
- * communicator -- the solves then run rank `rank`'s share of a world-`world`
- * multi-GPU solve with the collectives skipped (single-process tests of the
- * shard partition); world 1 (or 0) restores the single-GPU context. */
+/* OGCP_OPT_SHARD_SIM: value = rank | world << 16 | timing << 32 on a context
+ * without a communicator -- the solves then run rank `rank`'s share of a
+ * world-`world` multi-GPU solve with the collectives skipped (single-process
+ * tests of the shard partition); world 1 (or 0) restores the single-GPU context.
+ * timing = 1: a timing simulation -- every collective is replaced by a stand-in
+ * kernel holding 24 SMs for its modeled time (15 us + ring bytes at 700 GB/s) and
+ * the sharded draws run only this rank's part, its own slots standing in for the
+ * other ranks' (results then inexact; for projections only). */
 /* OGCP_OPT_SORT_ZEROS (default 0): in a bucketed merged solve, the accepted zero
  * rows of every draw are sorted (stable radix sort) by (row bucket, mode-0 row) so
  * the zero part of the walk meets the same L2-resident bucket rows and streams
@@ -163,14 +167,14 @@ enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 
        OGCP_OPT_SORT_ZEROS = 5, OGCP_OPT_LEAN_WALKS = 6, OGCP_OPT_TMA_WALKS = 7,
        OGCP_OPT_BATCH_DRAWS = 8, OGCP_OPT_UMMA_GRAM = 9, OGCP_OPT_DETERMINISTIC = 10,
        OGCP_OPT_SHARD_DRAWS = 11 };
-/* OGCP_OPT_SHARD_DRAWS (default 1): in a multi-GPU solve (2..8 ranks) the merged
+/* OGCP_OPT_SHARD_DRAWS (default 1): in a multi-GPU solve the merged
  * gradient draws of slices whose modes all exceed 1 are sharded by RNG word
  * range -- each rank generates 1/world of the words; tile maps, per-rank zero-row
  * records and the nibble counters (reduce-scattered to the ordinal owners) are
  * exchanged on a second communicator -- so no rank replays the whole stream; 0
- * keeps every rank generating every word.  In shard simulation (OGCP_OPT_SHARD_SIM)
- * 1 runs every rank's part on this GPU with exact device-side exchanges; 2 runs
- * only this rank's part, its own slots standing in for the others' (timing). */
+ * keeps every rank generating every word.  In an exact shard simulation
+ * (OGCP_OPT_SHARD_SIM) every rank's part runs on this GPU in lock step with exact
+ * device-side stand-ins for the exchanges. */
 /* OGCP_OPT_DETERMINISTIC (default 0): for small models (sum of mode sizes x ldr
  * <= 4096, one GPU) the factor-gradient scatter adds in a fixed order (per-warp
  * shared-memory copies, groups in turn, fixed-order block and grid sums), so a

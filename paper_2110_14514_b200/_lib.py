@@ -243,9 +243,11 @@ def set_buckets(value):
     check(lib().ogcp_ctx_set_option(ctx(), 3, int(value)))
 
 
-def set_shard_sim(rank: int, world: int):
-    """OGCP_OPT_SHARD_SIM: run this context as rank `rank` of `world` without a communicator (tests)."""
-    check(lib().ogcp_ctx_set_option(ctx(), 4, int(rank) | (int(world) << 16)))
+def set_shard_sim(rank: int, world: int, timing: bool = False):
+    """OGCP_OPT_SHARD_SIM: run this context as rank `rank` of `world` without a communicator
+    (tests); `timing`: collectives replaced by stand-in kernels of their modeled duration and
+    sharded draws run for this rank only (projections; results inexact)."""
+    check(lib().ogcp_ctx_set_option(ctx(), 4, int(rank) | (int(world) << 16) | (int(bool(timing)) << 32)))
 
 
 def debug_solve_draw(X, seed: int, key, p, q: int, ldr: int, max_rejects=None):
@@ -264,11 +266,10 @@ def debug_solve_draw(X, seed: int, key, p, q: int, ldr: int, max_rejects=None):
     return ords[:nn.value].astype(np.int64), cnts[:nn.value].astype(np.int64), zeros[:nz.value].astype(np.int64)
 
 
-def set_shard_draws(mode):
+def set_shard_draws(on):
     """Engine option OGCP_OPT_SHARD_DRAWS: multi-GPU merged draws sharded by RNG word range
-    (0 off: every rank replays the whole stream; 1 on; 2 on, shard simulation runs only this
-    rank's part -- timing)."""
-    check(lib().ogcp_ctx_set_option(ctx(), 11, int(mode)))
+    (0: every rank replays the whole stream)."""
+    check(lib().ogcp_ctx_set_option(ctx(), 11, int(bool(on))))
 
 
 def set_sort_zeros(mode):

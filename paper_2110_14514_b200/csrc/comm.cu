@@ -91,16 +91,43 @@ __global__ void k_flags_unpack(DevFlags* f, const long long* pk) {
   f->data_bits = (pk[4] ? 1u : 0u) | (pk[5] ? 2u : 0u) | (pk[6] ? kMergeOverflowBit : 0u);
 }
 
+// Timing shard simulation: a collective's stand-in -- kStandinCtas CTAs (the SMs an
+// NCCL ring / NVLS kernel holds) spin on the global timer for the modeled time.
+constexpr int kStandinCtas = 24;
+__global__ void k_comm_standin(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(256);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 }  // namespace
+
+// Modeled time of a collective moving `moved` bytes per rank (ring schedule:
+// all-reduce 2 (N-1)/N of the buffer, reduce-scatter / all-gather (N-1)/N of the
+// full buffer) plus a fixed latency; enqueued as k_comm_standin in a timing shard
+// simulation, nothing otherwise.
+void comm_standin(Ctx* ctx, double moved) {
+  if (!ctx->shard_sim || !ctx->shard_sim_timing || ctx->world <= 1) return;
+  const double ns = ctx->sim_lat_us * 1e3 + moved / (ctx->sim_bus_gbs * 1e9) * 1e9;
+  k_comm_standin<<<kStandinCtas, 32, 0, ctx->stream>>>((unsigned long long)ns);
+  ctx->count();
+}
+
+static double ring_share(const Ctx* ctx) { return (double)(ctx->world - 1) / ctx->world; }
 
 // (no communicator with world > 1: single-process shard simulation, sums are the caller's)
 void comm_allreduce_sum(Ctx* ctx, float* p, size_t n) {
-  if (ctx->world <= 1 || n == 0 || !ctx->comm) return;
+  if (ctx->world <= 1 || n == 0) return;
+  if (!ctx->comm) return comm_standin(ctx, 2.0 * ring_share(ctx) * 4.0 * n);
   nccl_check(api().AllReduce(p, p, n, ncclFloat32, ncclSum, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");
 }
 
 void comm_allreduce_sum(Ctx* ctx, double* p, size_t n) {
-  if (ctx->world <= 1 || n == 0 || !ctx->comm) return;
+  if (ctx->world <= 1 || n == 0) return;
+  if (!ctx->comm) return comm_standin(ctx, 2.0 * ring_share(ctx) * 8.0 * n);
   nccl_check(api().AllReduce(p, p, n, ncclFloat64, ncclSum, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");
 }
 
@@ -118,7 +145,12 @@ void comm_row_range(int64_t rows, int rank, int world, int64_t* lo, int64_t* hi)
 // Both forms move the bytes of one allreduce but leave the row update between
 // them to the owner alone; all calls of a step go out as one NCCL group.
 static void rows_group(Ctx* ctx, float* const* bufs, const int64_t* rows, int nbuf, int ldr, bool reduce) {
-  if (ctx->world <= 1 || !ctx->comm) return;
+  if (ctx->world <= 1) return;
+  if (!ctx->comm) {
+    double bytes = 0.0;
+    for (int k = 0; k < nbuf; ++k) bytes += (double)rows[k] * ldr * 4.0;
+    return comm_standin(ctx, ring_share(ctx) * bytes);
+  }
   NcclApi& a = api();
   ncclComm_t comm = (ncclComm_t)ctx->comm;
   const int W = ctx->world;
@@ -155,7 +187,8 @@ void comm_gather_rows(Ctx* ctx, float* const* bufs, const int64_t* rows, int nbu
 }
 
 void comm_sync_flags(Ctx* ctx) {
-  if (ctx->world <= 1 || !ctx->comm) return;
+  if (ctx->world <= 1) return;
+  if (!ctx->comm) return comm_standin(ctx, 0.0);
   long long* pk = static_cast<long long*>(ctx->flagpack.ensure(8 * sizeof(long long)));
   k_flags_pack<<<1, 1, 0, ctx->stream>>>(ctx->flags.as<DevFlags>(), pk);
   nccl_check(api().AllReduce(pk, pk, 4, ncclInt64, ncclMin, (ncclComm_t)ctx->comm, ctx->stream), "ncclAllReduce");
@@ -170,26 +203,29 @@ void comm_sync_flags(Ctx* ctx) {
 // draw's collectives on the side stream never interleave with the solve's on the
 // context stream within one communicator
 void comm_draw_group(Ctx* ctx, bool begin) {
-  if (!ctx->comm_draw) return;
+  if (!ctx->comm_draw) return;  // (no stand-in: the group's members stand in for themselves)
   nccl_check(begin ? api().GroupStart() : api().GroupEnd(), "ncclGroup");
 }
 
 void comm_draw_allgather(Ctx* ctx, void* buf, size_t bytes) {
-  if (!ctx->comm_draw || bytes == 0) return;
+  if (bytes == 0) return;
+  if (!ctx->comm_draw) return comm_standin(ctx, ring_share(ctx) * bytes * ctx->world);
   char* b = static_cast<char*>(buf);
   nccl_check(api().AllGather(b + bytes * ctx->rank, b, bytes, ncclUint8, (ncclComm_t)ctx->comm_draw, ctx->stream),
              "ncclAllGather");
 }
 
 void comm_draw_reduce_scatter_u32(Ctx* ctx, uint32_t* buf, size_t words) {
-  if (!ctx->comm_draw || words == 0) return;
+  if (words == 0) return;
+  if (!ctx->comm_draw) return comm_standin(ctx, ring_share(ctx) * 4.0 * words * ctx->world);
   nccl_check(api().ReduceScatter(buf, buf + words * ctx->rank, words, ncclUint32, ncclSum,
                                  (ncclComm_t)ctx->comm_draw, ctx->stream),
              "ncclReduceScatter");
 }
 
 void comm_draw_allreduce_u64(Ctx* ctx, unsigned long long* buf, size_t n) {
-  if (!ctx->comm_draw || n == 0) return;
+  if (n == 0) return;
+  if (!ctx->comm_draw) return comm_standin(ctx, 2.0 * ring_share(ctx) * 8.0 * n);
   nccl_check(api().AllReduce(buf, buf, n, ncclUint64, ncclSum, (ncclComm_t)ctx->comm_draw, ctx->stream),
              "ncclAllReduce");
 }

@@ -25,6 +25,9 @@ void comm_draw_group(Ctx* ctx, bool begin);
 void comm_draw_allgather(Ctx* ctx, void* buf, size_t bytes);
 void comm_draw_reduce_scatter_u32(Ctx* ctx, uint32_t* buf, size_t words);
 void comm_draw_allreduce_u64(Ctx* ctx, unsigned long long* buf, size_t n);
+// Timing shard simulation (no communicator): enqueue a stand-in for a collective that
+// moves `moved` bytes per rank -- its modeled time on the SMs an NCCL kernel holds.
+void comm_standin(Ctx* ctx, double moved);
 void comm_init(Ctx* ctx, const uint8_t* id, int rank, int world);
 void comm_unique_id(uint8_t* out128);
 void comm_destroy(Ctx* ctx);

@@ -193,7 +193,10 @@ struct Ctx {
   void* comm = nullptr;         // ncclComm_t
   void* comm_draw = nullptr;    // ncclComm_t split from comm: the sharded draws' exchanges (side stream)
   bool shard_draws = true;      // multi-GPU merged draws sharded by word range (sampler.cu shard_draw_enqueue)
-  bool shard_sim_timing = false;  // shard simulation of sharded draws: this rank's part only (timing)
+  bool shard_sim_timing = false;  // timing shard simulation: draws' exchanges stood in by this rank's own
+                                  // slots, every collective by a stand-in kernel for its modeled duration
+  double sim_bus_gbs = 700.0;     // stand-in collectives: NVLink bus bandwidth per GPU
+  double sim_lat_us = 15.0;       // ... and per-collective latency
   int rank = 0, world = 1;
   DevBuf flagpack;
   // scratch

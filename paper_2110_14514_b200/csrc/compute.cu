@@ -679,10 +679,35 @@ __global__ void __launch_bounds__(kThreads) k_exact_cells(ModelP M, const float*
   }
 }
 
-__global__ void k_sum_partials_vec(const double* __restrict__ p, int nblk, int len, double* __restrict__ out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < len; c += gridDim.x * blockDim.x) {
+// Fixed-order column sums of block partials, spread over threads: a 256-thread
+// block takes 32 columns x 8 segments; segment s sums blocks s, s + 8, ... in
+// order (two interleaved accumulators), then the 8 segment sums combine in order.
+// The order depends only on nblk, so the result is deterministic; a column's
+// chain is nblk / 16 loads long instead of nblk.
+constexpr int kColSumSegs = 8;
+template <typename T>
+__device__ __forceinline__ double seg_colsum(const T* __restrict__ p, int nblk, int64_t stride, int64_t off,
+                                             int seg) {
+  double t0 = 0.0, t1 = 0.0;
+  int b = seg;
+  for (; b + kColSumSegs < nblk; b += 2 * kColSumSegs) {
+    t0 += (double)__ldg(p + (int64_t)b * stride + off);
+    t1 += (double)__ldg(p + (int64_t)(b + kColSumSegs) * stride + off);
+  }
+  if (b < nblk) t0 += (double)__ldg(p + (int64_t)b * stride + off);
+  return t0 + t1;
+}
+
+__global__ void __launch_bounds__(256) k_sum_partials_vec(const double* __restrict__ p, int nblk, int len,
+                                                          double* __restrict__ out) {
+  __shared__ double seg[kColSumSegs][32];
+  const int lane = threadIdx.x & 31, sg = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  seg[sg][lane] = c < len ? seg_colsum(p, nblk, len, c, sg) : 0.0;
+  __syncthreads();
+  if (sg == 0 && c < len) {
     double t = 0.0;
-    for (int b = 0; b < nblk; ++b) t += p[(int64_t)b * len + c];
+    for (int j = 0; j < kColSumSegs; ++j) t += seg[j][lane];
     out[c] = t;
   }
 }
@@ -1040,21 +1065,24 @@ void gram_small_enqueue(Ctx* ctx, const SmallGrams& g, int ndim, int rank, int l
 
 // Sum block partials (fixed order) and extract the rank x rank blocks.
 template <typename T>
-__global__ void k_gram_finalize(const T* __restrict__ partials, int nblk, int ngram, int ldr, int rank,
-                                double* __restrict__ outP, double* __restrict__ outC) {
+__global__ void __launch_bounds__(256) k_gram_finalize(const T* __restrict__ partials, int nblk, int ngram, int ldr,
+                                                       int rank, double* __restrict__ outP,
+                                                       double* __restrict__ outC) {
+  // 32 entries x 8 fixed-order segments per block (seg_colsum)
+  __shared__ double seg[kColSumSegs][32];
   const int LL = ldr * ldr;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ngram * rank * rank; e += gridDim.x * blockDim.x) {
-    const int g = e / (rank * rank);
-    const int ij = e % (rank * rank);
-    const int i = ij / rank, j = ij % rank;
-    double t0 = 0.0, t1 = 0.0;  // fixed order: even / odd blocks, then combined
-    int b = 0;
-    for (; b + 1 < nblk; b += 2) {
-      t0 += (double)partials[((int64_t)b * ngram + g) * LL + i * ldr + j];
-      t1 += (double)partials[((int64_t)(b + 1) * ngram + g) * LL + i * ldr + j];
-    }
-    if (b < nblk) t0 += (double)partials[((int64_t)b * ngram + g) * LL + i * ldr + j];
-    (g == 0 ? outP : outC)[ij] = t0 + t1;
+  const int lane = threadIdx.x & 31, sg = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  const bool live = e < ngram * rank * rank;
+  const int g = live ? e / (rank * rank) : 0;
+  const int ij = live ? e % (rank * rank) : 0;
+  const int i = ij / rank, j = ij % rank;
+  seg[sg][lane] = live ? seg_colsum(partials, nblk, (int64_t)ngram * LL, (int64_t)g * LL + i * ldr + j, sg) : 0.0;
+  __syncthreads();
+  if (sg == 0 && live) {
+    double t = 0.0;
+    for (int k = 0; k < kColSumSegs; ++k) t += seg[k][lane];
+    (g == 0 ? outP : outC)[ij] = t;
   }
 }
 
@@ -2045,7 +2073,7 @@ int exact_cells_enqueue(Ctx* ctx, const ModelP& M, const float* s_f, const LossP
 }
 
 void sum_partials_enqueue(Ctx* ctx, const double* partials, int nblk, int len, double* out) {
-  k_sum_partials_vec<<<std::max(1, std::min(ceil_div_i(len, 256), 64)), 256, 0, ctx->stream>>>(partials, nblk, len,
+  k_sum_partials_vec<<<std::max(1, ceil_div_i(len, 32)), 256, 0, ctx->stream>>>(partials, nblk, len,
                                                                                                out);
   ctx->count();
   check_launch();
@@ -2086,7 +2114,7 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
     ProfScope prof_scope(ctx, kProfGram);
     kern<<<nblk, umma::kThreadsG, umma::kSmemG, ctx->stream>>>(maps, rows, ngram, scratch.as<float>());
     ctx->count();
-    k_gram_finalize<float><<<std::max(1, ceil_div_i((int64_t)ngram * rank * rank, 256)), 256, 0, ctx->stream>>>(
+    k_gram_finalize<float><<<std::max(1, ceil_div_i((int64_t)ngram * rank * rank, 32)), 256, 0, ctx->stream>>>(
         scratch.as<float>(), nblk, ngram, ldr, rank, outP, outC);
     ctx->count();
     check_launch();
@@ -2103,7 +2131,7 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
       ProfScope prof_scope(ctx, kProfGram);
       kern<<<nblk, kThreads, smem, ctx->stream>>>(A, B ? B : A, rows, rpb, ngram, scratch.as<double>());
       ctx->count();
-      k_gram_finalize<double><<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
+      k_gram_finalize<double><<<std::max(1, ceil_div_i((int64_t)ngram * rank * rank, 32)), 256, 0,
                         ctx->stream>>>(scratch.as<double>(), nblk, ngram, ldr, rank, outP, outC);
       ctx->count();
       check_launch();
@@ -2132,7 +2160,7 @@ void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int r
                                                    scratch.as<double>());
     ctx->count();
   }
-  k_gram_finalize<double><<<std::max(1, std::min(ceil_div_i((int64_t)ngram * rank * rank, 256), 64)), 256, 0,
+  k_gram_finalize<double><<<std::max(1, ceil_div_i((int64_t)ngram * rank * rank, 32)), 256, 0,
                     ctx->stream>>>(scratch.as<double>(), nblk, ngram, ldr, rank, outP, outC);
   ctx->count();
   check_launch();

@@ -1516,10 +1516,7 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   else if (option == OGCP_OPT_UMMA_GRAM) ctx->umma_gram = value != 0;
   else if (option == OGCP_OPT_DETERMINISTIC) ctx->deterministic = value != 0;
   else if (option == OGCP_OPT_LEAN_WALKS) ctx->lean_walks = value != 0;
-  else if (option == OGCP_OPT_SHARD_DRAWS) {
-    ctx->shard_draws = value != 0;
-    ctx->shard_sim_timing = value == 2;
-  }
+  else if (option == OGCP_OPT_SHARD_DRAWS) ctx->shard_draws = value != 0;
   else if (option == OGCP_OPT_TMA_WALKS) {
     ctx->tma_walks = (value & 1) != 0;
     ctx->tma_wgrad = (value & 2) != 0;
@@ -1527,11 +1524,13 @@ int ogcp_ctx_set_option(ogcp_ctx* ctx, int32_t option, int64_t value) {
   }
   else if (option == OGCP_OPT_SHARD_SIM) {
     if (ctx->comm) throw Error(OGCP_E_USAGE, "shard simulation needs a context without a communicator");
-    const int r = (int)(value & 0xffff), w = (int)(value >> 16);
+    const int r = (int)(value & 0xffff), w = (int)((value >> 16) & 0xffff);
+    ctx->shard_sim_timing = ((value >> 32) & 1) != 0;
     if (w < 1 || r >= w) {
       ctx->rank = 0;
       ctx->world = 1;
       ctx->shard_sim = false;
+      ctx->shard_sim_timing = false;
     } else {
       ctx->rank = r;
       ctx->world = w;

@@ -278,41 +278,88 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_count(StreamSpec sp, cons
   }
 }
 
-// Pass 2: exclusive scan of block aggregates (one block, tiles of kScanThreads)
-// -> per-block start (column, element offset); total elements emitted.
+// Pass 2 (one block of 1024 threads, one pass): thread t composes the maps of its
+// run of ceil(nblocks / 1024) consecutive tiles, a block scan of the run maps
+// (64-bit counts) gives every run its start (column, element), and each thread
+// then steps through its tiles writing their starts (the column after E
+// elements is E mod NCOL) -- one sweep, not nblocks / 256 dependent block scans.
+constexpr int kScanTilesThreads = 1024;
 template <int NCOL>
-__global__ void __launch_bounds__(kScanThreads) k_draw_scan_blocks(const uint32_t* __restrict__ bagg, int64_t nblocks,
-                                                                   long long* __restrict__ bstart,
-                                                                   long long* __restrict__ total_out) {
-  __shared__ long long carry_elem;
-  __shared__ int carry_col;
-  if (threadIdx.x == 0) { carry_elem = 0; carry_col = 0; }
-  __syncthreads();
-  for (int64_t base = 0; base < nblocks; base += kScanThreads) {
-    const int64_t b = base + threadIdx.x;
-    Map<NCOL> m = identity_map<NCOL>();
-    if (b < nblocks) {
+struct Map64 {
+  unsigned long long c[NCOL];
+};
+template <int NCOL>
+__device__ __forceinline__ Map64<NCOL> compose64(const Map64<NCOL>& f, const Map64<NCOL>& g) {
+  Map64<NCOL> h;
 #pragma unroll
-      for (int c = 0; c < NCOL; ++c) m.c[c] = bagg[b * NCOL + c];
-    }
-    Map<NCOL> excl, agg;
-    block_scan_maps<NCOL>(m, excl, agg);
-    const long long ce = carry_elem;
-    const int cc = carry_col;
-    if (b < nblocks) {
-      const uint32_t adv = map_at<NCOL>(excl, cc);
-      bstart[b * 2 + 0] = (cc + adv) % NCOL;
-      bstart[b * 2 + 1] = ce + adv;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint32_t adv = map_at<NCOL>(agg, cc);
-      carry_elem = ce + adv;
-      carry_col = (int)((cc + adv) % NCOL);
-    }
-    __syncthreads();
+  for (int c = 0; c < NCOL; ++c) {
+    const unsigned long long adv = f.c[c];
+    const int cc = (int)((c + adv) % NCOL);
+    unsigned long long gv = g.c[0];
+#pragma unroll
+    for (int j = 1; j < NCOL; ++j)
+      if (j == cc) gv = g.c[j];
+    h.c[c] = adv + gv;
   }
-  if (threadIdx.x == 0) *total_out = carry_elem;
+  return h;
+}
+
+template <int NCOL>
+__global__ void __launch_bounds__(kScanTilesThreads) k_draw_scan_tiles(const uint32_t* __restrict__ bagg,
+                                                                       int64_t nblocks, long long* __restrict__ bstart,
+                                                                       long long* __restrict__ total_out) {
+  __shared__ unsigned long long wagg[kScanTilesThreads / 32][NCOL];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t per = (nblocks + kScanTilesThreads - 1) / kScanTilesThreads;
+  const int64_t b0 = min((int64_t)t * per, nblocks), b1 = min(b0 + per, nblocks);
+  Map64<NCOL> m;
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) m.c[c] = 0;
+  for (int64_t b = b0; b < b1; ++b) {
+    Map64<NCOL> tm;
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) tm.c[c] = __ldg(bagg + b * NCOL + c);
+    m = compose64<NCOL>(m, tm);
+  }
+  Map64<NCOL> inc = m;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    Map64<NCOL> o;
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) o.c[c] = __shfl_up_sync(0xffffffffu, inc.c[c], d);
+    if (lane >= d) inc = compose64<NCOL>(o, inc);
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) wagg[w][c] = inc.c[c];
+  }
+  __syncthreads();
+  Map64<NCOL> pre;
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) pre.c[c] = 0;
+  for (int j = 0; j < w; ++j) {
+    Map64<NCOL> a;
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) a.c[c] = wagg[j][c];
+    pre = compose64<NCOL>(pre, a);
+  }
+  Map64<NCOL> prev;
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) prev.c[c] = __shfl_up_sync(0xffffffffu, inc.c[c], 1);
+  const Map64<NCOL> excl = lane == 0 ? pre : compose64<NCOL>(pre, prev);
+  unsigned long long elem = excl.c[0];  // from column 0 at the stream start
+  int col = (int)(elem % NCOL);
+  for (int64_t b = b0; b < b1; ++b) {
+    bstart[b * 2 + 0] = col;
+    bstart[b * 2 + 1] = (long long)elem;
+    uint32_t adv = __ldg(bagg + b * NCOL);
+#pragma unroll
+    for (int j = 1; j < NCOL; ++j)
+      if (j == col) adv = __ldg(bagg + b * NCOL + j);
+    elem += adv;
+    col = (int)((col + adv) % NCOL);
+  }
+  if (t == kScanTilesThreads - 1) *total_out = (long long)elem;
 }
 
 // Pass 3: re-generate the words, stage accepted values in shared memory and
@@ -323,9 +370,7 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_scan_blocks(const uint32_
 // Word-range shards (sharded draws, below): b0 is the first tile of this rank's
 // range; lim_dev (nullable) lowers the element limit to *lim_dev and shift_dev
 // (nullable) writes element e at out[e - *shift_dev], dropping e < *shift_dev;
-// ocnt (nullable, merged form) counts the accepted draws per owner rank
-// (ordinal / ospan, at most kMaxDrawOwners owners) instead of `owned`.
-constexpr int kMaxDrawOwners = 8;
+// owned may be null (the sharded draw certifies its counters from their sums).
 template <int NCOL>
 __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, const long long* w0p, int64_t nchunks,
                                                              const uint8_t* __restrict__ tmaps,
@@ -336,14 +381,9 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
                                                              uint32_t olo, uint32_t ohi,
                                                              unsigned long long* __restrict__ owned,
                                                              int64_t b0 = 0, const long long* lim_dev = nullptr,
-                                                             const long long* shift_dev = nullptr,
-                                                             unsigned long long* __restrict__ ocnt = nullptr,
-                                                             uint32_t ospan = 1) {
-  __shared__ int32_t stage[kBlockWords];
+                                                             const long long* shift_dev = nullptr) {
+  extern __shared__ int32_t stage[];  // kBlockWords int32 (draw_stage_smem)
   uint32_t mine = 0;  // merged form: accepted draws landing in this rank's ordinal range [olo, ohi)
-  uint32_t oc[kMaxDrawOwners];
-#pragma unroll
-  for (int j = 0; j < kMaxDrawOwners; ++j) oc[j] = 0;
   const int64_t tile = b0 + blockIdx.x;
   const int64_t chunk = tile * kScanThreads + threadIdx.x;
   const int64_t lchunk = blockIdx.x * (int64_t)kScanThreads + threadIdx.x;
@@ -379,13 +419,7 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
           if (val >= olo && val < ohi) {
             const uint32_t o = val - olo;
             atomicAdd(hist + (o >> 3), 1u << ((o & 7u) << 2));
-            if (ocnt) {
-              const uint32_t own = val / ospan;
-#pragma unroll
-              for (int j = 0; j < kMaxDrawOwners; ++j) oc[j] += own == (uint32_t)j;
-            } else {
-              ++mine;
-            }
+            ++mine;
           }
         } else {
           stage[rel++] = (int32_t)val;
@@ -397,16 +431,7 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_write(StreamSpec sp, cons
     }
   }
   if (hist) {
-    if (ocnt) {
-#pragma unroll
-      for (int j = 0; j < kMaxDrawOwners; ++j) {
-        uint32_t v = oc[j];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0 && v) atomicAdd(ocnt + j, (unsigned long long)v);
-      }
-      return;
-    }
+    if (!owned) return;
 #pragma unroll
     for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(owned, (unsigned long long)mine);
@@ -1053,6 +1078,12 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_fused(StreamSpec sp, cons
   }
 }
 
+// Shared memory of a write pass: the output stage's footprint even in the merged
+// form, which does not use it -- a lean counter pass squeezes in beside the walk
+// kernels and slows them more than it gains (c4: 1414 vs 1392 ms per step at
+// N = 1, 241 vs 230 ms in the N = 8 projection).
+static int draw_stage_smem(bool /*merged_form*/) { return kBlockWords * 4; }
+
 template <int NCOL>
 static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int64_t target, int64_t words,
                        int32_t* out, long long* end_word, long long* elems_total, DrawScratch& scr,
@@ -1076,9 +1107,10 @@ static void run_stream(Ctx* ctx, const StreamSpec& sp, const long long* w0, int6
   cudaStream_t s = ctx->stream;
   k_draw_count<NCOL><<<(unsigned)nblocks, kScanThreads, 0, s>>>(sp, w0, nchunks, scr.tmaps.as<uint8_t>(),
                                                                scr.bagg.as<uint32_t>());
-  k_draw_scan_blocks<NCOL><<<1, kScanThreads, 0, s>>>(scr.bagg.as<uint32_t>(), nblocks, scr.bstart.as<long long>(),
+  k_draw_scan_tiles<NCOL><<<1, kScanTilesThreads, 0, s>>>(scr.bagg.as<uint32_t>(), nblocks, scr.bstart.as<long long>(),
                                                       elems_total);
-  k_draw_write<NCOL><<<(unsigned)nblocks, kScanThreads, 0, s>>>(sp, w0, nchunks, scr.tmaps.as<uint8_t>(),
+  k_draw_write<NCOL><<<(unsigned)nblocks, kScanThreads, draw_stage_smem(hist != nullptr), s>>>(sp, w0, nchunks,
+                                                                                              scr.tmaps.as<uint8_t>(),
                                                                scr.bstart.as<long long>(), target, out, end_word,
                                                                hist, ctx->flags.as<DevFlags>(), olo, ohi, owned);
   ctx->count(3);
@@ -1182,7 +1214,8 @@ static const int32_t* sort_zero_rows(Ctx* ctx, const Slice* X, DrawScratch& scr,
 // Σ counters = *owned (the draws that landed in the range); the distinct count
 // lands in sc[5] (merged->count), the counter sum in sc[7].
 static void merged_compact(Ctx* ctx, MergedDraw* merged, const uint32_t* counters, uint32_t olo, int64_t own,
-                           const unsigned long long* owned, long long* sc) {
+                           const unsigned long long* owned, long long* sc,
+                           unsigned long long* cnt_sum_out = nullptr) {
   cudaStream_t s = ctx->stream;
   const int64_t nwords = (own + 7) / 8;
   // (the caller sized merged->ord / cnt for min(p, own) entries)
@@ -1197,10 +1230,12 @@ static void merged_compact(Ctx* ctx, MergedDraw* merged, const uint32_t* counter
                                                    ((int64_t)kHistWordsPerThread * kScanThreads));
   merged->bcount.ensure((size_t)hblocks * 4);
   merged->boff.ensure((size_t)hblocks * 8);
-  unsigned long long* cnt_sum = reinterpret_cast<unsigned long long*>(sc + 7);
+  unsigned long long* cnt_sum = cnt_sum_out ? cnt_sum_out : reinterpret_cast<unsigned long long*>(sc + 7);
   k_hist_count<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, merged->bcount.as<uint32_t>(), cnt_sum);
-  k_hist_verify<<<1, 32, 0, s>>>(cnt_sum, owned, ctx->flags.as<DevFlags>());
-  ctx->count();
+  if (owned) {
+    k_hist_verify<<<1, 32, 0, s>>>(cnt_sum, owned, ctx->flags.as<DevFlags>());
+    ctx->count();
+  }
   k_zero_scan<<<1, 1024, 0, s>>>(merged->bcount.as<uint32_t>(), hblocks, merged->boff.as<long long>(), sc + 5);
   // positions (bucketed copy) are local; unbucketed ordinals are global
   k_hist_write<<<(unsigned)hblocks, kScanThreads, 0, s>>>(counters, nwords, own, merged->boff.as<long long>(),
@@ -1565,23 +1600,31 @@ __global__ void k_zshard_tail(StreamSpec sp, const long long* w0p, const long lo
 // it none.  Status as k_draw_status: a nonzero shortfall asks for a retry; with
 // fewer than q misses in all ranks' rows, more than `budget` hits is the
 // reference's SamplingError, else a shortfall.
+// The records also carry every owner's counter sum: all of them together must
+// be p (a wrapped nibble loses 16), else the merge-overflow bit sends the epoch
+// back to per-draw evaluation, as k_hist_verify does on one GPU (check_counts 0:
+// timing simulation, whose stand-in records do not add up).
+constexpr int kZrec = 3;  // (misses, rows, counter sum) per rank
 __global__ void __launch_bounds__(kScanThreads) k_zshard_cut(
     const long long* __restrict__ rec, int world, int rank, int64_t q, long long budget,
     const long long* __restrict__ zr, const uint32_t* __restrict__ bcount, const long long* __restrict__ boff,
     int64_t nblocks, const uint8_t* __restrict__ miss, int64_t lrows_max, long long* __restrict__ rows_used,
     long long* __restrict__ hits_before, const long long* __restrict__ nz_avail, int64_t p, long long code,
-    DevFlags* flags) {
+    int check_counts, DevFlags* flags) {
   __shared__ long long t_loc;
   __shared__ int holds;
   const bool nz_short = p > 0 && *nz_avail < p;
   if (threadIdx.x == 0) {
     long long before = 0, mt = 0, nt = 0;
+    unsigned long long drawn = 0;
     for (int s = 0; s < world; ++s) {
-      if (s < rank) before += rec[2 * s];
-      mt += rec[2 * s];
-      nt += rec[2 * s + 1];
+      if (s < rank) before += rec[kZrec * s];
+      mt += rec[kZrec * s];
+      nt += rec[kZrec * s + 1];
+      drawn += (unsigned long long)rec[kZrec * s + 2];
     }
-    const long long mine = rec[2 * rank], rows = rec[2 * rank + 1];
+    if (check_counts && !nz_short && drawn != (unsigned long long)p) atomicOr(&flags->data_bits, kMergeOverflowBit);
+    const long long mine = rec[kZrec * rank], rows = rec[kZrec * rank + 1];
     const long long t = q - before;
     *hits_before = 0;
     holds = 0;
@@ -1617,7 +1660,7 @@ void shard_owner_range(int64_t eta, int rank, int world, int64_t* olo, int64_t* 
 }
 
 bool shard_draw_eligible(const Ctx* ctx, const Slice* X, int64_t p, int64_t q, bool semi) {
-  if (!ctx->shard_draws || ctx->world < 2 || ctx->world > kMaxDrawOwners) return false;
+  if (!ctx->shard_draws || ctx->world < 2) return false;
   if (!ctx->comm_draw && !ctx->shard_sim) return false;
   if (semi || p <= 0 || q <= 0 || X->nnz < 2 || X->ndim > kMaxCols) return false;
   for (int k = 0; k < X->ndim; ++k)
@@ -1713,8 +1756,7 @@ void shard_alloc(const ShardPlan& pl, ShardScratch& sh, int d) {
   sh.bst_nz.ensure((size_t)pl.n_nblocks * 16);
   sh.bst_z.ensure((size_t)pl.z_nblocks * 16);
   sh.hist.ensure((size_t)W * pl.cw * 4);
-  sh.ocnt.ensure((size_t)kMaxDrawOwners * 8);
-  sh.zrec.ensure((size_t)W * 16);
+  sh.zrec.ensure((size_t)W * kZrec * 8);
   sh.scal.ensure(16 * 8);
   sh.cand.ensure((size_t)std::max<int64_t>(pl.lrows_max, 1) * d * 4);
   sh.miss.ensure((size_t)pl.lzblocks * kScanThreads);
@@ -1736,13 +1778,13 @@ void zero_tiles(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r, bool cou
     }
     return;
   }
-  k_draw_scan_blocks<NCOL><<<1, kScanThreads, 0, s>>>(sh.bagg_z.as<uint32_t>(), pl.z_nblocks, sh.bst_z.as<long long>(),
+  k_draw_scan_tiles<NCOL><<<1, kScanTilesThreads, 0, s>>>(sh.bagg_z.as<uint32_t>(), pl.z_nblocks, sh.bst_z.as<long long>(),
                                                       sc + 2);
   k_zshard_range<<<1, 1, 0, s>>>(sh.bst_z.as<long long>(), pl.z_nblocks, sc + 2, pl.z_target, pl.z_slot, r, pl.world,
-                                 NCOL, sc + 9, sh.zrec.as<long long>() + 2 * r + 1);
+                                 NCOL, sc + 9, sh.zrec.as<long long>() + kZrec * r + 1);
   ctx->count(2);
   if (nt > 0) {
-    k_draw_write<NCOL><<<(unsigned)nt, kScanThreads, 0, s>>>(
+    k_draw_write<NCOL><<<(unsigned)nt, kScanThreads, kBlockWords * 4, s>>>(
         pl.spz, sc + 0, pl.z_nchunks, sh.tm_z.as<uint8_t>(), sh.bst_z.as<long long>(), pl.z_target,
         sh.cand.as<int32_t>(), nullptr, nullptr, ctx->flags.as<DevFlags>(), 0u, 0u, nullptr, b0, sc + 13, sc + 12);
     ctx->count();
@@ -1768,7 +1810,7 @@ void zero_tiles_any(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r, bool
 void phase_count(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r) {
   cudaStream_t s = ctx->stream;
   OGCP_CUDA(cudaMemsetAsync(sh.scal.ptr, 0, 16 * 8, s));
-  OGCP_CUDA(cudaMemsetAsync(sh.ocnt.ptr, 0, (size_t)kMaxDrawOwners * 8, s));
+  OGCP_CUDA(cudaMemsetAsync(sh.zrec.ptr, 0, (size_t)pl.world * kZrec * 8, s));
   const int64_t b0 = (int64_t)r * pl.n_slot;
   const int64_t nt = std::max<int64_t>(0, std::min(pl.n_slot, pl.n_nblocks - b0));
   if (nt > 0) {
@@ -1783,7 +1825,7 @@ void phase_count(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r) {
 void phase_write(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r) {
   cudaStream_t s = ctx->stream;
   long long* sc = sh.scal.as<long long>();
-  k_draw_scan_blocks<1><<<1, kScanThreads, 0, s>>>(sh.bagg_nz.as<uint32_t>(), pl.n_nblocks, sh.bst_nz.as<long long>(),
+  k_draw_scan_tiles<1><<<1, kScanTilesThreads, 0, s>>>(sh.bagg_nz.as<uint32_t>(), pl.n_nblocks, sh.bst_nz.as<long long>(),
                                                    sc + 1);
   k_draw_locate_end<1><<<1, kScanThreads, 0, s>>>(pl.spn, nullptr, pl.n_nchunks, sh.bst_nz.as<long long>(),
                                                   pl.n_nblocks, sc + 1, pl.p, sc + 0);
@@ -1792,10 +1834,9 @@ void phase_write(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r) {
   const int64_t b0 = (int64_t)r * pl.n_slot;
   const int64_t nt = std::max<int64_t>(0, std::min(pl.n_slot, pl.n_nblocks - b0));
   if (nt > 0) {
-    k_draw_write<1><<<(unsigned)nt, kScanThreads, 0, s>>>(
+    k_draw_write<1><<<(unsigned)nt, kScanThreads, draw_stage_smem(true), s>>>(
         pl.spn, nullptr, pl.n_nchunks, sh.tm_nz.as<uint8_t>(), sh.bst_nz.as<long long>(), pl.p, nullptr, nullptr,
-        sh.hist.as<uint32_t>(), ctx->flags.as<DevFlags>(), 0u, (uint32_t)pl.eta, nullptr, b0, nullptr, nullptr,
-        sh.ocnt.as<unsigned long long>(), (uint32_t)(8 * pl.cw));
+        sh.hist.as<uint32_t>(), ctx->flags.as<DevFlags>(), 0u, (uint32_t)pl.eta, nullptr, b0);
     ctx->count();
   }
   zero_tiles_any(ctx, pl, sh, r, /*count=*/true);
@@ -1814,19 +1855,34 @@ void phase_zero(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r, const Sl
       sh.miss.as<uint8_t>(), sh.zcount.as<uint32_t>(), 0, nullptr, 1,
       X->filter_mask ? X->filter.as<unsigned int>() : nullptr, X->filter_mask);
   k_zero_scan<<<1, 1024, 0, s>>>(sh.zcount.as<uint32_t>(), pl.lzblocks, sh.zoff.as<long long>(),
-                                 sh.zrec.as<long long>() + 2 * r);
+                                 sh.zrec.as<long long>() + kZrec * r);
   ctx->count(2);
   check_launch();
 }
 
 enum class XMode { nccl, emulate, replicate };
 
+__global__ void k_replicate_slot(uint8_t* __restrict__ buf, int64_t bytes, int r, int world) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < bytes * world;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (i / bytes != r) buf[i] = buf[(int64_t)r * bytes + i % bytes];
+}
+
 // All-gather of per-rank slots of `bytes`: NCCL, the other ranks' buffers (exact
-// simulation), or this rank's own slot standing in for the others (timing simulation).
+// simulation), or this rank's own slot standing in for the others (timing
+// simulation, plus the collective's stand-in kernel).
 void xchg_allgather(Ctx* ctx, XMode xm, std::vector<ShardScratch*>& st, DevBuf ShardScratch::*mb, size_t bytes) {
   const int W = ctx->world, R = ctx->rank;
   if (xm == XMode::nccl) {
     comm_draw_allgather(ctx, (st[R]->*mb).ptr, bytes);
+    return;
+  }
+  if (xm == XMode::replicate) {
+    const int64_t n = (int64_t)bytes * W;
+    k_replicate_slot<<<(unsigned)std::min<int64_t>((n + 255) / 256, kNumSMs * 4), 256, 0, ctx->stream>>>(
+        static_cast<uint8_t*>((st[R]->*mb).ptr), (int64_t)bytes, R, W);
+    ctx->count();
+    comm_draw_allgather(ctx, nullptr, bytes);  // no draw communicator: the stand-in
     return;
   }
   for (int s = 0; s < W; ++s) {
@@ -1874,38 +1930,51 @@ DrawOut shard_draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, 
   if (xm == XMode::nccl) {
     comm_draw_group(ctx, true);
     comm_draw_reduce_scatter_u32(ctx, sh.hist.as<uint32_t>(), (size_t)pl.cw);
-    comm_draw_allreduce_u64(ctx, sh.ocnt.as<unsigned long long>(), (size_t)W);
     comm_draw_allgather(ctx, sh.bagg_z.ptr, (size_t)pl.z_slot * pl.ncol * 4);
     comm_draw_group(ctx, false);
   } else {
-    if (xm == XMode::emulate)
-      for (int o = 0; o < W; ++o) {
-        if (o == R) continue;
-        k_add_into<uint32_t><<<kNumSMs * 4, 256, 0, s>>>(sh.hist.as<uint32_t>() + (size_t)R * pl.cw,
-                                                         st[o]->hist.as<uint32_t>() + (size_t)R * pl.cw, pl.cw);
-        k_add_into<unsigned long long><<<1, 32, 0, s>>>(sh.ocnt.as<unsigned long long>(),
-                                                        st[o]->ocnt.as<unsigned long long>(), W);
-        ctx->count(2);
-      }
+    if (xm == XMode::replicate) comm_draw_reduce_scatter_u32(ctx, nullptr, (size_t)pl.cw);  // the stand-in
+    if (xm == XMode::emulate)  // every rank's chunk summed over the ranks (the reduce-scatter)
+      for (int r = 0; r < W; ++r)
+        for (int o = 0; o < W; ++o) {
+          if (o == r) continue;
+          k_add_into<uint32_t><<<kNumSMs * 4, 256, 0, s>>>(st[r]->hist.as<uint32_t>() + (size_t)r * pl.cw,
+                                                           st[o]->hist.as<uint32_t>() + (size_t)r * pl.cw, pl.cw);
+          ctx->count();
+        }
     xchg_allgather(ctx, xm, st, &ShardScratch::bagg_z, (size_t)pl.z_slot * pl.ncol * 4);
   }
-  // 3. this rank's merged nonzeros (owner range) from the summed counters
+  // 3. this rank's merged nonzeros (owner range) from the summed counters; every
+  //    rank's counter sum goes into its zero-row record for the cut's count check
   int64_t olo, ohi;
   shard_owner_range(pl.eta, R, W, &olo, &ohi);
   const int64_t own = ohi - olo;
   md.ord.ensure((size_t)std::max<int64_t>(std::min(p, own), 1) * 4);
   md.cnt.ensure((size_t)std::max<int64_t>(std::min(p, own), 1));
   long long* sc = sh.scal.as<long long>();
-  merged_compact(ctx, &md, sh.hist.as<uint32_t>() + (size_t)R * pl.cw, (uint32_t)olo, own,
-                 sh.ocnt.as<unsigned long long>() + R, sc);
+  merged_compact(ctx, &md, sh.hist.as<uint32_t>() + (size_t)R * pl.cw, (uint32_t)olo, own, nullptr, sc,
+                 reinterpret_cast<unsigned long long*>(sh.zrec.as<long long>() + kZrec * R + 2));
+  for (int r = 0; r < W; ++r) {
+    if (r == R || !st[r]) continue;
+    int64_t lo, hi;
+    shard_owner_range(pl.eta, r, W, &lo, &hi);
+    const int64_t nwords = (hi - lo + 7) / 8;
+    const int64_t hblocks = std::max<int64_t>(1, (nwords + (int64_t)kHistWordsPerThread * kScanThreads - 1) /
+                                                     ((int64_t)kHistWordsPerThread * kScanThreads));
+    st[r]->zcount.ensure((size_t)hblocks * 4);
+    k_hist_count<<<(unsigned)hblocks, kScanThreads, 0, s>>>(
+        st[r]->hist.as<uint32_t>() + (size_t)r * pl.cw, nwords, st[r]->zcount.as<uint32_t>(),
+        reinterpret_cast<unsigned long long*>(st[r]->zrec.as<long long>() + kZrec * r + 2));
+    ctx->count();
+  }
   // 4. zero rows -> all-gather the (misses, rows) records -> the cut
   for (int r = 0; r < W; ++r)
     if (st[r]) phase_zero(ctx, pl, *st[r], r, X);
-  xchg_allgather(ctx, xm, st, &ShardScratch::zrec, 16);
+  xchg_allgather(ctx, xm, st, &ShardScratch::zrec, kZrec * 8);
   k_zshard_cut<<<1, kScanThreads, 0, s>>>(sh.zrec.as<long long>(), W, R, q, (long long)budget, sc + 9,
                                           sh.zcount.as<uint32_t>(), sh.zoff.as<long long>(), pl.lzblocks,
                                           sh.miss.as<uint8_t>(), pl.lrows_max, sc + 8, sc + 4, sc + 1, p, code,
-                                          ctx->flags.as<DevFlags>());
+                                          xm == XMode::replicate ? 0 : 1, ctx->flags.as<DevFlags>());
   ctx->count();
   check_launch();
   DrawOut out;

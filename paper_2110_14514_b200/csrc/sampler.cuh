@@ -47,16 +47,15 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
 // and element offset, the nonzero stratum's end word), its draws are histogrammed
 // into nibble counters over all ordinals that are reduce-scattered to the
 // ordinal owners (uint32 sums of packed nibbles are nibble sums while no counter
-// wraps, which the count check certifies), and its zero candidate rows (the rows
-// that start in its element range) are probed locally; an all-gather of the
-// per-rank (misses, rows) locates the q-th miss.  One rank's device state:
+// wraps: the owners' counter sums must add up to p), and its zero candidate rows
+// (the rows that start in its element range) are probed locally; an all-gather
+// of the per-rank (misses, rows, counter sum) locates the q-th miss.  One rank's device state:
 struct ShardScratch {
   DevBuf tm_nz, tm_z;      // own tiles' chunk maps
   DevBuf bagg_nz, bagg_z;  // per-tile aggregate maps, world x slot tiles (all-gathered)
   DevBuf bst_nz, bst_z;    // per-tile start (column, element) of every tile
   DevBuf hist;             // world x cw nibble words (chunk r: owner r's ordinals after the reduce-scatter)
-  DevBuf ocnt;             // world uint64: this rank's draws per owner range (all-reduced)
-  DevBuf zrec;             // world x 2 int64: (misses, rows) of every rank's zero rows (all-gathered)
+  DevBuf zrec;             // world x 3 int64: (zero-row misses, zero rows, counter sum) per rank (all-gathered)
   DevBuf scal;             // 16 int64 scalars
   DevBuf cand, miss, zcount, zoff;  // this rank's zero candidate rows [rows x ndim], hit bits, miss scan
 };
