@@ -98,9 +98,10 @@ struct Slice {
   DevBuf records;           // nnz * rec_ints int32
   DevBuf hash;              // table_size uint64 linear keys, ~0 = empty
   uint64_t table_mask = 0;
-  // Prefilter for large slices: one bit per filter_bit(mix64(key)); a clear bit
-  // proves absence without touching the (DRAM-resident) table.  <= 32 MB so it
-  // stays in L2 while the zero candidates are probed.
+  // Prefilter for large slices: a word-blocked Bloom filter (hash.cuh
+  // filter_may_contain); a clear bit proves absence without touching the
+  // (DRAM-resident) table.  <= 64 MB so it stays in L2 while the zero candidates
+  // are probed.
   DevBuf filter;
   uint64_t filter_mask = 0;  // 0: no prefilter
   uint64_t strides[kMaxModes] = {0};

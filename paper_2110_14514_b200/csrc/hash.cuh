@@ -37,9 +37,19 @@ __device__ __forceinline__ bool hash_insert(unsigned long long* table, uint64_t 
   }
 }
 
-// Bit of the membership prefilter (a one-hash Bloom bitmap over the same keys):
-// the high half of the mixed key, independent of the table's low-bit slot.
-__device__ __forceinline__ uint64_t filter_bit(uint64_t h, uint64_t fmask) { return (h >> 32) & fmask; }
+// Membership prefilter: a word-blocked Bloom filter over the same keys -- the
+// high half of the mixed key picks one 32-bit word, its low 15 bits set three
+// bits in that word (one load per probe; a clear bit proves absence).  fmask =
+// filter bits - 1.
+__device__ __forceinline__ uint64_t filter_word(uint64_t h, uint64_t fmask) { return (h >> 32) & (fmask >> 5); }
+__device__ __forceinline__ uint32_t filter_bits(uint64_t h) {
+  return (1u << (h & 31)) | (1u << ((h >> 5) & 31)) | (1u << ((h >> 10) & 31));
+}
+__device__ __forceinline__ bool filter_may_contain(const unsigned int* __restrict__ filter, uint64_t fmask,
+                                                   uint64_t h) {
+  const uint32_t b = filter_bits(h);
+  return (__ldg(filter + filter_word(h, fmask)) & b) == b;
+}
 
 __device__ __forceinline__ bool hash_contains(const unsigned long long* __restrict__ table, uint64_t mask,
                                               uint64_t key) {

@@ -489,10 +489,7 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_hits(ZeroSpec zs, const i
     bool present = false;
     if (table) {
       present = true;
-      if (filter) {  // a clear prefilter bit proves absence (L2-resident bitmap)
-        const uint64_t b = filter_bit(mix64(key[j]), fmask);
-        present = (__ldg(filter + (b >> 5)) >> (b & 31)) & 1u;
-      }
+      if (filter) present = filter_may_contain(filter, fmask, mix64(key[j]));  // a clear bit proves absence
       if (present) present = hash_contains(table, mask, key[j]);
     }
     if (!present) bits |= 1u << j;
@@ -584,10 +581,7 @@ __global__ void __launch_bounds__(kScanThreads) k_zero_fused(ZeroSpec zs, int32_
       bool present = false;
       if (table) {
         present = true;
-        if (filter) {
-          const uint64_t b = filter_bit(mix64(key), fmask);
-          present = (__ldg(filter + (b >> 5)) >> (b & 31)) & 1u;
-        }
+        if (filter) present = filter_may_contain(filter, fmask, mix64(key));
         if (present) present = hash_contains(table, mask, key);
       }
       if (present) cand[r * zs.ncol] = -1;  // lazy layout: a hit keeps its slot, flagged
