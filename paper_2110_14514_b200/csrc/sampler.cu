@@ -1072,10 +1072,133 @@ __global__ void __launch_bounds__(kScanThreads) k_draw_fused(StreamSpec sp, cons
   }
 }
 
-// Shared memory of a write pass: the output stage's footprint even in the merged
-// form, which does not use it -- a lean counter pass squeezes in beside the walk
-// kernels and slows them more than it gains (c4: 1414 vs 1392 ms per step at
-// N = 1, 241 vs 230 ms in the N = 8 projection).
+// ---- merged form of the nonzero stratum: one generating pass, then a trim.
+// The counters do not care about element order, so a single pass over the
+// tiles counts every tile's accepted words (for the scan) and histograms them
+// at once; the provisioning slack past element p - 1 (a couple of tiles at
+// slack 1) is then taken back out by k_draw_trim, which re-generates only the
+// tiles from the one holding element p - 1.  Saves the separate counting pass.
+__global__ void __launch_bounds__(kScanThreads) k_draw_count_hist(StreamSpec sp, const long long* w0p,
+                                                                  int64_t nchunks, uint32_t* __restrict__ bagg,
+                                                                  int64_t b0, uint32_t* __restrict__ hist,
+                                                                  uint32_t olo, uint32_t ohi,
+                                                                  unsigned long long* __restrict__ owned) {
+  const int64_t tile = b0 + blockIdx.x;
+  const int64_t chunk = tile * kScanThreads + threadIdx.x;
+  WordGen g = tile_wordgen(sp, w0p, tile);
+  uint32_t cnt = 0, mine = 0;
+  if (chunk < nchunks) {
+    const uint32_t n = sp.n[0], thr = sp.thr[0];
+#pragma unroll 4
+    for (int i = 0; i < kChunkWords; ++i) {
+      const uint64_t prod = (uint64_t)g.next() * n;
+      if ((uint32_t)prod >= thr) {
+        ++cnt;
+        const uint32_t val = (uint32_t)(prod >> 32);
+        if (val >= olo && val < ohi) {
+          const uint32_t o = val - olo;
+          atomicAdd(hist + (o >> 3), 1u << ((o & 7u) << 2));
+          ++mine;
+        }
+      }
+    }
+  }
+  __shared__ uint32_t wsum[kScanThreads / 32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    wsum[threadIdx.x >> 5] = cnt;
+    if (owned && mine) atomicAdd(owned, (unsigned long long)mine);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int j = 0; j < kScanThreads / 32; ++j) t += wsum[j];
+    bagg[tile] = t;
+  }
+}
+
+// Take the accepted words at element >= target out of the counters again, over
+// this caller's tiles [b_lo, b_hi) from the tile holding element target - 1 on
+// (grid-stride over those tiles), and record the end word of element target - 1
+// (end_word nullable).  Nothing to do if the stream fell short of target.
+__global__ void __launch_bounds__(kScanThreads) k_draw_trim(StreamSpec sp, const long long* w0p, int64_t nchunks,
+                                                            const long long* __restrict__ bstart, int64_t nblocks,
+                                                            const long long* __restrict__ total, int64_t target,
+                                                            int64_t b_lo, int64_t b_hi, uint32_t* __restrict__ hist,
+                                                            uint32_t olo, uint32_t ohi,
+                                                            unsigned long long* __restrict__ owned,
+                                                            long long* __restrict__ end_word) {
+  __shared__ long long tb;
+  __shared__ uint32_t wsum[kScanThreads / 32];
+  if (threadIdx.x == 0) {
+    tb = -1;
+    if (target > 0 && *total >= target) {
+      int64_t lo = 0, hi = nblocks - 1;  // last tile whose first element is <= target-1
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (bstart[mid * 2 + 1] <= target - 1) lo = mid;
+        else hi = mid - 1;
+      }
+      tb = lo;
+    }
+  }
+  __syncthreads();
+  if (tb < 0) return;
+  const uint32_t n = sp.n[0], thr = sp.thr[0];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t tile = max((int64_t)tb, b_lo) + blockIdx.x; tile < b_hi; tile += gridDim.x) {
+    const int64_t chunk = tile * kScanThreads + threadIdx.x;
+    WordGen g = tile_wordgen(sp, w0p, tile);
+    WordGen g0 = g;
+    uint32_t cnt = 0;
+    if (chunk < nchunks)
+      for (int i = 0; i < kChunkWords; ++i)
+        if ((uint32_t)((uint64_t)g.next() * n) >= thr) ++cnt;
+    uint32_t inc = cnt;  // block exclusive scan of the chunk counts
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += o;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int j = 0; j < w; ++j) pre += wsum[j];
+    __syncthreads();
+    long long e = bstart[tile * 2 + 1] + pre + inc - cnt;
+    uint32_t back = 0;
+    if (chunk < nchunks && e + cnt > target - 1) {
+      uint64_t wi = tile_word0(w0p, tile) + (uint64_t)threadIdx.x * kChunkWords;
+      for (int i = 0; i < kChunkWords; ++i, ++wi) {
+        const uint64_t prod = (uint64_t)g0.next() * n;
+        if ((uint32_t)prod < thr) continue;
+        if (e == target - 1 && end_word) *end_word = (long long)(wi + 1);
+        if (e >= target) {
+          const uint32_t val = (uint32_t)(prod >> 32);
+          if (val >= olo && val < ohi) {
+            const uint32_t o = val - olo;
+            atomicSub(hist + (o >> 3), 1u << ((o & 7u) << 2));
+            ++back;
+          }
+        }
+        ++e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) back += __shfl_xor_sync(0xffffffffu, back, o);
+    if (lane == 0 && back && owned) atomicAdd(owned, (unsigned long long)(-(long long)back));
+  }
+}
+
+// Shared memory of a write / counter pass: the output stage's footprint even in
+// the merged form, which does not use it -- a lean counter pass squeezes in
+// beside the walk kernels and slows them more than it gains (c4: 1414 vs 1392 ms
+// per step at N = 1, 241 vs 230 ms in the N = 8 projection; the fused counter
+// pass likewise 1394 vs 1376 without the footprint).
 static int draw_stage_smem(bool /*merged_form*/) { return kBlockWords * 4; }
 
 template <int NCOL>
@@ -1302,8 +1425,20 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
         merged->cnt.ensure((size_t)std::max<int64_t>(std::min(p, own), 1));
         OGCP_CUDA(cudaMemsetAsync(merged->hist.ptr, 0, (size_t)std::max<int64_t>(nwords, 1) * 4, s));
         unsigned long long* owned = reinterpret_cast<unsigned long long*>(sc + 9);
-        run_stream<1>(ctx, sp, nullptr, p, words, nullptr, nz_end, nz_avail, scr, merged->hist.as<uint32_t>(), olo,
-                      ohi, owned);
+        // one generating pass (count + counters), the tile scan, the trim of the slack
+        const int64_t nchunks = std::max<int64_t>(1, (words + kChunkWords - 1) / kChunkWords);
+        const int64_t nblocks = (nchunks + kScanThreads - 1) / kScanThreads;
+        scr.bagg.ensure((size_t)nblocks * 4);
+        scr.bstart.ensure((size_t)nblocks * 16);
+        k_draw_count_hist<<<(unsigned)nblocks, kScanThreads, draw_stage_smem(true), s>>>(
+            sp, nullptr, nchunks, scr.bagg.as<uint32_t>(), 0, merged->hist.as<uint32_t>(), olo, ohi, owned);
+        k_draw_scan_tiles<1><<<1, kScanTilesThreads, 0, s>>>(scr.bagg.as<uint32_t>(), nblocks,
+                                                             scr.bstart.as<long long>(), nz_avail);
+        k_draw_trim<<<kNumSMs, kScanThreads, 0, s>>>(sp, nullptr, nchunks, scr.bstart.as<long long>(), nblocks,
+                                                     nz_avail, p, 0, nblocks, merged->hist.as<uint32_t>(), olo, ohi,
+                                                     owned, nz_end);
+        ctx->count(3);
+        check_launch();
         merged_compact(ctx, merged, merged->hist.as<uint32_t>(), olo, own, owned, sc);
       } else {
         // q == 0: nothing follows, so the fused pass reports its own shortfall
@@ -1743,7 +1878,6 @@ ShardPlan shard_plan(const Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, 
 
 void shard_alloc(const ShardPlan& pl, ShardScratch& sh, int d) {
   const int W = pl.world;
-  sh.tm_nz.ensure((size_t)pl.n_slot * kScanThreads);
   sh.tm_z.ensure((size_t)pl.z_slot * kScanThreads * pl.ncol);
   sh.bagg_nz.ensure((size_t)W * pl.n_slot * 4);
   sh.bagg_z.ensure((size_t)W * pl.z_slot * pl.ncol * 4);
@@ -1805,11 +1939,14 @@ void phase_count(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r) {
   cudaStream_t s = ctx->stream;
   OGCP_CUDA(cudaMemsetAsync(sh.scal.ptr, 0, 16 * 8, s));
   OGCP_CUDA(cudaMemsetAsync(sh.zrec.ptr, 0, (size_t)pl.world * kZrec * 8, s));
+  OGCP_CUDA(cudaMemsetAsync(sh.hist.ptr, 0, (size_t)pl.world * pl.cw * 4, s));
   const int64_t b0 = (int64_t)r * pl.n_slot;
   const int64_t nt = std::max<int64_t>(0, std::min(pl.n_slot, pl.n_nblocks - b0));
-  if (nt > 0) {
-    k_draw_count<1><<<(unsigned)nt, kScanThreads, 0, s>>>(pl.spn, nullptr, pl.n_nchunks, sh.tm_nz.as<uint8_t>(),
-                                                          sh.bagg_nz.as<uint32_t>(), b0);
+  if (nt > 0) {  // its tiles' counts and its draws into counters over all ordinals, one pass
+    k_draw_count_hist<<<(unsigned)nt, kScanThreads, draw_stage_smem(true), s>>>(pl.spn, nullptr, pl.n_nchunks,
+                                                                                 sh.bagg_nz.as<uint32_t>(),
+                                                            b0, sh.hist.as<uint32_t>(), 0u, (uint32_t)pl.eta,
+                                                            nullptr);
     ctx->count();
   }
 }
@@ -1824,13 +1961,12 @@ void phase_write(Ctx* ctx, const ShardPlan& pl, ShardScratch& sh, int r) {
   k_draw_locate_end<1><<<1, kScanThreads, 0, s>>>(pl.spn, nullptr, pl.n_nchunks, sh.bst_nz.as<long long>(),
                                                   pl.n_nblocks, sc + 1, pl.p, sc + 0);
   ctx->count(2);
-  OGCP_CUDA(cudaMemsetAsync(sh.hist.ptr, 0, (size_t)pl.world * pl.cw * 4, s));
   const int64_t b0 = (int64_t)r * pl.n_slot;
-  const int64_t nt = std::max<int64_t>(0, std::min(pl.n_slot, pl.n_nblocks - b0));
-  if (nt > 0) {
-    k_draw_write<1><<<(unsigned)nt, kScanThreads, draw_stage_smem(true), s>>>(
-        pl.spn, nullptr, pl.n_nchunks, sh.tm_nz.as<uint8_t>(), sh.bst_nz.as<long long>(), pl.p, nullptr, nullptr,
-        sh.hist.as<uint32_t>(), ctx->flags.as<DevFlags>(), 0u, (uint32_t)pl.eta, nullptr, b0);
+  const int64_t b1 = std::min(b0 + pl.n_slot, pl.n_nblocks);
+  if (b1 > b0) {  // the slack past element p - 1, if in its tiles
+    k_draw_trim<<<4, kScanThreads, 0, s>>>(pl.spn, nullptr, pl.n_nchunks, sh.bst_nz.as<long long>(), pl.n_nblocks,
+                                           sc + 1, pl.p, b0, b1, sh.hist.as<uint32_t>(), 0u, (uint32_t)pl.eta, nullptr,
+                                           nullptr);
     ctx->count();
   }
   zero_tiles_any(ctx, pl, sh, r, /*count=*/true);

@@ -51,7 +51,7 @@ DrawOut draw_enqueue(Ctx* ctx, const Slice* X, const Pcg64& g, int64_t p, int64_
 // (the rows that start in its element range) are probed locally; an all-gather
 // of the per-rank (misses, rows, counter sum) locates the q-th miss.  One rank's device state:
 struct ShardScratch {
-  DevBuf tm_nz, tm_z;      // own tiles' chunk maps
+  DevBuf tm_z;             // own zero-stream tiles' chunk maps
   DevBuf bagg_nz, bagg_z;  // per-tile aggregate maps, world x slot tiles (all-gathered)
   DevBuf bst_nz, bst_z;    // per-tile start (column, element) of every tile
   DevBuf hist;             // world x cw nibble words (chunk r: owner r's ordinals after the reduce-scatter)
