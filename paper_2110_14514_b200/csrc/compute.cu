@@ -1053,12 +1053,92 @@ __global__ void __launch_bounds__(kThreads) k_gram_small(SmallGrams g, int rank,
   }
 }
 
+// Small models with ndim x R^2 <= 1024 whose rows fit in shared memory: every
+// mode's Grams in ONE block of 1024 threads.  All modes' rows are staged in one
+// coalesced pass (a single dependent round trip to L2), thread = (mode, row
+// group, entry) sums its interleaved row group from shared memory, the groups
+// combine in fixed order, and the history coefficients follow from the
+// shared-memory Grams after a block barrier -- no cross-block ticket or
+// grid-wide fence.
+constexpr int kGramOneThreads = 1024;
+constexpr size_t kGramOneRowSmem = 160 * 1024;  // staged rows (floats) at most
+__global__ void __launch_bounds__(kGramOneThreads) k_gram_small_one(SmallGrams g, int ndim, int rank, int ldr,
+                                                                    double* __restrict__ out1,
+                                                                    double* __restrict__ out2, CoeffTail tail) {
+  extern __shared__ float rs[];  // per mode: A [rows x ldr], B1, B2 (if any)
+  __shared__ double red1[kGramOneThreads], red2[kGramOneThreads];
+  __shared__ double P[kGramOneThreads], C[kGramOneThreads];
+  const int RR = rank * rank;
+  const int groups = max(1, min(kGramOneThreads / (ndim * RR), 64));
+  const int t = threadIdx.x;
+  const bool B2 = g.B2[0] != nullptr;
+  const int nmat = B2 ? 3 : 2;
+  int64_t off[kMaxModes];
+  int64_t o = 0;
+  for (int k = 0; k < ndim; ++k) {
+    off[k] = o;
+    const int64_t n = g.rows[k] * ldr;
+    for (int64_t x = t; x < n; x += blockDim.x) {
+      rs[o + x] = __ldg(g.A[k] + x);
+      rs[o + n + x] = __ldg(g.B1[k] + x);
+      if (B2) rs[o + 2 * n + x] = __ldg(g.B2[k] + x);
+    }
+    o += nmat * n;
+  }
+  __syncthreads();
+  const int e = t % RR, kg = t / RR, k = kg / groups, grp = kg % groups;
+  const int i = e / rank, j = e % rank;
+  double s1 = 0.0, s2 = 0.0;
+  if (k < ndim) {
+    const int64_t rows = g.rows[k], n = rows * ldr;
+    const float* A = rs + off[k];
+    const float* B1 = A + n;
+    const float* Bo = A + 2 * n;
+    for (int64_t r = grp; r < rows; r += groups) {
+      const double a = A[r * ldr + j];
+      s1 += (double)B1[r * ldr + i] * a;
+      if (B2) s2 += (double)Bo[r * ldr + i] * a;
+    }
+  }
+  red1[t] = s1;
+  red2[t] = s2;
+  __syncthreads();
+  if (t < ndim * RR) {
+    const int kk = t / RR, ee = t % RR;
+    double a1 = 0.0, a2 = 0.0;
+    for (int q = 0; q < groups; ++q) {
+      a1 += red1[(kk * groups + q) * RR + ee];
+      a2 += red2[(kk * groups + q) * RR + ee];
+    }
+    P[t] = a1;
+    C[t] = a2;
+    out1[t] = a1;
+    if (B2) out2[t] = a2;
+  }
+  if (tail.ticket) {  // every mode's history coefficients (k_hist_coeffs' arithmetic)
+    __syncthreads();
+    hist_coeffs_body(ndim, rank, P, B2 ? C : nullptr, tail.S, tail.w, tail.s, tail.extra, tail.Mk, tail.Nk);
+  }
+}
+
 void gram_small_enqueue(Ctx* ctx, const SmallGrams& g, int ndim, int rank, int ldr, double* out1, double* out2,
                         const CoeffTail* tail) {
   ProfScope prof_scope(ctx, kProfGram);
   CoeffTail t{};
   if (tail) t = *tail;
-  k_gram_small<<<dim3(1, ndim), kThreads, 0, ctx->stream>>>(g, rank, ldr, out1, out2, t);
+  size_t rows_bytes = 0;
+  for (int k = 0; k < ndim; ++k) rows_bytes += (size_t)g.rows[k] * ldr * 4 * (g.B2[0] ? 3 : 2);
+  if (ndim * rank * rank <= kGramOneThreads && rows_bytes <= kGramOneRowSmem) {
+    static thread_local bool attr = false;  // static 32 KB + staged rows may pass 48 KB in total
+    if (!attr) {
+      OGCP_CUDA(cudaFuncSetAttribute(k_gram_small_one, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kGramOneRowSmem));
+      attr = true;
+    }
+    k_gram_small_one<<<1, kGramOneThreads, rows_bytes, ctx->stream>>>(g, ndim, rank, ldr, out1, out2, t);
+  } else {
+    k_gram_small<<<dim3(1, ndim), kThreads, 0, ctx->stream>>>(g, rank, ldr, out1, out2, t);
+  }
   ctx->count();
   check_launch();
 }
