@@ -293,3 +293,26 @@ def test_gradient_tensor_large_merge_vs_oracle():
     _, ys, yv = O.sampled_y(O.Slice(dims, subs0, vals), A, w, "poisson", 600_000, 200_000, O.keyed_rng(2, 9, 3, 1, 4))
     np.testing.assert_array_equal(Y.subs0, ys)
     assert rel_err(Y.vals, yv) < GRAD_RTOL
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "poisson", "bernoulli"])
+def test_global_loss_vs_oracle(kind):
+    """global_loss (metrics.py:73-92): the average over the stream's slices of the exact
+    local loss of [[s_t; final factors]] -- every cell, zeros included, over ||X_t||^2 --
+    against the oracle's exact_local_loss (metrics.py:50-57) slice by slice."""
+    rng = np.random.default_rng(11)
+    dims, R, T = (14, 9, 6), 4, 3
+    factors = [rng.uniform(0.2, 1.0, (d, R)) for d in dims]
+    weights_log = [rng.uniform(0.5, 1.5, R) for _ in range(T)]
+    slices, want = [], []
+    for t in range(T):
+        lin = rng.choice(int(np.prod(dims)), size=150, replace=False)
+        subs0 = np.array(np.unravel_index(np.sort(lin), dims)).T
+        vals = (np.ones(lin.size) if kind == "bernoulli" else
+                rng.integers(1, 5, size=lin.size).astype(float) if kind == "poisson" else rng.normal(size=lin.size))
+        slices.append(P.SparseTensor.from_zero_based(dims, subs0, vals))
+        want.append(O.exact_local_loss(O.Slice(dims, subs0, vals), factors, weights_log[t], kind))
+    got = P.global_loss(slices, factors, weights_log, P.make_loss(kind))
+    assert got == pytest.approx(float(np.mean(want)), rel=1e-5)
+    with pytest.raises(P.DataError):
+        P.global_loss(slices, factors, weights_log[:1], P.make_loss(kind))
