@@ -349,6 +349,8 @@ def main():
     if os.environ.get("OGCP_TMA"):  # A/B knob for the TMA-fed 3-way walks (0 off, 1 on, 2 + A2 residency, 3 + weight walk)
         _lib.set_tma_walks(os.environ["OGCP_TMA"] != "0", wgrad=os.environ["OGCP_TMA"] == "3",
                            a2_resident=os.environ["OGCP_TMA"] == "2")
+    if os.environ.get("OGCP_UMMA_GRAM") == "0":  # A/B knob for the tcgen05 Grams (mma.sync instead)
+        _lib.set_umma_gram(False)
     if os.environ.get("OGCP_MERGE") == "0":  # A/B knob for the merged draws
         _lib.set_merge_draws(False)
     loss = P.make_loss("poisson")

@@ -180,9 +180,10 @@ enum { OGCP_OPT_MERGE_DRAWS = 1, OGCP_OPT_SPLIT_SCATTER = 2, OGCP_OPT_BUCKETS = 
  * shared-memory copies, groups in turn, fixed-order block and grid sums), so a
  * same-seed stream is bitwise reproducible; large models keep the 16-byte vector
  * reductions (run-to-run differences in the last bits). */
-/* OGCP_OPT_UMMA_GRAM (default 1): history Grams of factors with ldr 64 / 128 on
- * the tcgen05 tensor cores with TMEM accumulators (csrc/gram_umma.cuh); 0 keeps
- * the mma.sync split-TF32 kernel. */
+/* OGCP_OPT_UMMA_GRAM (default 1): history Grams of large factors with ldr 32 / 64 /
+ * 128 on the tcgen05 tensor cores with TMEM accumulators (csrc/gram_umma.cuh;
+ * ldr 32 packs both Grams of two row sub-chunks into one MMA); 0 keeps the
+ * mma.sync split-TF32 kernel. */
 /* OGCP_OPT_BATCH_DRAWS (default 1): small per-draw sample sets (the c1 / c2
  * shapes) -- all tau draws of a solver epoch are made at the epoch's start,
  * one launch per sampler pass with one block per draw, instead of one draw

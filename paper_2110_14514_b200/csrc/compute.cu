@@ -2177,6 +2177,29 @@ static CUtensorMap gram_tile_map(const float* A, int64_t rows, int ldr) {
 void gram2_enqueue(Ctx* ctx, const float* A, const float* B, int64_t rows, int rank, int ldr, double* outP,
                    double* outC, DevBuf& scratch) {
   const int ngram = B ? 2 : 1;
+  if (ldr == 32 && ctx->umma_gram && rows > 0) {  // tcgen05 / TMEM, packed 64-row chunks (gram_umma.cuh)
+    const int64_t nchunks = (rows + umma::kRows32 - 1) / umma::kRows32;
+    const int nblk = (int)std::min<int64_t>(nchunks, kNumSMs);
+    scratch.ensure((size_t)2 * nblk * ngram * 32 * 32 * 4);  // two sub-chunk partials per CTA
+    umma::GramMaps maps;
+    maps.a = gram_tile_map(A, rows, ldr);
+    maps.b = B ? gram_tile_map(B, rows, ldr) : maps.a;
+    static thread_local bool attr32 = false;
+    if (!attr32) {
+      OGCP_CUDA(cudaFuncSetAttribute(umma::k_gram_umma32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     umma::kSmem32));
+      attr32 = true;
+    }
+    ProfScope prof_scope(ctx, kProfGram);
+    umma::k_gram_umma32<<<nblk, umma::kThreadsG, umma::kSmem32, ctx->stream>>>(maps, rows, ngram,
+                                                                               scratch.as<float>());
+    ctx->count();
+    k_gram_finalize<float><<<std::max(1, ceil_div_i((int64_t)ngram * rank * rank, 32)), 256, 0, ctx->stream>>>(
+        scratch.as<float>(), 2 * nblk, ngram, ldr, rank, outP, outC);
+    ctx->count();
+    check_launch();
+    return;
+  }
   if ((ldr == 64 || ldr == 128) && ctx->umma_gram && rows > 0) {  // tcgen05 / TMEM path (gram_umma.cuh)
     const int64_t nchunks = (rows + umma::kRows - 1) / umma::kRows;
     const int nblk = (int)std::min<int64_t>(nchunks, kNumSMs);

@@ -1,5 +1,6 @@
 // K4 on the 5th-generation tensor cores (tcgen05 / TMEM, sm_100a): the history
 // Grams P = A'A and C = B'A (B = A_old) of a factor matrix with ldr 64 / 128
+// (k_gram_umma) and ldr 32 (k_gram_umma32, below)
 // (reference gram kernels.py:75-98, _add_reg_and_history
 // solvers.py:159-179).  Included by compute.cu.
 //
@@ -254,6 +255,194 @@ __global__ void __launch_bounds__(kThreadsG, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// ldr 32.  A 128-row transposed tile holds four 32-row operands, so one MMA can
+// serve two 32-row sub-chunks of rows and both Grams: X = [A1'; A2'; B1'; B2']
+// (sub-chunks 1, 2 of a 64-row chunk), Y = X rows 0-63 = [A1'; A2'] read as the
+// N = 64 x K operand, and D[128 x 64] = X Y' holds A1'A1 (lanes 0-31, columns
+// 0-31), A2'A2 (lanes 32-63, columns 32-63), B1'A1 (lanes 64-95, columns 0-31)
+// and B2'A2 (lanes 96-127, columns 32-63); the off-diagonal blocks pair rows of
+// different sub-chunks and are never read.  Three split-TF32 MMAs per K-step for
+// 64 rows of both Grams, no zero padding in the tile.  The raw-tile ring is
+// decoupled from the transposed ring: the TMA warp runs kRawRing chunks ahead
+// (64 KB in flight per SM), converters move a chunk into one of kTRing transposed
+// stages and free its raw stage at once, the MMA warp drains the transposed ring.
+// Barriers: rfull / rempty (TMA <-> converters), tfull / tempty (converters <->
+// MMA; tempty by tcgen05.commit).  CTA partials: [2 sub-chunks][ngram][32 x 32].
+constexpr int kRows32 = 64;              // rows per chunk (two 32-row sub-chunks)
+#ifndef OGCP_G32_TRING
+#define OGCP_G32_TRING 4
+#endif
+#ifndef OGCP_G32_RRING
+#define OGCP_G32_RRING 4
+#endif
+constexpr int kRawRing = OGCP_G32_RRING;
+constexpr int kTRing = OGCP_G32_TRING;
+constexpr int kRaw32 = kRows32 * 32 * 4; // one raw [64 x 32] operand tile
+constexpr int kTStage = 2 * kTile;       // X hi, X lo
+constexpr int kSmem32 = kTRing * kTStage + kRawRing * 2 * kRaw32 + 1024 + 512;
+
+__global__ void __launch_bounds__(kThreadsG, 1)
+    k_gram_umma32(const __grid_constant__ GramMaps maps, int64_t rows, int ngram, float* __restrict__ partials) {
+  constexpr int LDR = 32;
+  extern __shared__ __align__(1024) unsigned char g_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(g_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* tbase = sm;                         // kTRing transposed stages (1024-aligned)
+  unsigned char* rbase = sm + kTRing * kTStage;      // kRawRing raw stages
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(rbase + kRawRing * 2 * kRaw32);
+  uint64_t* rempty = rfull + kRawRing;
+  uint64_t* tfull = rempty + kRawRing;
+  uint64_t* tempty = tfull + kTRing;
+  uint64_t* done = tempty + kTRing;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool two = ngram == 2;
+  const int64_t nchunks = (rows + kRows32 - 1) / kRows32;
+  const int64_t G = gridDim.x, bi = blockIdx.x;
+  const int64_t my = nchunks > bi ? (nchunks - bi + G - 1) / G : 0;
+  auto raw = [&](int s, int t) { return rbase + (2 * s + t) * kRaw32; };
+  auto tx = [&](int j, int lo) { return tbase + j * kTStage + lo * kTile; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRawRing; ++s) {
+      bar_init(rfull + s, 1);
+      bar_init(rempty + s, 8);
+    }
+    for (int j = 0; j < kTRing; ++j) {
+      bar_init(tfull + j, 8);
+      bar_init(tempty + j, 1);
+    }
+    bar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (!two) {  // no second operand: rows 64-127 of every X tile stay zero
+    for (int j = 0; j < kTRing; ++j)
+      for (int lo = 0; lo < 2; ++lo) {
+        float4* z = reinterpret_cast<float4*>(tx(j, lo) + 64 * 128);
+        for (int e = threadIdx.x; e < 64 * 128 / 16; e += blockDim.x) z[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+  }
+  if (warp == 1) {  // TMEM: D[128 x 64] in columns [0, 64)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(su32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      for (int64_t k = 0; k < my; ++k) {
+        const int s = (int)(k % kRawRing);
+        const int64_t u = k / kRawRing;
+        if (u > 0) bar_wait(rempty + s, (unsigned)((u - 1) & 1));
+        const int r0 = (int)((bi + k * G) * kRows32);
+        bar_arrive_tx(rfull + s, (unsigned)(kRows32 * LDR * 4 * (two ? 2 : 1)));
+        for (int h = 0; h < 2; ++h) {  // two {32 x 32-row} boxes per operand
+          tma_box(raw(s, 0) + h * kRows * LDR * 4, &maps.a, 0, r0 + h * kRows, rfull + s);
+          if (two) tma_box(raw(s, 1) + h * kRows * LDR * 4, &maps.b, 0, r0 + h * kRows, rfull + s);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(64);
+      for (int64_t k = 0; k < my; ++k) {
+        const int j = (int)(k % kTRing);
+        bar_wait(tfull + j, (unsigned)((k / kTRing) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t xhi = su32(tx(j, 0)), xlo = su32(tx(j, 1));
+#pragma unroll
+        for (int g = 0; g < kRows / 8; ++g) {
+          const uint32_t o = g * 32;  // K-step of 8 tf32 = 32 bytes inside the 128-byte swizzle atom
+          const uint32_t acc = (k > 0 || g > 0) ? 1u : 0u;
+          // D += Xhi Yhi + Xhi Ylo + Xlo Yhi, Y = rows 0-63 of X
+          mma_tf32(tmem, k_desc(xhi + o), k_desc(xhi + o), idesc, acc);
+          mma_tf32(tmem, k_desc(xhi + o), k_desc(xlo + o), idesc, 1u);
+          mma_tf32(tmem, k_desc(xlo + o), k_desc(xhi + o), idesc, 1u);
+        }
+        mma_commit(tempty + j);  // the transposed stage may be rewritten once these MMAs have read it
+      }
+      mma_commit(done);
+    }
+  } else {
+    // ---------------------------------------------------------------- converters (warps 2-9)
+    // thread -> (k4, i): for sub-chunk h and operand t, rows 4 k4 .. 4 k4 + 3 of
+    // column i -> one 16-byte swizzled chunk of X hi / lo in row 64 t + 32 h + i
+    const int ct = threadIdx.x - 64;
+    const int k4 = ct >> 5, i = ct & 31;
+    for (int64_t k = 0; k < my; ++k) {
+      const int s = (int)(k % kRawRing), j = (int)(k % kTRing);
+      bar_wait(rfull + s, (unsigned)((k / kRawRing) & 1));
+      float v[2][2][4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (t == 1 && !two) break;
+        const float* x = reinterpret_cast<const float*>(raw(s, t));
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[t][h][q] = x[(32 * h + 4 * k4 + q) * LDR + i];
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive(rempty + s);  // the raw stage is in registers: the TMA may refill it
+      if (k >= kTRing) bar_wait(tempty + j, (unsigned)(((k / kTRing) - 1) & 1));
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (t == 1 && !two) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float4 hv, lv;
+          hv.x = rna_tf32(v[t][h][0]); lv.x = rna_tf32(v[t][h][0] - hv.x);
+          hv.y = rna_tf32(v[t][h][1]); lv.y = rna_tf32(v[t][h][1] - hv.y);
+          hv.z = rna_tf32(v[t][h][2]); lv.z = rna_tf32(v[t][h][2] - hv.z);
+          hv.w = rna_tf32(v[t][h][3]); lv.w = rna_tf32(v[t][h][3] - hv.w);
+          const uint32_t off = swz(64 * t + 32 * h + i, 4 * k4);
+          *reinterpret_cast<float4*>(tx(j, 0) + off) = hv;
+          *reinterpret_cast<float4*>(tx(j, 1) + off) = lv;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(tfull + j);
+    }
+    if (warp < 6) {  // warps 2-5: TMEM lane quadrant q = warp % 4 holds sub-chunk q % 2 of gram q / 2
+      const int q = warp & 3;
+      const int sub = q & 1, gsel = q >> 1;
+      if (gsel < ngram) {
+        bar_wait(done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * sub);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float4* out = reinterpret_cast<float4*>(partials + (((int64_t)bi * 2 + sub) * ngram + gsel) * LDR * LDR +
+                                                (int64_t)lane * LDR);
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          out[jj] = my > 0 ? make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
+                                         __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
 }
 
 }  // namespace umma

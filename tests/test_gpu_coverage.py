@@ -287,6 +287,29 @@ def test_tensor_core_grams_vs_oracle(R, umma):
 
 
 
+@pytest.mark.parametrize("umma", [True, False])
+@pytest.mark.parametrize("R", [20, 32])
+def test_ldr32_grams_vs_oracle(R, umma):
+    """ldr 32 (the c4 rank): the tcgen05 Gram with its decoupled raw-tile ring
+    (k_gram_umma32) and the mma.sync kernel against fp64 numpy.  Mode 0 past the
+    small-model size (5000 rows) so the Grams take the large-model path; 257 and
+    40 rows cover a ragged tail chunk and a single partial chunk."""
+    from paper_2110_14514_b200 import _lib
+    rng = np.random.default_rng(R)
+    dims = (5000, 257, 40)
+    A = [rng.uniform(-1, 1, (d, R)) for d in dims]
+    B = [a + 0.1 * rng.uniform(-1, 1, a.shape) for a in A]
+    _lib.set_umma_gram(umma)
+    try:
+        for mode in (None, 1):
+            g, want = P.gram(A, mode), O.hadamard_gram(A, mode)
+            assert rel_err(g, want) < 1e-5
+            np.testing.assert_allclose(np.diag(g), np.diag(want), rtol=1e-5)
+            assert rel_err(P.gram(A, mode, other_factors=B), O.hadamard_gram(A, mode, B)) < 1e-5
+    finally:
+        _lib.set_umma_gram(True)
+
+
 def test_tcgen05_gram_at_c5_scale():
     """The tcgen05 / TMEM Gram at the c5 shape (100K rows, ldr 128: 3125 32-row chunks over
     148 CTAs) against the mma.sync kernel and fp64 numpy (norm-wise 1e-5)."""
